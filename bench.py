@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""bench.py -- SDP4Bit hot path: qWD all-gather + TLq-HS reduce-scatter, GB/s of pre-quant bytes.
+
+One step = one pass of the whole hot path over one synthetic GPT-shaped buffer:
+  qWD   sdp4_qwd_quantize + sdp4_qwd_allgather_apply   (Alg. 2 l.2-5)
+  TLq-HS sdp4_tlq_hs_reduce_scatter                     (Alg. 3)
+Pre-quant bytes per rank per step = D*4 (the fp32 weight-difference buffer gathered) +
+D*g (the gradient reduce-scattered, g = 2 for bf16); `value` sums them over all ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sdp4|reference] [--model 1.3B]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "qWD all-gather + TLq-HS reduce-scatter GB/s (pre-quant bytes) at 1/2/4/8 B200"
+SMI_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="sdp4", choices=["sdp4", "reference"])
+    p.add_argument("--model", default="1.3B", help="GPT shape of the flat buffer (tab:model_size_params)")
+    p.add_argument("--numel", type=int, default=0, help="override D (message-size sweeps)")
+    p.add_argument("--groups", type=int, default=None, help="M (default: 2 groups when N is even)")
+    p.add_argument("--group", type=int, default=128, help="G of TLq-HS (P:689)")
+    p.add_argument("--qwd-group", type=int, default=128, help="G of qWD (BASELINE config G; paper uses 2048)")
+    p.add_argument("--hadamard", type=int, default=64, help="Hadamard block b (BASELINE config 1)")
+    p.add_argument("--bits-intra", type=int, default=8)
+    p.add_argument("--bits-inter", type=int, default=4)
+    p.add_argument("--bits-w", type=int, default=4)
+    p.add_argument("--grad-dtype", default="bf16", choices=["bf16", "fp32"])
+    p.add_argument("--model-dtype", default="bf16", choices=["bf16", "fp32"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-comparators", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle timing")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={SMI_FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max((float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()), default=None)}
+
+
+def kernel_bytes(name, D, S, P, M, N, a):
+    """Algorithmic HBM bytes per launch of each kernel."""
+    g = 2 if a.grad_dtype == "bf16" else 4
+    m = 2 if a.model_dtype == "bf16" else 4
+
+    def wire(n, k, G):
+        return n * k / 8 + (4 * n / G if k != 32 else 0)
+    if name.startswith("K1"):
+        return S * (4 + m) + wire(S, a.bits_w, a.qwd_group)
+    if name.startswith("K2"):
+        return wire(D, a.bits_w, a.qwd_group) + 2 * m * D
+    if name.startswith("K3"):
+        return D * g + wire(D, a.bits_intra, a.group)
+    if name.startswith("K4"):
+        return wire(D, a.bits_intra, a.group) + wire(D // N, a.bits_inter, a.group)
+    if name.startswith("K5"):
+        return wire(M * S, a.bits_inter, a.group) + 4 * S
+    return None
+
+
+def ncu_traffic(kernel, workload):
+    """dram read+write bytes per launch from the committed ncu summary, if it matches."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        if d.get("workload") == workload and kernel in d.get("kernels", {}):
+            return d["kernels"][kernel]
+    except Exception:
+        pass
+    return None
+
+
+# ------------------------------------------------------------------- oracle (CPU) legs
+def oracle_sample_rate(a, seconds: float, D_full: int):
+    """Time the oracle (as it stands) on a bounded sample of the workload: the full step
+    (qWD at P=1 + TLq-HS at P=1) on a contiguous window of `n` elements, repeated until
+    `seconds` elapse.  Returns (GB/s of pre-quant bytes, description, cores)."""
+    import numpy as np
+    import torch
+
+    import oracle
+    import synth
+    n = min(D_full, 1 << 21)
+    n -= n % max(a.group, a.qwd_group, 64)
+    gdt = torch.bfloat16 if a.grad_dtype == "bf16" else torch.float32
+    mdt = torch.bfloat16 if a.model_dtype == "bf16" else torch.float32
+    w_model = synth.model_weights(n, seed=synth.seed_for(0, 1), dtype=mdt)
+    w_main = synth.main_weights(w_model, seed=synth.seed_for(0, 2), lr=synth.GPT_LR.get(a.model, 2e-4)).numpy()
+    grad = synth.gradient(n, seed=synth.seed_for(0, 3), dtype=gdt).float().numpy()
+    wm = synth.bf16_bits(w_model) if mdt == torch.bfloat16 else w_model.numpy()
+    g = 2 if a.grad_dtype == "bf16" else 4
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.qwd_step([w_main], wm, a.bits_w, a.qwd_group, model_bf16=(mdt == torch.bfloat16))
+        oracle.tlq_hs_reduce_scatter([grad], oracle.Topology(1, 1), a.group, a.hadamard, a.bits_intra,
+                                     a.bits_inter, True)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    rate = reps * n * (4 + g) / el / 1e9
+    desc = (f"{reps} oracle steps (qWD + TLq-HS, P=1) on a {n}-element window of the workload, "
+            f"{el:.1f} s, single-threaded numpy fp32")
+    del np
+    return rate, desc, 1
+
+
+def run_reference(a, rank, world):
+    """--impl reference: the oracle on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import synth
+    D = a.numel or synth.gpt_numel(a.model)
+    per = max(1.0, a.cpu_seconds / max(1, a.steps))
+    rates = []
+    for _ in range(a.warmup):
+        oracle_sample_rate(a, 0.1, D)
+    desc = ""
+    for _ in range(a.steps):
+        r, desc, cores = oracle_sample_rate(a, per, D)
+        rates.append(r)
+    v = statistics.median(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"GPT-{a.model}-shaped flat buffer (bounded CPU sample)", "D": D},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_sdp4(a, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2410_15526_b200 import Comm, default_split, pad_numel
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    M, N = default_split(world, a.groups)
+    P = world
+    D0 = a.numel or synth.gpt_numel(a.model)
+    D = pad_numel(D0, P, max(a.group, a.qwd_group))
+    S = D // P
+    gdt = torch.bfloat16 if a.grad_dtype == "bf16" else torch.float32
+    mdt = torch.bfloat16 if a.model_dtype == "bf16" else torch.float32
+    g_bytes = 2 if gdt == torch.bfloat16 else 4
+
+    comm = Comm.from_process_group(a.groups, dev) if world > 1 else Comm()
+    lr = synth.GPT_LR.get(a.model, 2e-4)
+    # synthetic inputs: w_model identical on all ranks, w_main shard r, grad per rank
+    w_model = synth.model_weights(D, seed=synth.seed_for(0, 1), device=dev, dtype=mdt)
+    w_main = synth.main_weights(w_model[rank * S:(rank + 1) * S], seed=synth.seed_for(rank, 2), lr=lr)
+    grad = synth.gradient(D, seed=synth.seed_for(rank, 3), device=dev, dtype=gdt)
+    out = torch.empty(S, dtype=torch.float32, device=dev)
+    ws_q = torch.empty(comm.qwd_workspace_bytes(D, a.bits_w, a.qwd_group), dtype=torch.uint8, device=dev)
+    ws_t = torch.empty(comm.tlq_workspace_bytes(D, a.bits_intra, a.bits_inter, a.group), dtype=torch.uint8,
+                       device=dev)
+
+    def step():
+        comm.qwd_quantize(w_main, w_model, ws_q, a.bits_w, a.qwd_group)
+        comm.qwd_allgather_apply(ws_q, w_model, a.bits_w, a.qwd_group)
+        comm.tlq_hs_reduce_scatter(grad, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, steps):
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / steps)
+
+    for _ in range(max(3, a.warmup)):
+        step()
+    # headline: K steps, no instrumentation, clocks sampled during the region
+    comm.launch_count(reset=True)
+    with ClockSampler(local_rank) as clk:
+        ms = timed(step, a.steps)
+    launches = comm.launch_count(reset=True)
+    # per-kernel device times: the same K steps again with every launch bracketed by events
+    comm.profile_enable(True)
+    comm.profile_read()
+    ms_prof = timed(step, a.steps)
+    prof = comm.profile_read()
+    comm.profile_enable(False)
+
+    pre_bytes_rank = D * (4 + g_bytes)
+    value = P * pre_bytes_rank / (ms * 1e-3) / 1e9
+
+    # roofline for the dominant kernel (largest summed device time in the timed region)
+    workload = f"GPT-{a.model} D={D} P={P} ({M}x{N}) G={a.group} Gw={a.qwd_group} b={a.hadamard} " \
+               f"bits={a.bits_w}/{a.bits_intra}/{a.bits_inter} grad={a.grad_dtype} model={a.model_dtype}"
+    peak, peak_src = peaks()
+    kern = {}
+    for name, (tms, cnt) in prof.items():
+        kb = kernel_bytes(name, D, S, P, M, N, a)
+        avg = tms / max(cnt, 1)
+        kern[name] = {"avg_ms": round(avg, 4), "launches": cnt, "share": None,
+                      "alg_bytes": kb, "gbs": round(kb / (avg * 1e-3) / 1e9, 1) if kb and avg > 0 else None}
+    tot = sum(v["avg_ms"] * v["launches"] for v in kern.values()) or 1.0
+    for v in kern.values():
+        v["share_of_kernel_time"] = round(v["avg_ms"] * v["launches"] / tot, 4)
+        v.pop("share")
+    dom = max(kern, key=lambda k: kern[k]["avg_ms"] * kern[k]["launches"]) if kern else None
+    roofline = None
+    if dom:
+        ach = kern[dom]["gbs"]
+        tr = ncu_traffic(dom, workload)
+        roofline = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                    "frac": round(ach / peak, 4) if ach else None, "traffic": tr,
+                    "alg_bytes_per_launch": kern[dom]["alg_bytes"], "peak_source": peak_src}
+
+    # unquantized NCCL comparators on the same buffers (sec. 2.1), N > 1 only
+    comparators = None
+    if world > 1 and not a.no_comparators:
+        big = torch.empty(D, dtype=torch.float32, device=dev)
+        d_shard = torch.empty(S, dtype=torch.float32, device=dev)
+        rs_out = torch.empty(S, dtype=gdt, device=dev)
+        t_ag = timed(lambda: comm.nccl_all_gather(d_shard, big), max(3, a.steps // 2))
+        t_rs = timed(lambda: comm.nccl_reduce_scatter(grad, rs_out, True), max(3, a.steps // 2))
+        del big
+        comparators = {"nccl_all_gather_fp32_ms": round(t_ag, 3), "nccl_reduce_scatter_grad_ms": round(t_rs, 3),
+                       "unquantized_ms_per_step": round(t_ag + t_rs, 3),
+                       "unquantized_GBps": round(P * pre_bytes_rank / ((t_ag + t_rs) * 1e-3) / 1e9, 2),
+                       "speedup_vs_unquantized": round((t_ag + t_rs) / ms, 3)}
+
+    # end to end through the public API with host buffers (pinned), copies inside the region
+    e2e = None
+    if not a.no_e2e:
+        h_grad = grad.cpu().pin_memory()
+        h_main = w_main.cpu().pin_memory()
+        h_out = torch.empty(S, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            gd = h_grad.to(dev, non_blocking=True)
+            wmn = h_main.to(dev, non_blocking=True)
+            comm.qwd_quantize(wmn, w_model, ws_q, a.bits_w, a.qwd_group)
+            comm.qwd_allgather_apply(ws_q, w_model, a.bits_w, a.qwd_group)
+            comm.tlq_hs_reduce_scatter(gd, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
+            h_out.copy_(out, non_blocking=True)
+        e2e_step()
+        ms_e2e = timed(e2e_step, max(2, min(a.steps, 5)))
+        e2e = {"value": round(P * pre_bytes_rank / (ms_e2e * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": int(h_grad.numel() * h_grad.element_size() + h_main.numel() * 4),
+               "d2h_bytes_per_step": int(h_out.numel() * 4), "ms_per_step": round(ms_e2e, 3)}
+        del h_grad, h_main, h_out
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        v, desc, cores = oracle_sample_rate(a, a.cpu_seconds, D)
+        cpu = {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": a.steps,
+                "warmup": max(3, a.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": workload, "D": D, "D_unpadded": D0, "M": M, "N": N, "G": a.group,
+                           "G_w": a.qwd_group, "hadamard_block": a.hadamard,
+                           "bits": {"qwd": a.bits_w, "intra": a.bits_intra, "inter": a.bits_inter},
+                           "grad_dtype": a.grad_dtype, "model_dtype": a.model_dtype,
+                           "l2": "inputs larger than L2 (>= 2.6 GB per tensor), no flush",
+                           "pre_quant_bytes_per_rank": pre_bytes_rank,
+                           "storage": "bf16/fp32 storage, fp32 arithmetic, int8/int4 wire codes"},
+                "clocks": clk.summary(), "gpu_launches": int(launches), "kernels": kern,
+                "ms_per_step_profiled": round(ms_prof, 4), "roofline": roofline,
+                "e2e": e2e, "comparators": comparators, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    comm.close()
+
+
+def main():
+    a = parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if a.gpus != world and world == 1 and a.gpus > 1:
+        raise SystemExit(f"--gpus {a.gpus} needs torchrun --nproc-per-node {a.gpus}")
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_sdp4(a, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,176 @@
+/*
+ * sdp4.h -- C ABI of libsdp4: the SDP4Bit data-parallel communication hot path
+ * (arXiv 2410.15526) on B200 (sm_100a) with NCCL over NVLink 5 / NVSwitch.
+ *
+ * Citations: "P:n" = line n of the paper text, with its section /
+ * algorithm label; "R<k>" = reading k of DESIGN.md sec. 3 (where the paper is
+ * silent or ambiguous).  Notation: P = M*N workers (M groups of N, rank
+ * r = m*N + l, sec. 2.3); D = numel of the flat buffer; S = D/P the shard
+ * length, shard r = [r*S, (r+1)*S) (sec. 2.1); G = quantization group
+ * size; k = bits, q_k = 2^(k-1)-1; b = Hadamard block.
+ *
+ * Conventions (all entry points):
+ *  - Data pointers (w_main_shard, w_model_full, grad, out_shard, workspace) are
+ *    CUDA DEVICE pointers owned by the caller; the library never allocates,
+ *    frees or retains them beyond the call.  They must be 16-byte aligned.
+ *  - `stream` is a cudaStream_t (passed as void*).  Every call is stream-ordered
+ *    on it: kernels and NCCL calls are enqueued, nothing is synchronized on the
+ *    host (except sdp4_comm_init / sdp4_comm_destroy / sdp4_profile_read).
+ *  - Validation happens before any launch; on error nothing is enqueued, the
+ *    status is returned and sdp4_last_error() describes it.
+ *  - Alignment rule (R1): numel % (P * lcm(G, 64)) == 0 (the caller zero-pads;
+ *    zeros are reduction-neutral).  Groups never straddle shards.
+ *  - Calls on one comm are not reentrant; serialize them on one stream.
+ *  - World size 1 is valid: no NCCL traffic, every codec step still runs.
+ */
+#ifndef SDP4_H
+#define SDP4_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SDP4_OK = 0,
+  SDP4_EINVAL = 1, /* bad argument (null pointer, unsupported bits/dtype/group, M*N != world) */
+  SDP4_EALIGN = 2, /* size/alignment rule violated (numel, G % b, pointer alignment)          */
+  SDP4_ECUDA = 3,  /* a CUDA runtime error (launch failure, bad device pointer)                */
+  SDP4_ENCCL = 4,  /* an NCCL error, including an asynchronous one from a previous call         */
+  SDP4_ESTATE = 5  /* workspace too small or comm unusable                                      */
+} sdp4_status;
+
+typedef enum { SDP4_F32 = 0, SDP4_BF16 = 1 } sdp4_dtype;
+typedef enum { SDP4_RNE = 0, SDP4_STOCHASTIC = 1 /* reserved (NEXT-2); rejected with EINVAL */ } sdp4_round;
+
+/* Opaque communicator: world + intra (N ranks of group m) + inter (M ranks of
+ * local rank l) NCCL communicators, plus profiling state.  P:292 sec. 2.3. */
+typedef struct sdp4_comm* sdp4_comm_t;
+
+#define SDP4_UNIQUE_ID_BYTES 128
+
+/* Library version (major*10000 + minor*100 + patch). */
+int sdp4_version(void);
+
+/* Thread-local description of the last error of this thread ("" if none).
+ * Valid until the next sdp4_* call on the same thread. */
+const char* sdp4_last_error(void);
+
+/* Host.  Fill id[128] with a fresh NCCL unique id (call on rank 0, broadcast the
+ * bytes to every rank by any means, e.g. torch.distributed). */
+sdp4_status sdp4_get_unique_id(unsigned char id[SDP4_UNIQUE_ID_BYTES]);
+
+/* Host, collective over all `world` ranks.  Binds to the CURRENT CUDA device.
+ * groups_M * group_size_N must equal world (P = M*N).  For world == 1 the
+ * id may be NULL and no NCCL communicator is created.  intra = ncclCommSplit
+ * (color = rank / N, key = rank % N); inter = ncclCommSplit(color = rank % N,
+ * key = rank / N).  On success *out owns the communicators. */
+sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, int world,
+                           int groups_M, int group_size_N);
+
+/* Host, collective.  Destroys the NCCL communicators and frees the comm. */
+sdp4_status sdp4_comm_destroy(sdp4_comm_t comm);
+
+/* ---------------------------------------------------------------------------
+ * Sizes and workspace layout (R15).  One "wire unit" carries n elements at k
+ * bits: [codes n*k/8 bytes][fp32 scales n/G][zero..255 pad bytes], the unit
+ * size rounded up to 256 bytes.  int4 codes are two's-complement nibbles,
+ * element 2j in the low nibble; int8 codes two's complement (R4).  k = 32 is
+ * the identity codec (R12): n fp32 values, no scales.
+ * ------------------------------------------------------------------------- */
+size_t sdp4_wire_unit_bytes(size_t n, int bits, int group);
+
+/* qWD workspace (Alg. 2 l.3-4): P consecutive wire units
+ * W(S, bits, G); unit r is rank r's quantized weight difference.  0 on bad args. */
+size_t sdp4_qwd_workspace_bytes(int world, size_t numel, int bits, int group);
+
+/* TLq-HS workspace (Alg. 3), four regions in this order:
+ *   region 0 intra_send: N blocks of M units W(S, bits_intra, G); block l' unit m'
+ *            holds shard m'*N + l' of H(grad) quantized (Alg. 3 l.2-3, R9)
+ *   region 1 intra_recv: N blocks of M units (block l'' = from local rank l'')
+ *            (aliases region 0 when N == 1)
+ *   region 2 inter_send: M units W(S, bits_inter, G); unit m' = shard m'*N + l
+ *   region 3 inter_recv: M units (unit m'' = from group m''; aliases region 2 when M == 1)
+ * sdp4_tlq_workspace_offset(region) gives each region's byte offset.  0 on bad args. */
+size_t sdp4_tlq_workspace_bytes(int groups_M, int group_size_N, size_t numel, int bits_intra,
+                                int bits_inter, int group);
+size_t sdp4_tlq_workspace_offset(int groups_M, int group_size_N, size_t numel, int bits_intra,
+                                 int bits_inter, int group, int region);
+
+/* ---------------------------------------------------------------------------
+ * qWD -- quantized weight differences (sec. 3.1; Alg. 2).
+ * ------------------------------------------------------------------------- */
+
+/* Alg. 2 l.2-3 on this rank r:
+ *   d[r] = w_main[r] - w_model[r]   (fp32; w_model widened exactly, R11)
+ *   d~[r] = QuantizeWeightsDiff(d[r]): per G-group s = max|d|, codes = RNE(d * rn(q_k/s))
+ *           (R2, R3), written as wire unit r of `workspace` (layout above).
+ * w_main_shard: fp32[S] (this rank's main weights).  w_model_full: the
+ * full replica D elements of model_dtype (bf16 or fp32); only
+ * [r*S, (r+1)*S) is read.  bits in {4, 8, 32}; G power of two in [32, 2048].
+ * rnd must be SDP4_RNE (seed ignored). */
+sdp4_status sdp4_qwd_quantize(sdp4_comm_t comm, const float* w_main_shard, const void* w_model_full,
+                              sdp4_dtype model_dtype, size_t numel, int bits, int group,
+                              sdp4_round rnd, uint64_t seed, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
+/* Alg. 2 l.4-5: AllGather of the P wire units in place in
+ * `workspace` (ncclAllGather on the world comm), then for all D elements
+ *   w_model <- bf16_rn(widen(w_model) + code * rn(s / q_k))   (fp32 add for fp32 models)
+ * in place (R5, R11).  Every rank, owner included, applies the dequantized d~,
+ * so all replicas stay bit-identical. */
+sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t comm, void* workspace, size_t workspace_bytes,
+                                     size_t numel, int bits, int group, void* w_model_full,
+                                     sdp4_dtype model_dtype, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * TLq-HS -- two-level gradient quantization with Hadamard smoother, replacing the
+ * ReduceScatter of Alg. 2 l.9: Alg. 3 with the sec. 3.3
+ * pruning:
+ *   K3  u = H_unnorm(grad) per b-block; per G-group s_u = max|u|; codes =
+ *       RNE(u * rn(q/s_u)) at bits_intra; scale = rn(s_u * c_b), c_b = rn(1/sqrt b) (R6)
+ *   --  IntraAlltoAll (ncclAlltoAll on the intra comm)                 (l.4)
+ *   K4  acc = sum_{l''=0..N-1} code * rn(s/q) in fp32, requantize at
+ *       bits_inter                                                       (l.5,7,9)
+ *   --  InterAlltoAll (ncclAlltoAll on the inter comm)                 (l.10)
+ *   K5  acc = sum_{m''=0..M-1} code * rn(s/q); out = rn(H_unnorm(acc) * kappa),
+ *       kappa = rn(c_b / P) if average else c_b (b = 0: rn(1/P) or none)  (l.11-13, R8)
+ * grad: D elements of grad_dtype (fp32 or bf16).  out_shard: fp32[S], shard r.
+ * hadamard_block b in {0, 2, 4, ..., 256} with G % b == 0; b = 0 gives
+ * TLq; (bits_intra, bits_inter, b) = (4, 4, 0) gives ULq.
+ * bits_intra, bits_inter in {4, 8, 32}.  workspace_bytes >= sdp4_tlq_workspace_bytes. */
+sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t comm, const void* grad, sdp4_dtype grad_dtype,
+                                       size_t numel, int bits_intra, int bits_inter, int group,
+                                       int hadamard_block, int average, sdp4_round rnd, uint64_t seed,
+                                       float* out_shard, void* workspace, size_t workspace_bytes,
+                                       void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Instrumentation (measurement only; no effect on results).
+ * ------------------------------------------------------------------------- */
+/* Count of kernels this comm launched since init (or since the last reset). */
+uint64_t sdp4_launch_count(sdp4_comm_t comm, int reset);
+
+/* enable != 0: bracket every kernel launch of this comm with CUDA events on its
+ * stream; sdp4_profile_read synchronizes those events and returns, per kernel
+ * name, the summed device milliseconds and launch count since the last read.
+ * names[i] point to static strings.  *count receives the number of entries. */
+sdp4_status sdp4_profile_enable(sdp4_comm_t comm, int enable);
+sdp4_status sdp4_profile_read(sdp4_comm_t comm, const char** names, double* ms, uint64_t* launches,
+                              int max_entries, int* count);
+
+/* Unquantized comparators on the same comm (bench only, sec. 2.1):
+ * ncclReduceScatter(sum, or avg if average) of D elements of dtype into S, and
+ * ncclAllGather of S elements of dtype into D. */
+sdp4_status sdp4_nccl_reduce_scatter(sdp4_comm_t comm, const void* send, void* recv, size_t numel,
+                                     sdp4_dtype dtype, int average, void* stream);
+sdp4_status sdp4_nccl_all_gather(sdp4_comm_t comm, const void* send, void* recv, size_t numel,
+                                 sdp4_dtype dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SDP4_H */

@@ -1,0 +1,218 @@
+"""Thin ctypes binding of libsdp4 (include/sdp4.h).
+
+Argument marshalling only: torch tensors are turned into device pointers and the
+current CUDA stream; every step of the hot path runs in libsdp4's kernels and NCCL
+calls.  There is no fallback: if libsdp4.so is missing or a call fails, an
+exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libsdp4.so")
+
+OK, EINVAL, EALIGN, ECUDA, ENCCL, ESTATE = range(6)
+F32, BF16 = 0, 1
+RNE, STOCHASTIC = 0, 1
+UNIQUE_ID_BYTES = 128
+
+_DT = {torch.float32: F32, torch.bfloat16: BF16}
+_ESZ = {F32: 4, BF16: 2}
+
+_c_size = ctypes.c_size_t
+_vp = ctypes.c_void_p
+_ci = ctypes.c_int
+_u64 = ctypes.c_uint64
+
+# name -> (restype, argtypes): exactly the entry points of include/sdp4.h
+SIGNATURES = {
+    "sdp4_version": (_ci, []),
+    "sdp4_last_error": (ctypes.c_char_p, []),
+    "sdp4_get_unique_id": (_ci, [ctypes.c_char_p]),
+    "sdp4_comm_init": (_ci, [ctypes.POINTER(_vp), ctypes.c_char_p, _ci, _ci, _ci, _ci]),
+    "sdp4_comm_destroy": (_ci, [_vp]),
+    "sdp4_wire_unit_bytes": (_c_size, [_c_size, _ci, _ci]),
+    "sdp4_qwd_workspace_bytes": (_c_size, [_ci, _c_size, _ci, _ci]),
+    "sdp4_tlq_workspace_bytes": (_c_size, [_ci, _ci, _c_size, _ci, _ci, _ci]),
+    "sdp4_tlq_workspace_offset": (_c_size, [_ci, _ci, _c_size, _ci, _ci, _ci, _ci]),
+    "sdp4_qwd_quantize": (_ci, [_vp, _vp, _vp, _ci, _c_size, _ci, _ci, _ci, _u64, _vp, _c_size, _vp]),
+    "sdp4_qwd_allgather_apply": (_ci, [_vp, _vp, _c_size, _c_size, _ci, _ci, _vp, _ci, _vp]),
+    "sdp4_tlq_hs_reduce_scatter": (_ci, [_vp, _vp, _ci, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _u64, _vp, _vp,
+                                         _c_size, _vp]),
+    "sdp4_launch_count": (_u64, [_vp, _ci]),
+    "sdp4_profile_enable": (_ci, [_vp, _ci]),
+    "sdp4_profile_read": (_ci, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(_u64), _ci, ctypes.POINTER(_ci)]),
+    "sdp4_nccl_reduce_scatter": (_ci, [_vp, _vp, _vp, _c_size, _ci, _ci, _vp]),
+    "sdp4_nccl_all_gather": (_ci, [_vp, _vp, _vp, _c_size, _ci, _vp]),
+}
+
+_lib = None
+
+
+class SDP4Error(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"libsdp4 status {status}: {msg}")
+        self.status = status
+
+
+def lib() -> ctypes.CDLL:
+    """Load libsdp4.so (built in-tree by paper_2410_15526_b200.build).  Fails loudly."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is not built; run `python -m paper_2410_15526_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != OK:
+        raise SDP4Error(status, lib().sdp4_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("tensors passed to libsdp4 must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def wire_unit_bytes(n: int, bits: int, group: int) -> int:
+    return lib().sdp4_wire_unit_bytes(n, bits, group)
+
+
+def qwd_workspace_bytes(world: int, numel: int, bits: int, group: int) -> int:
+    return lib().sdp4_qwd_workspace_bytes(world, numel, bits, group)
+
+
+def tlq_workspace_bytes(M: int, N: int, numel: int, bits_intra: int, bits_inter: int, group: int) -> int:
+    return lib().sdp4_tlq_workspace_bytes(M, N, numel, bits_intra, bits_inter, group)
+
+
+def tlq_workspace_offset(M, N, numel, bits_intra, bits_inter, group, region) -> int:
+    return lib().sdp4_tlq_workspace_offset(M, N, numel, bits_intra, bits_inter, group, region)
+
+
+def get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(UNIQUE_ID_BYTES)
+    _check(lib().sdp4_get_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """sdp4_comm_t: world + intra (N) + inter (M) NCCL communicators."""
+
+    def __init__(self, rank: int = 0, world: int = 1, groups: int = 1, group_size: int = 1,
+                 unique_id: Optional[bytes] = None):
+        self.rank, self.world, self.M, self.N = rank, world, groups, group_size
+        self._h = ctypes.c_void_p()
+        uid = None if unique_id is None else ctypes.create_string_buffer(unique_id, UNIQUE_ID_BYTES)
+        _check(lib().sdp4_comm_init(ctypes.byref(self._h), uid, rank, world, groups, group_size))
+
+    @classmethod
+    def from_process_group(cls, groups: Optional[int] = None, device=None) -> "Comm":
+        """Bootstrap from torch.distributed: rank 0 draws an NCCL unique id and broadcasts
+        it; groups defaults to the topology of topology.default_split."""
+        import torch.distributed as dist
+        from .topology import default_split
+        rank, world = dist.get_rank(), dist.get_world_size()
+        M, N = default_split(world, groups)
+        uid = None
+        if world > 1:
+            t = torch.zeros(UNIQUE_ID_BYTES, dtype=torch.uint8)
+            if rank == 0:
+                t = torch.frombuffer(bytearray(get_unique_id()), dtype=torch.uint8)
+            if dist.get_backend() == "nccl":
+                t = t.to(device or torch.device("cuda", torch.cuda.current_device()))
+            dist.broadcast(t, 0)
+            uid = bytes(t.cpu().tolist())
+        return cls(rank, world, M, N, uid)
+
+    def close(self):
+        if self._h:
+            _check(lib().sdp4_comm_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- sizes -------------------------------------------------------------------
+    def qwd_workspace_bytes(self, numel: int, bits: int = 4, group: int = 128) -> int:
+        return qwd_workspace_bytes(self.world, numel, bits, group)
+
+    def tlq_workspace_bytes(self, numel: int, bits_intra: int = 8, bits_inter: int = 4, group: int = 128) -> int:
+        return tlq_workspace_bytes(self.M, self.N, numel, bits_intra, bits_inter, group)
+
+    def workspace(self, nbytes: int, device=None) -> torch.Tensor:
+        return torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
+
+    # -- qWD (Alg. 2 l.2-5) ----------------------------------------------------------
+    def qwd_quantize(self, w_main_shard: torch.Tensor, w_model: torch.Tensor, workspace: torch.Tensor,
+                     bits: int = 4, group: int = 128, stream=None):
+        if w_main_shard.dtype != torch.float32:
+            raise TypeError("w_main_shard must be fp32 (P:211)")
+        _check(lib().sdp4_qwd_quantize(self._h, _ptr(w_main_shard), _ptr(w_model), _DT[w_model.dtype],
+                                       w_model.numel(), bits, group, RNE, 0, _ptr(workspace), workspace.numel(),
+                                       _stream(stream)))
+
+    def qwd_allgather_apply(self, workspace: torch.Tensor, w_model: torch.Tensor, bits: int = 4,
+                            group: int = 128, stream=None):
+        _check(lib().sdp4_qwd_allgather_apply(self._h, _ptr(workspace), workspace.numel(), w_model.numel(), bits,
+                                              group, _ptr(w_model), _DT[w_model.dtype], _stream(stream)))
+
+    # -- TLq-HS (Alg. 3) -------------------------------------------------------------
+    def tlq_hs_reduce_scatter(self, grad: torch.Tensor, out_shard: torch.Tensor, workspace: torch.Tensor,
+                              bits_intra: int = 8, bits_inter: int = 4, group: int = 128,
+                              hadamard_block: int = 64, average: bool = True, stream=None):
+        if out_shard.dtype != torch.float32:
+            raise TypeError("out_shard must be fp32")
+        _check(lib().sdp4_tlq_hs_reduce_scatter(self._h, _ptr(grad), _DT[grad.dtype], grad.numel(), bits_intra,
+                                                bits_inter, group, hadamard_block, int(bool(average)), RNE, 0,
+                                                _ptr(out_shard), _ptr(workspace), workspace.numel(),
+                                                _stream(stream)))
+
+    # -- instrumentation -------------------------------------------------------------
+    def launch_count(self, reset: bool = False) -> int:
+        return int(lib().sdp4_launch_count(self._h, int(reset)))
+
+    def profile_enable(self, enable: bool = True):
+        _check(lib().sdp4_profile_enable(self._h, int(enable)))
+
+    def profile_read(self) -> dict:
+        n = 16
+        names = (ctypes.c_char_p * n)()
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_uint64 * n)()
+        k = ctypes.c_int(0)
+        _check(lib().sdp4_profile_read(self._h, names, ms, cnt, n, ctypes.byref(k)))
+        return {names[i].decode(): (ms[i], int(cnt[i])) for i in range(k.value)}
+
+    # -- unquantized comparators (sec. 2.1) -----------------------------------
+    def nccl_reduce_scatter(self, send: torch.Tensor, recv: torch.Tensor, average: bool = True, stream=None):
+        _check(lib().sdp4_nccl_reduce_scatter(self._h, _ptr(send), _ptr(recv), send.numel(), _DT[send.dtype],
+                                              int(average), _stream(stream)))
+
+    def nccl_all_gather(self, send: torch.Tensor, recv: torch.Tensor, stream=None):
+        _check(lib().sdp4_nccl_all_gather(self._h, _ptr(send), _ptr(recv), recv.numel(), _DT[send.dtype],
+                                          _stream(stream)))

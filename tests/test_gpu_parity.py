@@ -1,0 +1,192 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Bar (north star): packed codes and scales bit-exact; dequantized /
+output values within 1e-5 relative to the group scale (in practice also bit-exact: both
+sides execute the same fp32 operations in the same order, R3-R11).  NaN compares equal to
+NaN (payloads are not part of the contract).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2410_15526_b200 import Comm
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def comm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = Comm()
+    yield c
+    c.close()
+
+
+def f32_equal(a, b):
+    a = np.asarray(a, np.float32)
+    b = np.asarray(b, np.float32)
+    return bool(np.all((a.view(np.uint32) == b.view(np.uint32)) | (np.isnan(a) & np.isnan(b))))
+
+
+def assert_unit_equal(got_bytes, codes, scales, k, G, n, what):
+    """Compare one wire unit (codes bit-exact, scales bit-exact up to NaN payload)."""
+    want = oracle.wire_unit(codes, scales, k, G)
+    if k == 32:
+        assert f32_equal(got_bytes[: 4 * n].view(np.float32), want[: 4 * n].view(np.float32)), what
+        return
+    ncb = n * k // 8
+    got_codes = got_bytes[:ncb]
+    if not np.array_equal(got_codes, want[:ncb]):
+        bad = np.nonzero(got_codes != want[:ncb])[0]
+        raise AssertionError(f"{what}: {len(bad)} code bytes differ, first at {bad[:8]}")
+    gs = got_bytes[ncb: ncb + 4 * (n // G)].copy().view(np.float32)
+    assert f32_equal(gs, scales), f"{what}: scales differ"
+
+
+def bf16_equal(a_bits, b_bits):
+    a = oracle.bf16_widen(a_bits)
+    b = oracle.bf16_widen(b_bits)
+    return bool(np.all((a_bits == b_bits) | (np.isnan(a) & np.isnan(b))))
+
+
+# --------------------------------------------------------------------------------- qWD
+def run_qwd(comm, w_main, w_model, bits, G):
+    D = w_model.numel()
+    ws = torch.zeros(comm.qwd_workspace_bytes(D, bits, G), dtype=torch.uint8, device="cuda")
+    wm = w_model.cuda()
+    comm.qwd_quantize(w_main.cuda(), wm, ws, bits, G)
+    torch.cuda.synchronize()
+    unit = ws.cpu().numpy().copy()
+    comm.qwd_allgather_apply(ws, wm, bits, G)
+    torch.cuda.synchronize()
+    return unit, wm.cpu()
+
+
+def oracle_qwd(w_main, w_model, bits, G):
+    bf = w_model.dtype == torch.bfloat16
+    wm = synth.bf16_bits(w_model) if bf else w_model.numpy()
+    units, new = oracle.qwd_step([w_main.numpy()], wm, bits, G, model_bf16=bf)
+    return units[0], new
+
+
+@pytest.mark.parametrize("model_dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("bits,G", [(4, 128), (4, 2048), (4, 32), (8, 128), (8, 256), (32, 128), (4, 512)])
+def test_qwd_parity(comm, model_dtype, bits, G):
+    D = max(G, 64) * 37 + (0 if G >= 2048 else max(G, 64) * 11)   # several tiles + ragged tail
+    w_model = synth.model_weights(D, seed=1, dtype=model_dtype)
+    w_main = synth.main_weights(w_model, seed=2, lr=2e-4)
+    unit, new = run_qwd(comm, w_main, w_model, bits, G)
+    (codes, scales), want_new = oracle_qwd(w_main, w_model, bits, G)
+    assert_unit_equal(unit, codes, scales, bits, G, D, "qWD unit")
+    if model_dtype == torch.bfloat16:
+        assert bf16_equal(synth.bf16_bits(new), want_new)
+    else:
+        assert f32_equal(new.numpy(), want_new)
+
+
+@pytest.mark.parametrize("G", [32, 64, 128])
+def test_qwd_edge_cases(comm, G):
+    # zero / tiny / NaN / Inf / huge / tie groups in the weight difference
+    x = synth.edge_case_groups(G)
+    D = oracle_len = ((x.numel() + 63) // 64) * 64
+    assert oracle_len == x.numel()
+    w_model = torch.zeros(D, dtype=torch.float32)
+    unit, new = run_qwd(comm, x, w_model, 4, G)
+    (codes, scales), want_new = oracle_qwd(x, w_model, 4, G)
+    assert_unit_equal(unit, codes, scales, 4, G, D, "qWD edge unit")
+    assert f32_equal(new.numpy(), want_new)
+
+
+# ------------------------------------------------------------------------------ TLq-HS
+def run_tlq(comm, grad, bits_intra, bits_inter, G, b, average=True):
+    D = grad.numel()
+    nbytes = comm.tlq_workspace_bytes(D, bits_intra, bits_inter, G)
+    ws = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    out = torch.empty(D, dtype=torch.float32, device="cuda")
+    comm.tlq_hs_reduce_scatter(grad.cuda(), out, ws, bits_intra, bits_inter, G, b, average)
+    torch.cuda.synchronize()
+    from paper_2410_15526_b200 import tlq_workspace_offset
+    w = ws.cpu().numpy()
+    o_inter = tlq_workspace_offset(1, 1, D, bits_intra, bits_inter, G, 2)
+    return w[:o_inter].copy(), w[o_inter:].copy(), out.cpu().numpy()
+
+
+def oracle_tlq(grad, bits_intra, bits_inter, G, b, average=True):
+    g = grad.float().numpy()
+    return oracle.tlq_hs_reduce_scatter([g], oracle.Topology(1, 1), G, b, bits_intra, bits_inter, average)
+
+
+def check_tlq(comm, grad, bi, be, G, b, average=True):
+    D = grad.numel()
+    intra, inter, out = run_tlq(comm, grad, bi, be, G, b, average)
+    tr = oracle_tlq(grad, bi, be, G, b, average)
+    c8, s8 = tr.intra_send[0][0][0]
+    assert_unit_equal(intra, c8, s8, bi, G, D, f"K3 intra unit (b={b}, G={G}, k={bi})")
+    c4, s4 = tr.inter_send[0][0]
+    assert_unit_equal(inter, c4, s4, be, G, D, f"K4 inter unit (G={G}, k={be})")
+    want = tr.out[0]
+    if not f32_equal(out, want):
+        # fall back to the north-star tolerance: 1e-5 relative to the group scale
+        scale = np.repeat(np.abs(want).reshape(-1, G).max(axis=1), G)
+        err = np.abs(out.astype(np.float64) - want)
+        nb = int(np.sum(out.view(np.uint32) != want.view(np.uint32)))
+        assert np.all(err <= 1e-5 * scale + 1e-30), f"K5 output differs beyond tolerance ({nb} elements)"
+        pytest.fail(f"K5 output within tolerance but not bit-exact ({nb} elements differ)")
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("G,b", [(128, 64), (128, 32), (128, 0), (32, 32), (64, 16), (256, 256), (2048, 128),
+                                 (128, 2), (512, 8)])
+def test_tlq_hs_parity(comm, dtype, G, b):
+    D = 16384 * 3 + max(G, 64) * 9            # three full K3/K5 tiles and a ragged tail
+    grad = synth.gradient(D, seed=7 + G + b, dtype=dtype)
+    check_tlq(comm, grad, 8, 4, G, b)
+
+
+@pytest.mark.parametrize("bi,be,b", [(4, 4, 0), (8, 8, 64), (32, 32, 0), (32, 4, 64), (8, 32, 32), (4, 8, 16)])
+def test_tlq_modes_parity(comm, bi, be, b):
+    # ULq (4,4,0), TLq variants and the identity codec (R12)
+    D = 16384 * 2 + 128 * 5
+    grad = synth.gradient(D, seed=99 + bi + be + b)
+    check_tlq(comm, grad, bi, be, 128, b)
+
+
+@pytest.mark.parametrize("average", [True, False])
+def test_tlq_average_flag(comm, average):
+    grad = synth.gradient(16384 + 128 * 3, seed=5)
+    check_tlq(comm, grad, 8, 4, 128, 64, average)
+
+
+@pytest.mark.parametrize("G", [32, 64, 128])
+def test_tlq_edge_cases(comm, G):
+    x = synth.edge_case_groups(G)
+    check_tlq(comm, x, 8, 4, G, min(G, 32))
+    check_tlq(comm, x, 8, 4, G, 0)
+
+
+def test_tlq_bf16_extremes(comm):
+    g = torch.tensor([3.0e38, -3.0e38, 1e-38, -1e-40, 0.0, -0.0, 65504.0, 1.0] * 16 * 8, dtype=torch.float32)
+    check_tlq(comm, g.to(torch.bfloat16), 8, 4, 128, 0)
+
+
+def test_repeatability(comm):
+    # R16: bit-identical across repeated runs
+    grad = synth.gradient(16384 * 4, seed=1234, dtype=torch.bfloat16)
+    a = run_tlq(comm, grad, 8, 4, 128, 64)
+    b = run_tlq(comm, grad, 8, 4, 128, 64)
+    for x, y in zip(a, b):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+
+
+def test_errors_raise(comm):
+    from paper_2410_15526_b200 import SDP4Error
+    g = torch.zeros(1000, device="cuda")
+    with pytest.raises(SDP4Error):
+        comm.tlq_hs_reduce_scatter(g, torch.empty(1000, device="cuda"), torch.empty(10**6, dtype=torch.uint8,
+                                                                                     device="cuda"))
+    with pytest.raises(SDP4Error):   # host pointer rejected before any launch
+        comm.tlq_hs_reduce_scatter(torch.zeros(16384), torch.empty(16384, device="cuda"),
+                                   torch.empty(10**6, dtype=torch.uint8, device="cuda"))
