@@ -89,7 +89,9 @@ def quantize(x: np.ndarray, k: int, G: int, c: np.float32 = F32(1.0)):
     produced); scales: fp32 per group.
       s      = max |x_g|                                   (R2)
       inv    = rn(q_k / s)                                 (R3, one division per group)
-      y      = rn(x * inv);  code = clamp(RNE(y), +-q_k)   (R3)
+      code   = clamp(RNE(x * inv), +-q_k)                  (R3: the exact product x*inv is
+               rounded once, to the nearest-even integer -- the single round() of P:281;
+               fp64 holds the 24x24-bit product exactly)
       scale  = rn(s * c)                                   (R6: c = c_b folds the
                Hadamard normalization into the scale; c = 1 without Hadamard)
     Zero / tiny groups (s < 2^-120) and non-finite groups get codes 0; the scale
@@ -106,8 +108,8 @@ def quantize(x: np.ndarray, k: int, G: int, c: np.float32 = F32(1.0)):
     ok = np.isfinite(s) & (s >= TINY)
     with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
         inv = np.where(ok, q / np.where(ok, s, F32(1.0)), F32(0.0)).astype(F32)
-        y = X * inv[:, None]
-        y = np.where(ok[:, None], y, F32(0.0))
+        y = X.astype(np.float64) * inv.astype(np.float64)[:, None]     # exact product
+        y = np.where(ok[:, None], y, 0.0)
         codes = np.clip(np.rint(y), -q, q).astype(np.int32)
         scales = np.where(s < TINY, F32(0.0), s * F32(c)).astype(F32)
     return codes.reshape(-1), scales

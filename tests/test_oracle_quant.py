@@ -149,3 +149,31 @@ def test_pack_unpack_and_wire_sizes():
         assert len(w) % 256 == 0
         c2, s2 = wire_unit_decode(w, 4096, k, 128)
         assert np.array_equal(c2, codes) and np.array_equal(s2, scales)
+
+
+def test_codes_are_single_rounding_of_exact_product():
+    # R3 (P:281 has one round()): code = RNE(x * inv) of the EXACT product, inv = rn(q/s).
+    # Pinned against exact rational arithmetic (fractions; Python's round() is half-to-even) on
+    # groups built so that rn(x * inv) lands on a .5 tie while the exact product does not: there
+    # the single-rounding and the double-rounding readings give different codes.
+    from fractions import Fraction
+    rng = np.random.default_rng(42)
+    k, q = 4, q_levels(4)
+    found = 0
+    for trial in range(400):
+        s_ = F32(rng.uniform(1.0, 2.0))
+        inv = F32(F32(q) / s_)
+        t = float(rng.integers(0, q)) + 0.5
+        x0 = np.float32(t / float(inv))
+        for x in (np.nextafter(x0, np.float32(0)), x0, np.nextafter(x0, np.float32(10))):
+            x = F32(x)
+            if not (0 < x < s_):
+                continue
+            exact = Fraction(float(x)) * Fraction(float(inv))
+            if exact == t or F32(x * inv) != F32(t):
+                continue
+            codes, sc = quantize(np.array([s_, x], F32), k, 2)
+            assert sc[0] == s_ and codes[0] == q
+            assert codes[1] == round(exact)
+            found += round(exact) != round(Fraction(t))      # double rounding would give round(t)
+    assert found >= 10
