@@ -147,6 +147,24 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t comm, const void* grad, sdp4_
                                        float* out_shard, void* workspace, size_t workspace_bytes,
                                        void* stream);
 
+/* Stage entry points: the three kernels of sdp4_tlq_hs_reduce_scatter on ONE rank's
+ * buffers, with no communication and no comm object (argument rules as above, with
+ * P = groups_M * group_size_N).  They let a caller verify each stage or emulate P ranks
+ * on one GPU by moving the blocks itself.  Buffers use the region layouts of
+ * sdp4_tlq_workspace_offset: intra_send / intra_recv = N blocks of M units
+ * W(S, bits_intra, G); inter_send / inter_recv = M units W(S, bits_inter, G).
+ *   stage_quantize  K3: Alg. 3 l.2-3: grad (D) -> intra_send
+ *   stage_reduce    K4: Alg. 3 l.5,7,9 for local rank l: intra_recv -> inter_send
+ *   stage_final     K5: Alg. 3 l.11-13: inter_recv -> out_shard (S) */
+sdp4_status sdp4_tlq_stage_quantize(const void* grad, sdp4_dtype grad_dtype, size_t numel, int groups_M,
+                                    int group_size_N, int bits_intra, int group, int hadamard_block,
+                                    void* intra_send, void* stream);
+sdp4_status sdp4_tlq_stage_reduce(const void* intra_recv, size_t numel, int groups_M, int group_size_N,
+                                  int bits_intra, int bits_inter, int group, void* inter_send, void* stream);
+sdp4_status sdp4_tlq_stage_final(const void* inter_recv, size_t numel, int groups_M, int group_size_N,
+                                 int bits_inter, int group, int hadamard_block, int average, float* out_shard,
+                                 void* stream);
+
 /* ---------------------------------------------------------------------------
  * Instrumentation (measurement only; no effect on results).
  * ------------------------------------------------------------------------- */

@@ -151,6 +151,29 @@ size_t tlq_region(int M, int N, size_t numel, int bi, int be, int group, int reg
   return off[region];
 }
 
+sdp4_status check_tlq_args(int P, size_t numel, int bi, int be, int group, int b) {
+  if (!valid_bits(bi) || !valid_bits(be)) return fail(SDP4_EINVAL, "bits (%d, %d) not in {4, 8, 32}", bi, be);
+  if (b != 0 && (!is_pow2(b) || b < 2 || b > 256))
+    return fail(SDP4_EINVAL, "hadamard_block %d not in {0, 2, 4, ..., 256}", b);
+  sdp4_status s = check_sizes(P, numel, group);
+  if (s != SDP4_OK) return s;
+  if (b > group) return fail(SDP4_EALIGN, "group %d must be divisible by hadamard_block %d (P:395)", group, b);
+  return SDP4_OK;
+}
+
+// R6/R8 constants: c_b = rn(1/sqrt(b)); kappa = rn(c_b / P) (average) or c_b; b = 0: rn(1/P) or 1.
+float hadamard_cb(int b) { return b ? (float)(1.0 / std::sqrt((double)b)) : 1.0f; }
+float final_kappa(int b, int P, int average) {
+  const float cb = hadamard_cb(b);
+  return average ? (b ? cb / (float)P : 1.0f / (float)P) : cb;
+}
+
+int sm_count_current() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
 }  // namespace
 
 extern "C" {
@@ -307,15 +330,10 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
   g_err.clear();
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (rnd != SDP4_RNE) return fail(SDP4_EINVAL, "only SDP4_RNE rounding is implemented");
-  if (!valid_bits(bits_intra) || !valid_bits(bits_inter))
-    return fail(SDP4_EINVAL, "bits (%d, %d) not in {4, 8, 32}", bits_intra, bits_inter);
   if (grad_dtype != SDP4_F32 && grad_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad grad dtype");
   const int b = hadamard_block;
-  if (b != 0 && (!is_pow2(b) || b < 2 || b > 256))
-    return fail(SDP4_EINVAL, "hadamard_block %d not in {0, 2, 4, ..., 256}", b);
-  sdp4_status s = check_sizes(c->world, numel, group);
+  sdp4_status s = check_tlq_args(c->world, numel, bits_intra, bits_inter, group, b);
   if (s != SDP4_OK) return s;
-  if (b > group) return fail(SDP4_EALIGN, "group %d must be divisible by hadamard_block %d (P:395)", group, b);
   if ((s = check_ptr(grad, "grad")) != SDP4_OK) return s;
   if ((s = check_ptr(out_shard, "out_shard")) != SDP4_OK) return s;
   if ((s = check_ptr(workspace, "workspace")) != SDP4_OK) return s;
@@ -334,9 +352,7 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
   uint8_t* inter_recv = ws + tlq_region(M, N, numel, bits_intra, bits_inter, group, 3, nullptr);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
-  // R6/R8 constants: c_b = rn(1/sqrt(b)); kappa = rn(c_b / P) (average) or c_b; b = 0: rn(1/P) or 1.
-  const float cb = b ? (float)(1.0 / std::sqrt((double)b)) : 1.0f;
-  const float kappa = average ? (b ? cb / (float)P : 1.0f / (float)P) : cb;
+  const float cb = hadamard_cb(b), kappa = final_kappa(b, P, average);
 
   // Alg. 3 l.2-3: Hadamard + Quantize8Bit into the intra send layout (K3)
   s = launch(c, "K3_tlq_had_quant", st, [&] {
@@ -365,6 +381,58 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     return sdp4::launch_tlq_dq_reduce_had(inter_recv, w4, bits_inter, M, S, group, b, kappa, out_shard,
                                           c->grid_cap(), st);
   });
+}
+
+sdp4_status sdp4_tlq_stage_quantize(const void* grad, sdp4_dtype grad_dtype, size_t numel, int M, int N,
+                                    int bits_intra, int group, int hadamard_block, void* intra_send, void* stream) {
+  g_err.clear();
+  if (M < 1 || N < 1) return fail(SDP4_EINVAL, "bad topology %d x %d", M, N);
+  if (grad_dtype != SDP4_F32 && grad_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad grad dtype");
+  sdp4_status s = check_tlq_args(M * N, numel, bits_intra, 4, group, hadamard_block);
+  if (s != SDP4_OK) return s;
+  if ((s = check_ptr(grad, "grad")) != SDP4_OK) return s;
+  if ((s = check_ptr(intra_send, "intra_send")) != SDP4_OK) return s;
+  const size_t S = numel / ((size_t)M * N);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = sdp4::launch_tlq_had_quant(grad, grad_dtype, S, M, N, group, hadamard_block,
+                                             hadamard_cb(hadamard_block), bits_intra,
+                                             static_cast<uint8_t*>(intra_send), unit_bytes(S, bits_intra, group),
+                                             sm_count_current() * 8, st);
+  return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "K3 launch failed: %s", cudaGetErrorString(e));
+}
+
+sdp4_status sdp4_tlq_stage_reduce(const void* intra_recv, size_t numel, int M, int N, int bits_intra,
+                                  int bits_inter, int group, void* inter_send, void* stream) {
+  g_err.clear();
+  if (M < 1 || N < 1) return fail(SDP4_EINVAL, "bad topology %d x %d", M, N);
+  sdp4_status s = check_tlq_args(M * N, numel, bits_intra, bits_inter, group, 0);
+  if (s != SDP4_OK) return s;
+  if ((s = check_ptr(intra_recv, "intra_recv")) != SDP4_OK) return s;
+  if ((s = check_ptr(inter_send, "inter_send")) != SDP4_OK) return s;
+  const size_t S = numel / ((size_t)M * N);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = sdp4::launch_tlq_dq_reduce_q(static_cast<const uint8_t*>(intra_recv),
+                                               unit_bytes(S, bits_intra, group), bits_intra, N, M, S, group,
+                                               static_cast<uint8_t*>(inter_send), unit_bytes(S, bits_inter, group),
+                                               bits_inter, sm_count_current() * 8, st);
+  return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "K4 launch failed: %s", cudaGetErrorString(e));
+}
+
+sdp4_status sdp4_tlq_stage_final(const void* inter_recv, size_t numel, int M, int N, int bits_inter, int group,
+                                 int hadamard_block, int average, float* out_shard, void* stream) {
+  g_err.clear();
+  if (M < 1 || N < 1) return fail(SDP4_EINVAL, "bad topology %d x %d", M, N);
+  sdp4_status s = check_tlq_args(M * N, numel, 8, bits_inter, group, hadamard_block);
+  if (s != SDP4_OK) return s;
+  if ((s = check_ptr(inter_recv, "inter_recv")) != SDP4_OK) return s;
+  if ((s = check_ptr(out_shard, "out_shard")) != SDP4_OK) return s;
+  const size_t S = numel / ((size_t)M * N);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = sdp4::launch_tlq_dq_reduce_had(static_cast<const uint8_t*>(inter_recv),
+                                                 unit_bytes(S, bits_inter, group), bits_inter, M, S, group,
+                                                 hadamard_block, final_kappa(hadamard_block, M * N, average),
+                                                 out_shard, sm_count_current() * 8, st);
+  return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "K5 launch failed: %s", cudaGetErrorString(e));
 }
 
 uint64_t sdp4_launch_count(sdp4_comm_t c, int reset) {

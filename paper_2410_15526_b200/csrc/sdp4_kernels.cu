@@ -8,10 +8,10 @@
 //
 //  K1 qwd_quantize      Alg. 2 l.2-3          vector layout, 8 el/thread
 //  K2 qwd_apply         Alg. 2 l.5              vector layout, 16 el/thread
-//  K3 tlq_had_quant     Alg. 3 l.2-3, fused   row layout (64 el/thread),
-//                       Hadamard + quantize    smem-staged (cp.async)
-//  K4 tlq_dq_reduce_q   Alg. 3 l.5,7,9        vector layout, 16 el/thread
-//  K5 tlq_dq_reduce_had Alg. 3 l.11-13 row layout, smem-staged output
+//  K3 tlq_had_quant     Alg. 3 l.2-3, fused   row layout (64 el/thread, f32x2),
+//                       Hadamard + quantize    TMA tensor ring in, TMA store out
+//  K4 tlq_dq_reduce_q   Alg. 3 l.5,7,9        vector layout, 1-D bulk-copy ring
+//  K5 tlq_dq_reduce_had Alg. 3 l.11-13 row layout, TMA ring in, TMA store out
 //
 // Integer rounding uses the magic-number identity: for |y| <= 2^22,
 // rn(y + 1.5*2^23) is the nearest-even integer of y and its low mantissa bits
@@ -20,6 +20,8 @@
 #include "sdp4_kernels.cuh"
 
 #include <cfloat>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
 namespace sdp4 {
@@ -57,10 +59,9 @@ __device__ __forceinline__ QP qparam(float s, float q) {
 __device__ __forceinline__ float stored_scale(float s, float c) {
   return (s < kTiny) ? 0.f : __fmul_rn(s, c);
 }
-// rn(x * inv) rounded to the nearest-even integer, as magic-number bits.
-__device__ __forceinline__ uint32_t rq(float x, float inv) {
-  return __float_as_uint(__fadd_rn(__fmul_rn(x, inv), kMagic));
-}
+// RNE(x * inv) of the exact product (R3: one rounding), as magic-number bits:
+// fma(x, inv, 1.5*2^23) rounds the exact x*inv + 1.5*2^23 once, to an integer.
+__device__ __forceinline__ uint32_t rq(float x, float inv) { return __float_as_uint(__fmaf_rn(x, inv, kMagic)); }
 __device__ __forceinline__ uint32_t pack8x4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
@@ -110,60 +111,6 @@ __device__ __forceinline__ float group_max(float v, int tpg, float* red) {
   return v;
 }
 
-// Physical 16-byte chunk index of logical chunk c of row `row` in a smem tile whose
-// rows are `cpr` chunks long.  XOR swizzle: conflict-free both for one-row-per-thread
-// access (8 consecutive rows per quarter-warp) and for linear (coalescing) access.
-// For cpr = 2/4/8 it equals the TMA SWIZZLE_32B/64B/128B patterns.
-__device__ __forceinline__ int swz(int row, int c, int cpr) {
-  const int f = (cpr >= 8) ? (row & 7) : ((row / (8 / cpr)) & (cpr - 1));
-  return row * cpr + (c ^ f);
-}
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
-  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-__device__ __forceinline__ uint4 ldg_stream(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-// In-register butterfly stages h = 1..min(b,64)/2 of the unnormalized Sylvester
-// Hadamard (R6): pairs (i, i+h) -> (a + c, a - c), ascending h.
-__device__ __forceinline__ void fwht_row(float* v, int b) {
-#pragma unroll
-  for (int h = 1; h < 64; h <<= 1) {
-    if (b > h) {
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        if ((i & h) == 0) {
-          const float a = v[i], c = v[i + h];
-          v[i] = __fadd_rn(a, c);
-          v[i + h] = __fsub_rn(a, c);
-        }
-      }
-    }
-  }
-  // b = 128, 256: stages h = 64, 128 pair row t with row t ^ (h / 64) (lanes of one warp).
-  for (int hx = 1; 64 * hx < b; hx <<= 1) {
-    const bool upper = (threadIdx.x & hx) != 0;
-#pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      const float o = __shfl_xor_sync(0xffffffffu, v[i], hx);
-      v[i] = upper ? __fsub_rn(o, v[i]) : __fadd_rn(v[i], o);
-    }
-  }
-}
-
 // =====================================================================================
 // K1  qWD quantize (Alg. 2 l.2-3): d = rn(w_main - widen(w_model)),
 // per G-group s = max|d|, codes = RNE(d * rn(q/s)).  8 elements per thread, a group is
@@ -172,10 +119,10 @@ __device__ __forceinline__ void fwht_row(float* v, int b) {
 template <typename TM, int BITS>
 __global__ void __launch_bounds__(256) k1_qwd_quantize(const float* __restrict__ w_main,
                                                        const TM* __restrict__ w_model, size_t S,
-                                                       int G, uint8_t* __restrict__ unit) {
+                                                       int lg, uint8_t* __restrict__ unit) {
   __shared__ float red[8];
   constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
-  const int tpg = G >> 3;
+  const int tpg = (1 << lg) >> 3;
   const size_t ntiles = (S + 2047) / 2048;
   float* scales = reinterpret_cast<float*>(unit + S * (BITS == 32 ? 4 : BITS) / 8);
   for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -230,7 +177,7 @@ __global__ void __launch_bounds__(256) k1_qwd_quantize(const float* __restrict__
           if (!p.ok) w = make_uint2(0u, 0u);
           *reinterpret_cast<uint2*>(unit + e0) = w;
         }
-        if ((threadIdx.x & (tpg - 1)) == 0) scales[e0 / G] = stored_scale(a, 1.f);
+        if ((threadIdx.x & (tpg - 1)) == 0) scales[e0 >> lg] = stored_scale(a, 1.f);
       }
     }
   }
@@ -242,7 +189,7 @@ __global__ void __launch_bounds__(256) k1_qwd_quantize(const float* __restrict__
 // =====================================================================================
 template <typename TM, int BITS>
 __global__ void __launch_bounds__(256) k2_qwd_apply(const uint8_t* __restrict__ units,
-                                                    size_t unit_bytes, size_t S, int G,
+                                                    size_t unit_bytes, size_t S, int lg,
                                                     TM* __restrict__ w_model) {
   constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
   const int j = blockIdx.y;
@@ -262,7 +209,7 @@ __global__ void __launch_bounds__(256) k2_qwd_apply(const uint8_t* __restrict__ 
         x[4 * i] = t.x; x[4 * i + 1] = t.y; x[4 * i + 2] = t.z; x[4 * i + 3] = t.w;
       }
     } else {
-      const float ds = __fdiv_rn(scales[e0 / G], q);
+      const float ds = __fdiv_rn(scales[e0 >> lg], q);
       float f[16];
       if constexpr (BITS == 4) {
         const uint2 w = *reinterpret_cast<const uint2*>(unit + e0 / 2);
@@ -304,314 +251,676 @@ __global__ void __launch_bounds__(256) k2_qwd_apply(const uint8_t* __restrict__ 
 }
 
 // =====================================================================================
-// K3  TLq-HS Hadamard + quantize (Alg. 3 l.2-3, P:368-369; fused per P:394-395).
-// One thread owns one 64-element row; a CTA tile is 256 rows of one shard j, staged
-// global -> smem with cp.async (double-buffered, XOR-swizzled), butterflied in
-// registers, quantized, staged in smem and written coalesced to block l' = j % N,
-// unit m' = j / N of the intra send buffer (R9).
+// TMA (cp.async.bulk[.tensor]) + mbarrier primitives (sm_90+ PTX, used on sm_100a).
 // =====================================================================================
-template <typename TG, int BITS>
-__global__ void __launch_bounds__(kTileRows) k3_tlq_had_quant(const TG* __restrict__ grad, size_t S,
-                                                             int M, int N, int G, int b, float cb,
-                                                             uint8_t* __restrict__ intra_send,
-                                                             size_t unit_bytes, size_t tiles_per_shard,
-                                                             size_t ntiles) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int IN_CPR = kRowElems * (int)sizeof(TG) / 16;    // 8 (bf16) or 16 (fp32)
-  constexpr int IN_TILE = kTileRows * IN_CPR * 16;
-  constexpr int OUT_CPR = kRowElems * BITS / 8 / 16;          // 2, 4 or 16
-  constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
-  uint8_t* out_buf = smem + 2 * IN_TILE;
-  const int t = threadIdx.x;
-  const size_t rows_per_shard = S / kRowElems;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
+               : "memory");
+}
+// 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
 
-  auto issue_load = [&](size_t tile, int buf) {
-    if (tile < ntiles) {
-      const size_t j = tile / tiles_per_shard, ts = tile % tiles_per_shard;
-      const size_t row0 = ts * kTileRows;
-      const int rows = (int)min((size_t)kTileRows, rows_per_shard - row0);
-      const uint8_t* src = reinterpret_cast<const uint8_t*>(grad + j * S + row0 * kRowElems);
-      uint8_t* dst = smem + buf * IN_TILE;
-      for (int i = t; i < rows * IN_CPR; i += kTileRows)
-        cp_async16(dst + 16 * swz(i / IN_CPR, i % IN_CPR, IN_CPR), src + 16 * (size_t)i);
-    }
-    cp_async_commit();
-  };
+// Row tiles: kTileRows rows of R bytes of one unit.  R <= 128: one TMA box {R, 256, 1},
+// smem [256][R] with the hardware swizzle of width R (SWIZZLE_32B/64B/128B: 16-byte chunk
+// index XOR address bits 7..); R == 256: two boxes (halves) {128, 1, 256, 1}, smem
+// [2][256][128], SWIZZLE_128B.  Thread r touching chunk c of its own row is conflict-free
+// (8 consecutive rows of a quarter-warp hit 8 distinct bank groups).
+template <int R>
+__device__ __forceinline__ uint32_t tile_off(int r, int c) {
+  if constexpr (R == 256) return (c >> 3) * (kTileRows * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+  else if constexpr (R == 128) return r * 128 + ((c ^ (r & 7)) << 4);
+  else if constexpr (R == 64) return r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
+  else return r * 32 + ((c ^ ((r >> 2) & 1)) << 4);
+}
+template <int R>
+__device__ __forceinline__ void tma_load_tile(void* dst, const CUtensorMap* map, uint64_t* bar, int row, int unit) {
+  if constexpr (R == 256) {
+    tma_load_4d(dst, map, bar, 0, 0, row, unit);
+    tma_load_4d(static_cast<uint8_t*>(dst) + kTileRows * 128, map, bar, 0, 1, row, unit);
+  } else {
+    tma_load_3d(dst, map, bar, 0, row, unit);
+  }
+}
+template <int R>
+__device__ __forceinline__ void tma_store_tile(const CUtensorMap* map, const void* src, int row, int unit) {
+  if constexpr (R == 256) {
+    tma_store_4d(map, src, 0, 0, row, unit);
+    tma_store_4d(map, static_cast<const uint8_t*>(src) + kTileRows * 128, 0, 1, row, unit);
+  } else {
+    tma_store_3d(map, src, 0, row, unit);
+  }
+}
 
-  int buf = 0;
-  issue_load(blockIdx.x, 0);
-  for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
-    issue_load(tile + gridDim.x, buf ^ 1);
-    cp_async_wait<1>();
-    __syncthreads();
-    const size_t j = tile / tiles_per_shard, ts = tile % tiles_per_shard;
-    const size_t row0 = ts * kTileRows;
-    const int rows = (int)min((size_t)kTileRows, rows_per_shard - row0);
-    const bool act = t < rows;
+// ---- packed fp32x2 (sm_100a FADD2 / FMUL2: two IEEE round-to-nearest ops per instruction).
+// Inline PTX with an explicit .rn: never contracted into FFMA2 (the __fmul2_rn/__fadd2_rn
+// builtins were observed to fuse into FFMA2 under nvcc 12.9, which changes roundings).
+__device__ __forceinline__ float2 f2op_add(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 pa, pb, pd;\n\tmov.b64 pa, {%2, %3};\n\tmov.b64 pb, {%4, %5};\n\t"
+      "add.rn.f32x2 pd, pa, pb;\n\tmov.b64 {%0, %1}, pd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 pa, pb, pd;\n\tmov.b64 pa, {%2, %3};\n\tmov.b64 pb, {%4, %5};\n\t"
+      "sub.rn.f32x2 pd, pa, pb;\n\tmov.b64 {%0, %1}, pd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 pa, pb, pd;\n\tmov.b64 pa, {%2, %3};\n\tmov.b64 pb, {%4, %5};\n\t"
+      "mul.rn.f32x2 pd, pa, pb;\n\tmov.b64 {%0, %1}, pd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) { return f2op_add(a, b); }
+// Packed rq: RNE(x * inv) bits for two elements (explicit FFMA2, exact product).
+__device__ __forceinline__ float2 f2rq(float2 a, float2 inv) {
+  float2 r;
+  asm("{\n\t.reg .b64 pa, pb, pc, pd;\n\tmov.b64 pa, {%2, %3};\n\tmov.b64 pb, {%4, %5};\n\t"
+      "mov.b64 pc, {%6, %6};\n\tfma.rn.f32x2 pd, pa, pb, pc;\n\tmov.b64 {%0, %1}, pd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(inv.x), "f"(inv.y), "f"(kMagic));
+  return r;
+}
+// NOTE: ptxas (12.9) contracts an f32x2 multiply feeding an f32x2 add into FFMA2 even with
+// .rn and --fmad=false.  Products that feed additions are therefore computed with scalar
+// __fmul_rn (scalar .rn is honoured); f2mul is used only where its result is not added.
 
-    float v[64];
-    const uint8_t* in = smem + buf * IN_TILE;
-    if (act) {
+// A 64-element row lives in 32 f32x2 registers p[i] = {v[i], v[i+32]}.
+//
+// Unnormalized Sylvester butterfly of one b-block (R6): stages h = 1, 2, ..., B/2 in
+// ascending order, pairs (i, i+h) -> (a + c, a - c).  Stages h < 32 act on whole pairs
+// (elements i and i+32 play the same role), h = 32 inside each pair, and h = 64, 128 pair
+// row t with row t ^ (h / 64) of the same warp.
+template <int B>
+__device__ __forceinline__ void fwht_pairs(float2* p) {
 #pragma unroll
-      for (int c = 0; c < IN_CPR; ++c) {
-        const uint4 u = *reinterpret_cast<const uint4*>(in + 16 * swz(t, c, IN_CPR));
-        if constexpr (sizeof(TG) == 2) {
-          v[8 * c + 0] = bf16_lo(u.x); v[8 * c + 1] = bf16_hi(u.x);
-          v[8 * c + 2] = bf16_lo(u.y); v[8 * c + 3] = bf16_hi(u.y);
-          v[8 * c + 4] = bf16_lo(u.z); v[8 * c + 5] = bf16_hi(u.z);
-          v[8 * c + 6] = bf16_lo(u.w); v[8 * c + 7] = bf16_hi(u.w);
+  for (int h = 1; h < 32 && h < B; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if ((i & h) == 0) {
+        const float2 a = p[i], c = p[i + h];
+        p[i] = f2add(a, c);
+        p[i + h] = f2sub(a, c);
+      }
+    }
+  }
+  if constexpr (B >= 64) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float a = p[i].x, c = p[i].y;
+      p[i] = make_float2(__fadd_rn(a, c), __fsub_rn(a, c));
+    }
+  }
+#pragma unroll
+  for (int hx = 1; 64 * hx < B; hx <<= 1) {
+    const bool upper = (threadIdx.x & hx) != 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, p[i].x, hx), __shfl_xor_sync(0xffffffffu, p[i].y, hx));
+      p[i] = upper ? f2sub(o, p[i]) : f2add(p[i], o);
+    }
+  }
+}
+
+// Decode the 64 codes of row t of a row tile (R = 64*BIN/8 bytes) and dequantize:
+// x[i] = {code_i * ds0, code_{i+32} * ds1} (ds0 for elements 0..31, ds1 for 32..63).
+template <int BIN, int R>
+__device__ __forceinline__ void dequant_row(const uint8_t* tile, int t, float ds0, float ds1, float2* x) {
+  float f[64];
+#pragma unroll
+  for (int c = 0; c < R / 16; ++c) {
+    const uint4 u = *reinterpret_cast<const uint4*>(tile + tile_off<R>(t, c));
+    if constexpr (BIN == 4) {
+      dec4x8(u.x, f + 32 * c); dec4x8(u.y, f + 32 * c + 8); dec4x8(u.z, f + 32 * c + 16); dec4x8(u.w, f + 32 * c + 24);
+    } else if constexpr (BIN == 8) {
+      dec8x4(u.x, f + 16 * c); dec8x4(u.y, f + 16 * c + 4); dec8x4(u.z, f + 16 * c + 8); dec8x4(u.w, f + 16 * c + 12);
+    } else {
+      f[4 * c] = __uint_as_float(u.x); f[4 * c + 1] = __uint_as_float(u.y);
+      f[4 * c + 2] = __uint_as_float(u.z); f[4 * c + 3] = __uint_as_float(u.w);
+    }
+  }
+  if constexpr (BIN == 32) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = make_float2(f[i], f[i + 32]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = make_float2(__fmul_rn(f[i], ds0), __fmul_rn(f[i + 32], ds1));
+  }
+}
+
+// Quantize a 64-element row held as pairs (R2, R3) into codes in an output row tile; the
+// group's first row writes the scale rn(s * c) (R6) straight to global.  lg = log2 G:
+// G >= 64 -> a group spans G/64 rows (lanes); G == 32 -> two groups per row (one per half).
+template <int BITS, int R>
+__device__ __forceinline__ void quant_row(const float2* p, int t, int lg, float c, bool act, uint8_t* out_tile,
+                                          float* scales_tile) {
+  constexpr float q = float((1 << (BITS - 1)) - 1);
+  float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    a0 = max_nan(a0, fabsf(p[i].x));
+    a1 = max_nan(a1, fabsf(p[i].y));
+  }
+  QP p0, p1;
+  if (lg >= 6) {
+    a0 = max_nan(a0, a1);
+    const int rpg = 1 << (lg - 6);
+    for (int off = 1; off < rpg; off <<= 1) a0 = max_nan(a0, __shfl_xor_sync(0xffffffffu, a0, off));
+    p0 = qparam(a0, q);
+    p1 = p0;
+    if (act && (t & (rpg - 1)) == 0) scales_tile[t >> (lg - 6)] = stored_scale(a0, c);
+  } else {
+    p0 = qparam(a0, q);
+    p1 = qparam(a1, q);
+    if (act) *reinterpret_cast<float2*>(scales_tile + 2 * t) = make_float2(stored_scale(a0, c), stored_scale(a1, c));
+  }
+  const float2 inv = make_float2(p0.inv, p1.inv);
+  uint32_t rx[32], ry[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float2 y = f2rq(p[i], inv);
+    rx[i] = __float_as_uint(y.x);
+    ry[i] = __float_as_uint(y.y);
+  }
+  if constexpr (BITS == 8) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t* r = (k < 2 ? rx : ry) + 16 * (k & 1);
+      uint4 w = make_uint4(pack8x4(r[0], r[1], r[2], r[3]), pack8x4(r[4], r[5], r[6], r[7]),
+                           pack8x4(r[8], r[9], r[10], r[11]), pack8x4(r[12], r[13], r[14], r[15]));
+      if (!(k < 2 ? p0.ok : p1.ok)) w = make_uint4(0u, 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(out_tile + tile_off<R>(t, k)) = w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t* r = k == 0 ? rx : ry;
+      uint4 w = make_uint4(pack4x8(r), pack4x8(r + 8), pack4x8(r + 16), pack4x8(r + 24));
+      if (!(k == 0 ? p0.ok : p1.ok)) w = make_uint4(0u, 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(out_tile + tile_off<R>(t, k)) = w;
+    }
+  }
+}
+
+// Incremental (unit, tile-in-unit) coordinates of tile = blockIdx.x + i * gridDim.x.
+struct TileIter {
+  uint32_t unit, ts, per;
+  __device__ TileIter(uint32_t per_unit) : per(per_unit) {
+    unit = blockIdx.x / per;
+    ts = blockIdx.x - unit * per;
+  }
+  __device__ void next() {
+    ts += gridDim.x;
+    while (ts >= per) {
+      ts -= per;
+      ++unit;
+    }
+  }
+};
+
+template <int IN_R, int OUT_R>
+struct K3Cfg {
+  static constexpr int IN_TILE = kTileRows * IN_R;
+  static constexpr int OUT_TILE = kTileRows * OUT_R;
+  static constexpr int BUDGET = 200 * 1024;
+  static constexpr int S0 = (BUDGET - 2 * OUT_TILE) / IN_TILE;
+  static constexpr int STAGES = S0 > 4 ? 4 : (S0 < 1 ? 1 : S0);
+  static constexpr int SMEM = STAGES * IN_TILE + 2 * OUT_TILE + 64 + 1024;
+};
+
+// =====================================================================================
+// K3  TLq-HS Hadamard + quantize (Alg. 3 l.2-3, P:368-369; fused per P:394-395).
+// Persistent CTAs (one per SM); tile = 256 rows of 64 elements of one shard j.  Thread 0
+// keeps a STAGES-deep ring of TMA tensor loads in flight (mbarrier complete_tx); every
+// thread butterflies its own row in f32x2 registers, quantizes it and writes its codes
+// into a double-buffered swizzled smem tile that thread 0 TMA-stores to unit
+// (l' = j % N, m' = j / N) of the intra send buffer (R9).  Scales go straight to global.
+// =====================================================================================
+template <int IN_R, int BITS, int B>
+__global__ void __launch_bounds__(kTileRows, 1)
+    k3_tlq_had_quant(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
+                     size_t S, int M, int N, int lg, float cb, uint8_t* __restrict__ intra_send, size_t unit_bytes,
+                     uint32_t tps, uint32_t ntiles) {
+  constexpr int OUT_R = kRowElems * BITS / 8;
+  using C = K3Cfg<IN_R, OUT_R>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* in_buf = smem;
+  uint8_t* out_buf = smem + STAGES * C::IN_TILE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(out_buf + 2 * C::OUT_TILE);
+  const int t = threadIdx.x;
+  const uint32_t rows_per_shard = (uint32_t)(S / kRowElems);
+
+  if (t == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t i) {
+    const uint32_t tile = blockIdx.x + i * gridDim.x;
+    if (tile < ntiles) {
+      const int s = i % STAGES;
+      mbar_arrive_tx(&bar[s], C::IN_TILE);
+      tma_load_tile<IN_R>(in_buf + s * C::IN_TILE, &in_map, &bar[s], (int)((tile % tps) * kTileRows),
+                          (int)(tile / tps));
+    }
+  };
+  if (t == 0)
+    for (int i = 0; i < STAGES; ++i) issue(i);
+
+  TileIter it(tps);
+  for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i, it.next()) {
+    const int s = i % STAGES;
+    const uint32_t j = it.unit, ts = it.ts;
+    const bool act = (int)(ts * kTileRows) + t < (int)rows_per_shard;
+    mbar_wait(&bar[s], (i / STAGES) & 1);
+    float2 p[32];
+    const uint8_t* in = in_buf + s * C::IN_TILE;
+#pragma unroll
+    for (int c = 0; c < IN_R / 16; ++c) {
+      const uint4 u = *reinterpret_cast<const uint4*>(in + tile_off<IN_R>(t, c));
+      if constexpr (IN_R == 128) {  // bf16: chunk c = elements 8c..8c+7
+        const int b0 = 8 * (c & 3);
+        float2* d = p + b0;
+        if (c < 4) {
+          d[0].x = bf16_lo(u.x); d[1].x = bf16_hi(u.x); d[2].x = bf16_lo(u.y); d[3].x = bf16_hi(u.y);
+          d[4].x = bf16_lo(u.z); d[5].x = bf16_hi(u.z); d[6].x = bf16_lo(u.w); d[7].x = bf16_hi(u.w);
         } else {
-          v[4 * c + 0] = __uint_as_float(u.x); v[4 * c + 1] = __uint_as_float(u.y);
-          v[4 * c + 2] = __uint_as_float(u.z); v[4 * c + 3] = __uint_as_float(u.w);
+          d[0].y = bf16_lo(u.x); d[1].y = bf16_hi(u.x); d[2].y = bf16_lo(u.y); d[3].y = bf16_hi(u.y);
+          d[4].y = bf16_lo(u.z); d[5].y = bf16_hi(u.z); d[6].y = bf16_lo(u.w); d[7].y = bf16_hi(u.w);
+        }
+      } else {  // fp32: chunk c = elements 4c..4c+3
+        float2* d = p + 4 * (c & 7);
+        if (c < 8) {
+          d[0].x = __uint_as_float(u.x); d[1].x = __uint_as_float(u.y);
+          d[2].x = __uint_as_float(u.z); d[3].x = __uint_as_float(u.w);
+        } else {
+          d[0].y = __uint_as_float(u.x); d[1].y = __uint_as_float(u.y);
+          d[2].y = __uint_as_float(u.z); d[3].y = __uint_as_float(u.w);
         }
       }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 64; ++i) v[i] = 0.f;
     }
-    fwht_row(v, b);
+    if (t == 0) bulk_wait_read<1>();  // the store issued two tiles ago has left out_buf[i & 1]
+    __syncthreads();                  // stage s fully consumed -> refill it
+    if (t == 0) issue(i + STAGES);
 
-    const size_t lp = j % N, mp = j / N;
-    uint8_t* unit = intra_send + (lp * M + mp) * unit_bytes;
+    fwht_pairs<B>(p);
+
+    const uint32_t unit = (j % N) * M + j / N;
+    uint8_t* ot = out_buf + (i & 1) * C::OUT_TILE;
     if constexpr (BITS == 32) {  // identity codec (R12): rn(u * c_b)
+      const float2 cc = make_float2(cb, cb);
+#pragma unroll
+      for (int i2 = 0; i2 < 32; ++i2) p[i2] = f2mul(p[i2], cc);
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
-        const float4 o = make_float4(__fmul_rn(v[4 * c], cb), __fmul_rn(v[4 * c + 1], cb),
-                                     __fmul_rn(v[4 * c + 2], cb), __fmul_rn(v[4 * c + 3], cb));
-        *reinterpret_cast<float4*>(out_buf + 16 * swz(t, c, OUT_CPR)) = o;
+        const float2* q = p + 4 * (c & 7);
+        *reinterpret_cast<float4*>(ot + tile_off<256>(t, c)) =
+            c < 8 ? make_float4(q[0].x, q[1].x, q[2].x, q[3].x) : make_float4(q[0].y, q[1].y, q[2].y, q[3].y);
       }
     } else {
-      float* scales = reinterpret_cast<float*>(unit + S * BITS / 8) + row0 * kRowElems / G;
-      // group maxima: G >= 64 -> one group spans G/64 rows (lanes); G == 32 -> two per row
-      float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) a0 = max_nan(a0, fabsf(v[i]));
-#pragma unroll
-      for (int i = 32; i < 64; ++i) a1 = max_nan(a1, fabsf(v[i]));
-      QP p0, p1;
-      if (G >= 64) {
-        a0 = max_nan(a0, a1);
-        for (int off = 1; off < G / 64; off <<= 1)
-          a0 = max_nan(a0, __shfl_xor_sync(0xffffffffu, a0, off));
-        a1 = a0;
-        p0 = qparam(a0, q);
-        p1 = p0;
-        if (act && (t & (G / 64 - 1)) == 0) scales[t / (G / 64)] = stored_scale(a0, cb);
-      } else {
-        p0 = qparam(a0, q);
-        p1 = qparam(a1, q);
-        if (act)
-          *reinterpret_cast<float2*>(scales + 2 * t) =
-              make_float2(stored_scale(a0, cb), stored_scale(a1, cb));
-      }
-      uint32_t r[64];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) r[i] = rq(v[i], p0.inv);
-#pragma unroll
-      for (int i = 32; i < 64; ++i) r[i] = rq(v[i], p1.inv);
-      if constexpr (BITS == 8) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint4 w = make_uint4(pack8x4(r[16 * c], r[16 * c + 1], r[16 * c + 2], r[16 * c + 3]),
-                               pack8x4(r[16 * c + 4], r[16 * c + 5], r[16 * c + 6], r[16 * c + 7]),
-                               pack8x4(r[16 * c + 8], r[16 * c + 9], r[16 * c + 10], r[16 * c + 11]),
-                               pack8x4(r[16 * c + 12], r[16 * c + 13], r[16 * c + 14], r[16 * c + 15]));
-          if (!(c < 2 ? p0.ok : p1.ok)) w = make_uint4(0u, 0u, 0u, 0u);
-          *reinterpret_cast<uint4*>(out_buf + 16 * swz(t, c, OUT_CPR)) = w;
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint4 w = make_uint4(pack4x8(r + 32 * c), pack4x8(r + 32 * c + 8), pack4x8(r + 32 * c + 16),
-                               pack4x8(r + 32 * c + 24));
-          if (!(c == 0 ? p0.ok : p1.ok)) w = make_uint4(0u, 0u, 0u, 0u);
-          *reinterpret_cast<uint4*>(out_buf + 16 * swz(t, c, OUT_CPR)) = w;
-        }
-      }
+      float* scales = reinterpret_cast<float*>(intra_send + unit * unit_bytes + S * BITS / 8) +
+                      (((size_t)ts * kTileElems) >> lg);
+      quant_row<BITS, OUT_R>(p, t, lg, cb, act, ot, scales);
     }
+    fence_proxy_async();
     __syncthreads();
-    // coalesced write-out of the tile's codes
-    uint8_t* dst = unit + row0 * kRowElems * BITS / 8;
-    for (int i = t; i < rows * OUT_CPR; i += kTileRows)
-      *reinterpret_cast<uint4*>(dst + 16 * (size_t)i) =
-          *reinterpret_cast<const uint4*>(out_buf + 16 * swz(i / OUT_CPR, i % OUT_CPR, OUT_CPR));
+    if (t == 0) {
+      tma_store_tile<OUT_R>(&out_map, ot, (int)(ts * kTileRows), (int)unit);
+      bulk_commit();
+    }
   }
-  cp_async_wait<0>();
+  if (t == 0) bulk_wait<0>();
 }
 
 // =====================================================================================
-// K4  TLq dequantize + reduce + requantize (Alg. 3 l.5, 7, 9, FP32 reduce
-// P:344).  Sub-block m' = blockIdx.y; sources l'' = 0..N-1 summed in order (R8).
-// 16 elements per thread; a group is G/16 consecutive threads.
+// K4  TLq dequantize + reduce + requantize (Alg. 3 l.5, 7, 9, FP32 reduce P:344).
+// Vector layout: a tile is 8192 elements of sub-block m'; thread t owns elements
+// [16t, 16t+16) and [4096+16t, 4096+16t+16).  Thread 0 streams (tile, source l'') items
+// through a STAGES-deep ring of 1-D bulk copies (codes + scales); sources are summed in
+// order l'' = 0..N-1 (R8); the sum is requantized and stored coalesced to unit m' of the
+// inter send buffer.
 // =====================================================================================
-template <int BIN, int BOUT>
-__global__ void __launch_bounds__(256) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv,
-                                                          size_t in_unit_bytes, int N, int M,
-                                                          size_t S, int G,
-                                                          uint8_t* __restrict__ send,
-                                                          size_t out_unit_bytes) {
-  __shared__ float red[8];
-  constexpr float qin = float((1 << (BIN == 32 ? 1 : BIN - 1)) - 1);
-  constexpr float qout = float((1 << (BOUT == 32 ? 1 : BOUT - 1)) - 1);
-  const int mp = blockIdx.y;
-  const int tpg = G >> 4;
-  uint8_t* out = send + (size_t)mp * out_unit_bytes;
-  float* oscales = reinterpret_cast<float*>(out + S * BOUT / 8);
-  const size_t ntiles = (S + 4095) / 4096;
-  for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const size_t e0 = tile * 4096 + threadIdx.x * 16;
-    const bool act = e0 < S;
-    float acc[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-    if (act) {
-      for (int l = 0; l < N; ++l) {
-        const uint8_t* unit = recv + ((size_t)l * M + mp) * in_unit_bytes;
-        float x[16];
-        if constexpr (BIN == 32) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint4 u = ldg_stream(unit + (e0 + 4 * i) * 4);
-            x[4 * i] = __uint_as_float(u.x); x[4 * i + 1] = __uint_as_float(u.y);
-            x[4 * i + 2] = __uint_as_float(u.z); x[4 * i + 3] = __uint_as_float(u.w);
-          }
-        } else {
-          const float s = reinterpret_cast<const float*>(unit + S * BIN / 8)[e0 / G];
-          const float ds = __fdiv_rn(s, qin);
-          float f[16];
-          if constexpr (BIN == 8) {
-            const uint4 w = ldg_stream(unit + e0);
-            dec8x4(w.x, f); dec8x4(w.y, f + 4); dec8x4(w.z, f + 8); dec8x4(w.w, f + 12);
-          } else {
-            const uint2 w = *reinterpret_cast<const uint2*>(unit + e0 / 2);
-            dec4x8(w.x, f); dec4x8(w.y, f + 8);
-          }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) x[i] = __fmul_rn(f[i], ds);
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = __fadd_rn(acc[i], x[i]);
-      }
-    }
-    if constexpr (BOUT == 32) {
-      if (act) {
-        float4* o = reinterpret_cast<float4*>(out + e0 * 4);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) o[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
-      }
-    } else {
-      float a = 0.f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) a = max_nan(a, fabsf(acc[i]));
-      a = group_max(a, tpg, red);
-      const QP p = qparam(a, qout);
-      if (act) {
-        uint32_t r[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) r[i] = rq(acc[i], p.inv);
-        if constexpr (BOUT == 4) {
-          uint2 w = make_uint2(pack4x8(r), pack4x8(r + 8));
-          if (!p.ok) w = make_uint2(0u, 0u);
-          *reinterpret_cast<uint2*>(out + e0 / 2) = w;
-        } else {
-          uint4 w = make_uint4(pack8x4(r[0], r[1], r[2], r[3]), pack8x4(r[4], r[5], r[6], r[7]),
-                               pack8x4(r[8], r[9], r[10], r[11]), pack8x4(r[12], r[13], r[14], r[15]));
-          if (!p.ok) w = make_uint4(0u, 0u, 0u, 0u);
-          *reinterpret_cast<uint4*>(out + e0) = w;
-        }
-        if ((threadIdx.x & (tpg - 1)) == 0) oscales[e0 / G] = stored_scale(a, 1.f);
-      }
-    }
-  }
-}
+constexpr int kK4Tile = 8192;
 
-// =====================================================================================
-// K5  TLq-HS dequantize + reduce + inverse Hadamard (Alg. 3 l.11-13; the H
-// moved after the final reduction).  Row layout (64 elements per thread);
-// sources m'' = 0..M-1 in order (R8); out = rn(H_unnorm(acc) * kappa) (R8).
-// =====================================================================================
 template <int BIN>
-__global__ void __launch_bounds__(kTileRows) k5_tlq_dq_reduce_had(const uint8_t* __restrict__ recv,
-                                                                 size_t in_unit_bytes, int M, size_t S,
-                                                                 int G, int b, float kappa,
-                                                                 float* __restrict__ out,
-                                                                 size_t ntiles) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  constexpr float qin = float((1 << (BIN == 32 ? 1 : BIN - 1)) - 1);
-  constexpr int ROW_BYTES = kRowElems * BIN / 8;
-  const int t = threadIdx.x;
-  const size_t rows_per_shard = S / kRowElems;
-  for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const size_t row0 = tile * kTileRows;
-    const int rows = (int)min((size_t)kTileRows, rows_per_shard - row0);
-    const bool act = t < rows;
-    const size_t row = row0 + t;
-    float v[64];
+struct K4Cfg {
+  static constexpr int CODE_BYTES = kK4Tile * BIN / 8;
+  static constexpr int SC_BYTES = BIN == 32 ? 0 : kK4Tile / 32 * 4;
+  static constexpr int STAGE = CODE_BYTES + SC_BYTES;
+  static constexpr int STAGES = BIN == 32 ? 2 : 4;
+  static constexpr int SMEM = STAGES * STAGE + 64 + 128;
+};
+
+// 16 dequantized elements as 8 pairs of adjacent elements.
+template <int BIN>
+__device__ __forceinline__ void load_vec16(const uint8_t* codes, const float* sc, int e, int lg, float2* x) {
+  if constexpr (BIN == 32) {
 #pragma unroll
-    for (int i = 0; i < 64; ++i) v[i] = 0.f;
+    for (int i = 0; i < 4; ++i) {
+      const float4 f = *reinterpret_cast<const float4*>(codes + (e + 4 * i) * 4);
+      x[2 * i] = make_float2(f.x, f.y);
+      x[2 * i + 1] = make_float2(f.z, f.w);
+    }
+  } else {
+    constexpr float q = float((1 << (BIN - 1)) - 1);
+    const float d = __fdiv_rn(sc[e >> lg], q);
+    float f[16];
+    if constexpr (BIN == 8) {
+      const uint4 w = *reinterpret_cast<const uint4*>(codes + e);
+      dec8x4(w.x, f); dec8x4(w.y, f + 4); dec8x4(w.z, f + 8); dec8x4(w.w, f + 12);
+    } else {
+      const uint2 w = *reinterpret_cast<const uint2*>(codes + e / 2);
+      dec4x8(w.x, f); dec4x8(w.y, f + 8);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = make_float2(__fmul_rn(f[2 * i], d), __fmul_rn(f[2 * i + 1], d));
+  }
+}
+
+template <int BOUT>
+__device__ __forceinline__ void store_vec16(const float2* acc, bool act, int lg, int tpg, float* red, uint8_t* out,
+                                            float* oscales, size_t e) {
+  if constexpr (BOUT == 32) {
     if (act) {
-      for (int m = 0; m < M; ++m) {
-        const uint8_t* unit = recv + (size_t)m * in_unit_bytes;
-        const uint8_t* src = unit + row * ROW_BYTES;
-        if constexpr (BIN == 32) {
+      float4* o = reinterpret_cast<float4*>(out + e * 4);
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const uint4 u = ldg_stream(src + 16 * c);
-            v[4 * c] = __fadd_rn(v[4 * c], __uint_as_float(u.x));
-            v[4 * c + 1] = __fadd_rn(v[4 * c + 1], __uint_as_float(u.y));
-            v[4 * c + 2] = __fadd_rn(v[4 * c + 2], __uint_as_float(u.z));
-            v[4 * c + 3] = __fadd_rn(v[4 * c + 3], __uint_as_float(u.w));
-          }
-        } else {
-          const float* sc = reinterpret_cast<const float*>(unit + S * BIN / 8);
-          float ds0, ds1;
-          if (G >= 64) {
-            ds0 = ds1 = __fdiv_rn(sc[row * kRowElems / G], qin);
-          } else {
-            const float2 s2 = *reinterpret_cast<const float2*>(sc + 2 * row);
-            ds0 = __fdiv_rn(s2.x, qin);
-            ds1 = __fdiv_rn(s2.y, qin);
-          }
+      for (int i = 0; i < 4; ++i) o[i] = make_float4(acc[2 * i].x, acc[2 * i].y, acc[2 * i + 1].x, acc[2 * i + 1].y);
+    }
+  } else {
+    constexpr float q = float((1 << (BOUT - 1)) - 1);
+    float a = 0.f;
 #pragma unroll
-          for (int c = 0; c < ROW_BYTES / 16; ++c) {
-            const uint4 u = ldg_stream(src + 16 * c);
-            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    for (int i = 0; i < 8; ++i) a = max_nan(a, max_nan(fabsf(acc[i].x), fabsf(acc[i].y)));
+    a = group_max(a, tpg, red);
+    const QP p = qparam(a, q);
+    if (act) {
+      const float2 inv = make_float2(p.inv, p.inv);
+      uint32_t r[16];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if constexpr (BIN == 4) {
-                float f[8];
-                dec4x8(w[k], f);
-                const int base = 32 * c + 8 * k;
-                const float ds = base < 32 ? ds0 : ds1;
+      for (int i = 0; i < 8; ++i) {
+        const float2 y = f2rq(acc[i], inv);
+        r[2 * i] = __float_as_uint(y.x);
+        r[2 * i + 1] = __float_as_uint(y.y);
+      }
+      if constexpr (BOUT == 4) {
+        uint2 w = make_uint2(pack4x8(r), pack4x8(r + 8));
+        if (!p.ok) w = make_uint2(0u, 0u);
+        *reinterpret_cast<uint2*>(out + e / 2) = w;
+      } else {
+        uint4 w = make_uint4(pack8x4(r[0], r[1], r[2], r[3]), pack8x4(r[4], r[5], r[6], r[7]),
+                             pack8x4(r[8], r[9], r[10], r[11]), pack8x4(r[12], r[13], r[14], r[15]));
+        if (!p.ok) w = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(out + e) = w;
+      }
+      if ((threadIdx.x & (tpg - 1)) == 0) oscales[e >> lg] = stored_scale(a, 1.f);
+    }
+  }
+}
+
+template <int BIN, int BOUT>
+__global__ void __launch_bounds__(256) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
+                                                          int N, int M, size_t S, int lg,
+                                                          uint8_t* __restrict__ send, size_t out_unit_bytes,
+                                                          uint32_t tpu, uint32_t ntiles) {
+  using C = K4Cfg<BIN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
+  __shared__ float red[8];
+  const int t = threadIdx.x;
+  if (t == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t k) {
+    const uint32_t i = k / N, l = k % N;
+    const uint32_t tile = blockIdx.x + i * gridDim.x;
+    if (tile < ntiles) {
+      const int s = k % STAGES;
+      const uint32_t mp = tile / tpu, ts = tile % tpu;
+      const size_t e0 = (size_t)ts * kK4Tile;
+      const uint32_t n = (uint32_t)min((size_t)kK4Tile, S - e0);
+      const uint8_t* unit = recv + ((size_t)l * M + mp) * in_unit_bytes;
+      const uint32_t cb = n * BIN / 8;
+      uint32_t sb = 0;
+      if constexpr (BIN != 32) sb = (((n >> lg) * 4) + 15) & ~15u;
+      mbar_arrive_tx(&bar[s], cb + sb);
+      bulk_load(smem + s * C::STAGE, unit + e0 * BIN / 8, cb, &bar[s]);
+      if constexpr (BIN != 32)
+        bulk_load(smem + s * C::STAGE + C::CODE_BYTES, unit + S * BIN / 8 + (e0 >> lg) * 4, sb, &bar[s]);
+    }
+  };
+  if (t == 0)
+    for (int k = 0; k < STAGES; ++k) issue(k);
+
+  const int tpg = (1 << lg) >> 4;
+  TileIter it(tpu);
+  uint32_t k = 0;
+  for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i, it.next()) {
+    const uint32_t mp = it.unit, ts = it.ts;
+    const size_t e0 = (size_t)ts * kK4Tile;
+    const int n = (int)min((size_t)kK4Tile, S - e0);
+    const int ea = 16 * t, eb = 4096 + 16 * t;
+    const bool act_a = ea < n, act_b = eb < n;
+    float2 acc_a[8], acc_b[8];
+    for (int l = 0; l < N; ++l, ++k) {
+      const int s = k % STAGES;
+      mbar_wait(&bar[s], (k / STAGES) & 1);
+      const uint8_t* codes = smem + s * C::STAGE;
+      const float* sc = reinterpret_cast<const float*>(codes + C::CODE_BYTES);
+      float2 xa[8], xb[8];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) v[base + i] = __fadd_rn(v[base + i], __fmul_rn(f[i], ds));
-              } else {
-                float f[4];
-                dec8x4(w[k], f);
-                const int base = 16 * c + 4 * k;
-                const float ds = base < 32 ? ds0 : ds1;
+      for (int q = 0; q < 8; ++q) xa[q] = xb[q] = make_float2(0.f, 0.f);
+      if (act_a) load_vec16<BIN>(codes, sc, ea, lg, xa);
+      if (act_b) load_vec16<BIN>(codes, sc, eb, lg, xb);
+      // R8: acc = 0; acc += x_l'' in order.  A dequantized code*ds is never -0 (a zero code
+      // gives +0), so for quantized inputs 0 + x_0 == x_0 and the first add is elided.
+      if (l == 0 && BIN != 32) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) v[base + i] = __fadd_rn(v[base + i], __fmul_rn(f[i], ds));
-              }
-            }
-          }
+        for (int q = 0; q < 8; ++q) { acc_a[q] = xa[q]; acc_b[q] = xb[q]; }
+      } else {
+        if (l == 0) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc_a[q] = acc_b[q] = make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          acc_a[q] = f2add(acc_a[q], xa[q]);
+          acc_b[q] = f2add(acc_b[q], xb[q]);
         }
       }
+      __syncthreads();
+      if (t == 0) issue(k + STAGES);
     }
-    fwht_row(v, b);
-    __syncthreads();  // previous tile's write-out finished reading smem
+    uint8_t* out = send + (size_t)mp * out_unit_bytes;
+    float* oscales = reinterpret_cast<float*>(out + S * BOUT / 8);
+    store_vec16<BOUT>(acc_a, act_a, lg, tpg, red, out, oscales, e0 + ea);
+    store_vec16<BOUT>(acc_b, act_b, lg, tpg, red, out, oscales, e0 + eb);
+  }
+}
+
+// =====================================================================================
+// K5  TLq-HS dequantize + reduce + inverse Hadamard (Alg. 3 l.11-13; H after
+// the final reduction).  Row layout; thread 0 streams (tile, source m'') items
+// through a STAGES-deep ring (TMA tensor load of the codes + 1-D bulk copy of the scales);
+// sources summed in order m'' = 0..M-1 (R8); out = rn(H_unnorm(acc) * kappa) (R8) is
+// written into a double-buffered swizzled smem tile that thread 0 TMA-stores.
+// =====================================================================================
+template <int IN_R>
+struct K5Cfg {
+  static constexpr int IN_TILE = kTileRows * IN_R;
+  static constexpr int SC_BYTES = 2048;  // kTileElems / 32 groups * 4 bytes (G >= 32)
+  static constexpr int STAGE = IN_TILE + SC_BYTES;
+  static constexpr int OUT_TILE = kTileRows * 256;
+  static constexpr int S0 = (200 * 1024 - 2 * OUT_TILE) / STAGE;
+  static constexpr int STAGES = S0 > 6 ? 6 : (S0 < 1 ? 1 : S0);
+  static constexpr int SMEM = STAGES * STAGE + 2 * OUT_TILE + 64 + 1024;
+};
+
+template <int IN_R, int B>
+__global__ void __launch_bounds__(kTileRows, 1)
+    k5_tlq_dq_reduce_had(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
+                         const uint8_t* __restrict__ recv, size_t in_unit_bytes, int M, size_t S, int lg, float kappa,
+                         uint32_t ntiles) {
+  constexpr int BIN = IN_R * 8 / kRowElems;
+  using C = K5Cfg<IN_R>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* out_buf = smem + STAGES * C::STAGE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(out_buf + 2 * C::OUT_TILE);
+  const int t = threadIdx.x;
+  const uint32_t rows_per_shard = (uint32_t)(S / kRowElems);
+  if (t == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t k) {
+    const uint32_t i = k / M, m = k % M;
+    const uint32_t tile = blockIdx.x + i * gridDim.x;
+    if (tile < ntiles) {
+      const int s = k % STAGES;
+      uint32_t sb = 0;
+      if constexpr (BIN != 32) {
+        const uint32_t rows = min((uint32_t)kTileRows, rows_per_shard - tile * kTileRows);
+        sb = (((rows * kRowElems) >> lg) * 4 + 15) & ~15u;
+      }
+      mbar_arrive_tx(&bar[s], C::IN_TILE + sb);
+      tma_load_tile<IN_R>(smem + s * C::STAGE, &in_map, &bar[s], (int)(tile * kTileRows), (int)m);
+      if constexpr (BIN != 32)
+        bulk_load(smem + s * C::STAGE + C::IN_TILE,
+                  recv + (size_t)m * in_unit_bytes + S * BIN / 8 + (((size_t)tile * kTileElems) >> lg) * 4, sb,
+                  &bar[s]);
+    }
+  };
+  if (t == 0)
+    for (int k = 0; k < STAGES; ++k) issue(k);
+
+  constexpr float qin = float((1 << (BIN == 32 ? 1 : BIN - 1)) - 1);
+  uint32_t k = 0;
+  for (uint32_t i = 0;; ++i) {
+    const uint32_t tile = blockIdx.x + i * gridDim.x;
+    if (tile >= ntiles) break;
+    float2 acc[32];
+    for (int m = 0; m < M; ++m, ++k) {
+      const int s = k % STAGES;
+      mbar_wait(&bar[s], (k / STAGES) & 1);
+      const uint8_t* st = smem + s * C::STAGE;
+      float ds0 = 0.f, ds1 = 0.f;
+      if constexpr (BIN != 32) {
+        const float* sc = reinterpret_cast<const float*>(st + C::IN_TILE);
+        if (lg >= 6) {
+          ds0 = ds1 = __fdiv_rn(sc[t >> (lg - 6)], qin);
+        } else {
+          const float2 s2 = *reinterpret_cast<const float2*>(sc + 2 * t);
+          ds0 = __fdiv_rn(s2.x, qin);
+          ds1 = __fdiv_rn(s2.y, qin);
+        }
+      }
+      float2 x[32];
+      dequant_row<BIN, IN_R>(st, t, ds0, ds1, x);
+      // R8 order; the first add 0 + x_0 is exact for quantized inputs (x_0 != -0).
+      if (m == 0 && BIN != 32) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[q] = x[q];
+      } else {
+        if (m == 0) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) acc[q] = make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[q] = f2add(acc[q], x[q]);
+      }
+      if (t == 0 && m == M - 1) bulk_wait_read<1>();  // out_buf[i & 1] released by the store of tile i-2
+      __syncthreads();
+      if (t == 0) issue(k + STAGES);
+    }
+    fwht_pairs<B>(acc);
+    const float2 kk = make_float2(kappa, kappa);
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc[q] = f2mul(acc[q], kk);
+    uint8_t* ot = out_buf + (i & 1) * C::OUT_TILE;
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
-      const float4 o = make_float4(__fmul_rn(v[4 * c], kappa), __fmul_rn(v[4 * c + 1], kappa),
-                                   __fmul_rn(v[4 * c + 2], kappa), __fmul_rn(v[4 * c + 3], kappa));
-      *reinterpret_cast<float4*>(smem + 16 * swz(t, c, 16)) = o;
+      const float2* q = acc + 4 * (c & 7);
+      *reinterpret_cast<float4*>(ot + tile_off<256>(t, c)) =
+          c < 8 ? make_float4(q[0].x, q[1].x, q[2].x, q[3].x) : make_float4(q[0].y, q[1].y, q[2].y, q[3].y);
     }
+    fence_proxy_async();
     __syncthreads();
-    uint8_t* dst = reinterpret_cast<uint8_t*>(out + row0 * kRowElems);
-    for (int i = t; i < rows * 16; i += kTileRows)
-      *reinterpret_cast<uint4*>(dst + 16 * (size_t)i) =
-          *reinterpret_cast<const uint4*>(smem + 16 * swz(i / 16, i % 16, 16));
+    if (t == 0) {
+      tma_store_tile<256>(&out_map, ot, (int)(tile * kTileRows), 0);
+      bulk_commit();
+    }
   }
+  if (t == 0) bulk_wait<0>();
 }
 
 inline int grid_for(size_t ntiles, int cap) {
@@ -623,6 +932,95 @@ cudaError_t set_smem(K kernel, int bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Tensor map over `units` units of `rows` rows of R bytes (row tiles of kTileRows rows).
+cudaError_t make_row_map(CUtensorMap* map, const void* base, int R, uint64_t rows, uint64_t units,
+                         uint64_t unit_stride) {
+  auto fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r;
+  if (R <= 128) {
+    const CUtensorMapSwizzle sw =
+        R == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : (R == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
+    cuuint64_t dims[3] = {(cuuint64_t)R, rows, units};
+    cuuint64_t strides[2] = {(cuuint64_t)R, unit_stride};
+    cuuint32_t box[3] = {(cuuint32_t)R, (cuuint32_t)kTileRows, 1};
+    r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[4] = {128, 2, rows, units};
+    cuuint64_t strides[3] = {128, (cuuint64_t)R, unit_stride};
+    cuuint32_t box[4] = {128, 1, (cuuint32_t)kTileRows, 1};
+    r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+#define SDP4_B_SWITCH(b, ...)                                   \
+  switch (b) {                                                  \
+    case 0: { constexpr int BB = 0; __VA_ARGS__; } break;       \
+    case 2: { constexpr int BB = 2; __VA_ARGS__; } break;       \
+    case 4: { constexpr int BB = 4; __VA_ARGS__; } break;       \
+    case 8: { constexpr int BB = 8; __VA_ARGS__; } break;       \
+    case 16: { constexpr int BB = 16; __VA_ARGS__; } break;     \
+    case 32: { constexpr int BB = 32; __VA_ARGS__; } break;     \
+    case 64: { constexpr int BB = 64; __VA_ARGS__; } break;     \
+    case 128: { constexpr int BB = 128; __VA_ARGS__; } break;   \
+    case 256: { constexpr int BB = 256; __VA_ARGS__; } break;   \
+    default: return cudaErrorInvalidValue;                      \
+  }
+
+template <int IN_R, int BITS, int B>
+cudaError_t k3_launch(const CUtensorMap& in_map, const CUtensorMap& out_map, size_t S, int M, int N, int G, float cb,
+                      uint8_t* intra_send, size_t unit_bytes, uint32_t tps, uint32_t ntiles, int grid,
+                      cudaStream_t st) {
+  constexpr int SMEM = K3Cfg<IN_R, kRowElems * BITS / 8>::SMEM;
+  cudaError_t e = set_smem(k3_tlq_had_quant<IN_R, BITS, B>, SMEM);
+  if (e != cudaSuccess) return e;
+  k3_tlq_had_quant<IN_R, BITS, B><<<grid, kTileRows, SMEM, st>>>(in_map, out_map, S, M, N, __builtin_ctz(G), cb, intra_send,
+                                                                  unit_bytes, tps, ntiles);
+  return cudaGetLastError();
+}
+
+template <int IN_R, int B>
+cudaError_t k5_launch(const CUtensorMap& in_map, const CUtensorMap& out_map, const uint8_t* recv, size_t unit_bytes,
+                      int M, size_t S, int G, float kappa, uint32_t ntiles, int grid, cudaStream_t st) {
+  constexpr int SMEM = K5Cfg<IN_R>::SMEM;
+  cudaError_t e = set_smem(k5_tlq_dq_reduce_had<IN_R, B>, SMEM);
+  if (e != cudaSuccess) return e;
+  k5_tlq_dq_reduce_had<IN_R, B><<<grid, kTileRows, SMEM, st>>>(in_map, out_map, recv, unit_bytes, M, S, __builtin_ctz(G), kappa,
+                                                                ntiles);
+  return cudaGetLastError();
+}
+
+template <int BIN, int BOUT>
+cudaError_t k4_launch(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, uint8_t* send,
+                      size_t out_unit_bytes, int grid_cap, cudaStream_t st) {
+  constexpr int SMEM = K4Cfg<BIN>::SMEM;
+  cudaError_t e = set_smem(k4_tlq_dq_reduce_q<BIN, BOUT>, SMEM);
+  if (e != cudaSuccess) return e;
+  const uint32_t tpu = (uint32_t)((S + kK4Tile - 1) / kK4Tile);
+  const uint32_t ntiles = tpu * (uint32_t)M;
+  const int grid = grid_for(ntiles, grid_cap / 2);
+  k4_tlq_dq_reduce_q<BIN, BOUT><<<grid, 256, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G), send, out_unit_bytes, tpu,
+                                                         ntiles);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 // ------------------------------- launchers -------------------------------------------
@@ -631,7 +1029,7 @@ cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, 
                                 cudaStream_t st) {
   const int grid = grid_for((S + 2047) / 2048, grid_cap);
 #define K1(TM, B) \
-  k1_qwd_quantize<TM, B><<<grid, 256, 0, st>>>(w_main, static_cast<const TM*>(w_model_shard), S, G, unit)
+  k1_qwd_quantize<TM, B><<<grid, 256, 0, st>>>(w_main, static_cast<const TM*>(w_model_shard), S, __builtin_ctz(G), unit)
   if (model_dtype == kBF16) {
     if (bits == 4) K1(uint16_t, 4); else if (bits == 8) K1(uint16_t, 8); else K1(uint16_t, 32);
   } else {
@@ -646,7 +1044,7 @@ cudaError_t launch_qwd_apply(const uint8_t* units, size_t unit_bytes, int P, siz
   const int gx = grid_for((S + 4095) / 4096, (grid_cap + P - 1) / P);
   const dim3 grid(gx, P);
 #define K2(TM, B) \
-  k2_qwd_apply<TM, B><<<grid, 256, 0, st>>>(units, unit_bytes, S, G, static_cast<TM*>(w_model))
+  k2_qwd_apply<TM, B><<<grid, 256, 0, st>>>(units, unit_bytes, S, __builtin_ctz(G), static_cast<TM*>(w_model))
   if (model_dtype == kBF16) {
     if (bits == 4) K2(uint16_t, 4); else if (bits == 8) K2(uint16_t, 8); else K2(uint16_t, 32);
   } else {
@@ -659,62 +1057,58 @@ cudaError_t launch_qwd_apply(const uint8_t* units, size_t unit_bytes, int P, siz
 cudaError_t launch_tlq_had_quant(const void* grad, int grad_dtype, size_t S, int M, int N, int G,
                                  int b, float cb, int bits, uint8_t* intra_send, size_t unit_bytes,
                                  int grid_cap, cudaStream_t st) {
-  const size_t tps = (S / kRowElems + kTileRows - 1) / kTileRows;
-  const size_t ntiles = tps * (size_t)M * N;
-  const int grid = grid_for(ntiles, grid_cap);
-  cudaError_t e = cudaSuccess;
-#define K3(TG, B)                                                                              \
-  do {                                                                                         \
-    const int smem = 2 * kTileRows * kRowElems * (int)sizeof(TG) + kTileRows * kRowElems * B / 8; \
-    e = set_smem(k3_tlq_had_quant<TG, B>, smem);                                               \
-    if (e != cudaSuccess) return e;                                                            \
-    k3_tlq_had_quant<TG, B><<<grid, kTileRows, smem, st>>>(static_cast<const TG*>(grad), S, M, N, \
-                                                           G, b, cb, intra_send, unit_bytes, tps, \
-                                                           ntiles);                            \
-  } while (0)
-  if (grad_dtype == kBF16) {
-    if (bits == 4) K3(uint16_t, 4); else if (bits == 8) K3(uint16_t, 8); else K3(uint16_t, 32);
+  const uint64_t rows = S / kRowElems;
+  const uint32_t tps = (uint32_t)((rows + kTileRows - 1) / kTileRows);
+  const uint32_t ntiles = tps * (uint32_t)(M * N);
+  const int grid = grid_for(ntiles, grid_cap / 8);
+  const int in_r = grad_dtype == kBF16 ? 128 : 256;
+  const int out_r = kRowElems * bits / 8;
+  CUtensorMap in_map, out_map;
+  cudaError_t e = make_row_map(&in_map, grad, in_r, rows, (uint64_t)M * N, (uint64_t)S * (in_r / kRowElems));
+  if (e != cudaSuccess) return e;
+  e = make_row_map(&out_map, intra_send, out_r, rows, (uint64_t)M * N, unit_bytes);
+  if (e != cudaSuccess) return e;
+#define K3(IR, BT) SDP4_B_SWITCH(b, return (k3_launch<IR, BT, BB>(in_map, out_map, S, M, N, G, cb, intra_send, \
+                                                                  unit_bytes, tps, ntiles, grid, st)))
+  if (in_r == 128) {
+    if (bits == 4) { K3(128, 4); } else if (bits == 8) { K3(128, 8); } else { K3(128, 32); }
   } else {
-    if (bits == 4) K3(float, 4); else if (bits == 8) K3(float, 8); else K3(float, 32);
+    if (bits == 4) { K3(256, 4); } else if (bits == 8) { K3(256, 8); } else { K3(256, 32); }
   }
 #undef K3
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_tlq_dq_reduce_q(const uint8_t* intra_recv, size_t in_unit_bytes, int bits_in,
                                    int N, int M, size_t S, int G, uint8_t* inter_send,
                                    size_t out_unit_bytes, int bits_out, int grid_cap,
                                    cudaStream_t st) {
-  const int gx = grid_for((S + 4095) / 4096, (grid_cap + M - 1) / M);
-  const dim3 grid(gx, M);
-#define K4(BI, BO)                                                                          \
-  k4_tlq_dq_reduce_q<BI, BO><<<grid, 256, 0, st>>>(intra_recv, in_unit_bytes, N, M, S, G, \
-                                                    inter_send, out_unit_bytes)
+#define K4(BI, BO) return k4_launch<BI, BO>(intra_recv, in_unit_bytes, N, M, S, G, inter_send, out_unit_bytes, \
+                                            grid_cap, st)
 #define K4O(BI) \
-  if (bits_out == 4) K4(BI, 4); else if (bits_out == 8) K4(BI, 8); else K4(BI, 32)
+  if (bits_out == 4) { K4(BI, 4); } else if (bits_out == 8) { K4(BI, 8); } else { K4(BI, 32); }
   if (bits_in == 4) { K4O(4); } else if (bits_in == 8) { K4O(8); } else { K4O(32); }
 #undef K4O
 #undef K4
-  return cudaGetLastError();
 }
 
 cudaError_t launch_tlq_dq_reduce_had(const uint8_t* inter_recv, size_t in_unit_bytes, int bits_in,
                                      int M, size_t S, int G, int b, float kappa, float* out,
                                      int grid_cap, cudaStream_t st) {
-  const size_t ntiles = (S / kRowElems + kTileRows - 1) / kTileRows;
-  const int grid = grid_for(ntiles, grid_cap);
-  const int smem = kTileRows * kRowElems * 4;
-  cudaError_t e = cudaSuccess;
-#define K5(BI)                                                                                 \
-  do {                                                                                         \
-    e = set_smem(k5_tlq_dq_reduce_had<BI>, smem);                                              \
-    if (e != cudaSuccess) return e;                                                            \
-    k5_tlq_dq_reduce_had<BI><<<grid, kTileRows, smem, st>>>(inter_recv, in_unit_bytes, M, S, G, b, \
-                                                            kappa, out, ntiles);               \
-  } while (0)
-  if (bits_in == 4) K5(4); else if (bits_in == 8) K5(8); else K5(32);
+  const uint64_t rows = S / kRowElems;
+  const uint32_t ntiles = (uint32_t)((rows + kTileRows - 1) / kTileRows);
+  const int grid = grid_for(ntiles, grid_cap / 8);
+  const int in_r = kRowElems * bits_in / 8;
+  CUtensorMap in_map, out_map;
+  cudaError_t e = make_row_map(&in_map, inter_recv, in_r, rows, (uint64_t)M, in_unit_bytes);
+  if (e != cudaSuccess) return e;
+  e = make_row_map(&out_map, out, 256, rows, 1, (uint64_t)S * 4);
+  if (e != cudaSuccess) return e;
+#define K5(IR) SDP4_B_SWITCH(b, return (k5_launch<IR, BB>(in_map, out_map, inter_recv, in_unit_bytes, M, S, G, \
+                                                          kappa, ntiles, grid, st)))
+  if (in_r == 32) { K5(32); } else if (in_r == 64) { K5(64); } else { K5(256); }
 #undef K5
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace sdp4

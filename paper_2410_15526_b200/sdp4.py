@@ -44,6 +44,9 @@ SIGNATURES = {
     "sdp4_qwd_allgather_apply": (_ci, [_vp, _vp, _c_size, _c_size, _ci, _ci, _vp, _ci, _vp]),
     "sdp4_tlq_hs_reduce_scatter": (_ci, [_vp, _vp, _ci, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _u64, _vp, _vp,
                                          _c_size, _vp]),
+    "sdp4_tlq_stage_quantize": (_ci, [_vp, _ci, _c_size, _ci, _ci, _ci, _ci, _ci, _vp, _vp]),
+    "sdp4_tlq_stage_reduce": (_ci, [_vp, _c_size, _ci, _ci, _ci, _ci, _ci, _vp, _vp]),
+    "sdp4_tlq_stage_final": (_ci, [_vp, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _vp, _vp]),
     "sdp4_launch_count": (_u64, [_vp, _ci]),
     "sdp4_profile_enable": (_ci, [_vp, _ci]),
     "sdp4_profile_read": (_ci, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
@@ -109,6 +112,28 @@ def tlq_workspace_bytes(M: int, N: int, numel: int, bits_intra: int, bits_inter:
 
 def tlq_workspace_offset(M, N, numel, bits_intra, bits_inter, group, region) -> int:
     return lib().sdp4_tlq_workspace_offset(M, N, numel, bits_intra, bits_inter, group, region)
+
+
+def tlq_stage_quantize(grad: torch.Tensor, intra_send: torch.Tensor, M: int, N: int, bits_intra: int = 8,
+                       group: int = 128, hadamard_block: int = 64, stream=None):
+    """K3 alone (Alg. 3 l.2-3) on one rank's gradient, no communication."""
+    _check(lib().sdp4_tlq_stage_quantize(_ptr(grad), _DT[grad.dtype], grad.numel(), M, N, bits_intra, group,
+                                         hadamard_block, _ptr(intra_send), _stream(stream)))
+
+
+def tlq_stage_reduce(intra_recv: torch.Tensor, inter_send: torch.Tensor, numel: int, M: int, N: int,
+                     bits_intra: int = 8, bits_inter: int = 4, group: int = 128, stream=None):
+    """K4 alone (Alg. 3 l.5, 7, 9) for one rank, no communication."""
+    _check(lib().sdp4_tlq_stage_reduce(_ptr(intra_recv), numel, M, N, bits_intra, bits_inter, group,
+                                       _ptr(inter_send), _stream(stream)))
+
+
+def tlq_stage_final(inter_recv: torch.Tensor, out_shard: torch.Tensor, numel: int, M: int, N: int,
+                    bits_inter: int = 4, group: int = 128, hadamard_block: int = 64, average: bool = True,
+                    stream=None):
+    """K5 alone (Alg. 3 l.11-13) for one rank, no communication."""
+    _check(lib().sdp4_tlq_stage_final(_ptr(inter_recv), numel, M, N, bits_inter, group, hadamard_block,
+                                      int(bool(average)), _ptr(out_shard), _stream(stream)))
 
 
 def get_unique_id() -> bytes:

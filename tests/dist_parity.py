@@ -1,0 +1,89 @@
+"""Distributed parity of the full NCCL path (run with torchrun, one process per GPU).
+
+    torchrun --nproc-per-node P --master-addr 127.0.0.1 tests/dist_parity.py [--groups M]
+
+Every rank draws all P ranks' synthetic inputs (seeded, CPU), runs
+  qWD:    sdp4_qwd_quantize + sdp4_qwd_allgather_apply  (ncclAllGather)
+  TLq-HS: sdp4_tlq_hs_reduce_scatter                     (2 x ncclAlltoAll, intra/inter split)
+through the C ABI, and checks against the oracle (bit-exact codes/outputs), plus the
+replica identity of w_model across ranks.  Prints one PASS/FAIL line per rank.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_2410_15526_b200 import Comm, default_split  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--groups", type=int, default=None)
+    ap.add_argument("--G", type=int, default=128)
+    ap.add_argument("--b", type=int, default=64)
+    a = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    M, N = default_split(world, a.groups)
+    comm = Comm.from_process_group(a.groups)
+    P, G, b = world, a.G, a.b
+    S = 16384 * 2 + 64 * 5 * max(1, G // 64)
+    S -= S % max(G, 64)
+    D = P * S
+    ok = True
+    msgs = []
+
+    # ---- qWD (Alg. 2 l.2-5)
+    w_model = synth.model_weights(D, seed=1)
+    mains = [synth.main_weights(w_model[r * S:(r + 1) * S], seed=synth.seed_for(r, 2)) for r in range(P)]
+    ws = torch.zeros(comm.qwd_workspace_bytes(D, 4, G), dtype=torch.uint8, device="cuda")
+    wm = w_model.cuda()
+    comm.qwd_quantize(mains[rank].cuda(), wm, ws, 4, G)
+    comm.qwd_allgather_apply(ws, wm, 4, G)
+    torch.cuda.synchronize()
+    _, want = oracle.qwd_step([m.numpy() for m in mains], synth.bf16_bits(w_model), 4, G, model_bf16=True)
+    got = synth.bf16_bits(wm.cpu())
+    if not np.array_equal(got, want):
+        ok = False
+        msgs.append(f"qWD replica differs from oracle in {int(np.sum(got != want))} elements")
+    h = torch.tensor([int(np.uint64(np.sum(got.astype(np.uint64) * np.arange(1, D + 1, dtype=np.uint64))) & 0x7FFFFFFF)],
+                     device="cuda")
+    hs = [torch.zeros_like(h) for _ in range(P)]
+    dist.all_gather(hs, h)
+    if len({int(x.item()) for x in hs}) != 1:
+        ok = False
+        msgs.append("w_model replicas differ across ranks")
+
+    # ---- TLq-HS (Alg. 3)
+    for dtype in (torch.bfloat16, torch.float32):
+        grads = [synth.gradient(D, seed=synth.seed_for(r, 3), dtype=dtype) for r in range(P)]
+        tws = torch.zeros(comm.tlq_workspace_bytes(D, 8, 4, G), dtype=torch.uint8, device="cuda")
+        out = torch.empty(S, dtype=torch.float32, device="cuda")
+        comm.tlq_hs_reduce_scatter(grads[rank].cuda(), out, tws, 8, 4, G, b, True)
+        torch.cuda.synchronize()
+        tr = oracle.tlq_hs_reduce_scatter([g.float().numpy() for g in grads], oracle.Topology(M, N), G, b, 8, 4, True)
+        o = out.cpu().numpy()
+        w = tr.out[rank]
+        same = (o.view(np.uint32) == w.view(np.uint32)) | (np.isnan(o) & np.isnan(w))
+        if not same.all():
+            ok = False
+            msgs.append(f"TLq-HS {dtype} out shard: {int((~same).sum())} of {S} elements differ")
+    comm.close()
+    print(f"rank {rank}/{world} ({M}x{N}) {'PASS' if ok else 'FAIL'} {'; '.join(msgs)}", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,22 @@
+"""Runs tests/dist_parity.py under torchrun when >= 2 GPUs are visible (NCCL path)."""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("nproc,groups", [(2, 1), (2, 2), (4, 2), (4, 1), (4, 4), (8, 2), (8, 4)])
+def test_dist_parity(nproc, groups):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + nproc * 10 + groups}",
+           os.path.join(ROOT, "tests", "dist_parity.py"), "--groups", str(groups)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("PASS") == nproc, r.stdout

@@ -1,0 +1,95 @@
+"""Multi-rank TLq-HS parity on ONE GPU: P = M x N ranks emulated through the stage entry
+points (sdp4_tlq_stage_quantize / _reduce / _final).  The two all-to-alls of Alg. 3
+ are done here by slicing the documented workspace layouts (R9, R15), so
+K3/K4/K5 run with real M, N > 1 (multi-source fp32 reductions, per-shard routing) and are
+compared with the oracle message by message.  The NCCL path itself is covered by
+tests/dist_parity.py (multi-GPU)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2410_15526_b200 import tlq_stage_final, tlq_stage_quantize, tlq_stage_reduce, wire_unit_bytes
+from tests.test_gpu_parity import assert_unit_equal, f32_equal
+
+pytestmark = pytest.mark.gpu
+
+
+def emulate(grads, M, N, bi, be, G, b, average=True):
+    P = M * N
+    D = grads[0].numel()
+    S = D // P
+    w8, w4 = wire_unit_bytes(S, bi, G), wire_unit_bytes(S, be, G)
+    dev = "cuda"
+    intra_send = []
+    for r in range(P):
+        buf = torch.zeros(N * M * w8, dtype=torch.uint8, device=dev)
+        tlq_stage_quantize(grads[r].to(dev), buf, M, N, bi, G, b)
+        intra_send.append(buf)
+    inter_send = []
+    for r in range(P):
+        m, l = divmod(r, N)
+        recv = torch.cat([intra_send[m * N + lpp][l * M * w8:(l + 1) * M * w8] for lpp in range(N)])
+        buf = torch.zeros(M * w4, dtype=torch.uint8, device=dev)
+        tlq_stage_reduce(recv, buf, D, M, N, bi, be, G)
+        inter_send.append(buf)
+    outs = []
+    for r in range(P):
+        m, l = divmod(r, N)
+        recv = torch.cat([inter_send[mpp * N + l][m * w4:(m + 1) * w4] for mpp in range(M)])
+        out = torch.empty(S, dtype=torch.float32, device=dev)
+        tlq_stage_final(recv, out, D, M, N, be, G, b, average)
+        outs.append(out)
+    torch.cuda.synchronize()
+    return ([x.cpu().numpy() for x in intra_send], [x.cpu().numpy() for x in inter_send],
+            [x.cpu().numpy() for x in outs], w8, w4, S)
+
+
+CASES = [  # (M, N, bits_intra, bits_inter, G, b, dtype)
+    (2, 4, 8, 4, 128, 64, torch.bfloat16),
+    (4, 2, 8, 4, 128, 64, torch.bfloat16),
+    (2, 4, 8, 4, 128, 32, torch.float32),
+    (1, 8, 8, 4, 128, 64, torch.bfloat16),
+    (8, 1, 8, 4, 128, 64, torch.bfloat16),
+    (2, 2, 4, 4, 128, 0, torch.float32),      # ULq
+    (3, 2, 8, 4, 64, 16, torch.float32),      # P = 6: kappa = rn(c_b / 6)
+    (2, 4, 8, 4, 256, 256, torch.bfloat16),   # cross-lane Hadamard stages
+    (2, 2, 8, 4, 32, 32, torch.bfloat16),     # two groups per row
+    (2, 2, 32, 32, 128, 64, torch.float32),   # identity codec (R12)
+    (4, 2, 8, 8, 2048, 128, torch.bfloat16),  # large groups (cross-warp K4 group max)
+]
+
+
+@pytest.mark.parametrize("M,N,bi,be,G,b,dtype", CASES)
+def test_tlq_multirank_emulated(M, N, bi, be, G, b, dtype):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    P = M * N
+    align = P * max(G, 64)
+    D = ((16384 * P * 2 + 64 * 37 * P) // align + 1) * align     # > 2 tiles per shard + ragged tail
+    grads = [synth.gradient(D, seed=synth.seed_for(r, 3), dtype=dtype) for r in range(P)]
+    intra, inter, outs, w8, w4, S = emulate(grads, M, N, bi, be, G, b)
+    tr = oracle.tlq_hs_reduce_scatter([g.float().numpy() for g in grads], oracle.Topology(M, N), G, b, bi, be, True)
+    for r in range(P):
+        for lp in range(N):
+            for mp in range(M):
+                off = (lp * M + mp) * w8
+                c, s = tr.intra_send[r][lp][mp]
+                assert_unit_equal(intra[r][off:off + w8], c, s, bi, G, S, f"rank {r} intra block {lp} unit {mp}")
+        for mp in range(M):
+            c, s = tr.inter_send[r][mp]
+            assert_unit_equal(inter[r][mp * w4:(mp + 1) * w4], c, s, be, G, S, f"rank {r} inter unit {mp}")
+        assert f32_equal(outs[r], tr.out[r]), f"rank {r} output shard differs"
+
+
+def test_multirank_matches_exact_mean_within_quantization_error():
+    # end to end sanity at 2 x 4: the emulated outputs approach the exact mean
+    M, N, G, b = 2, 4, 128, 64
+    P = M * N
+    D = P * 16384
+    grads = [synth.gradient(D, seed=100 + r) for r in range(P)]
+    _, _, outs, _, _, S = emulate(grads, M, N, 8, 4, G, b)
+    exact = oracle.exact_reduce_scatter_f64([g.numpy() for g in grads], P)
+    rel = np.linalg.norm(np.concatenate(outs) - np.concatenate(exact)) / np.linalg.norm(np.concatenate(exact))
+    assert rel < 0.2
