@@ -185,68 +185,96 @@ __global__ void __launch_bounds__(256) k1_qwd_quantize(const float* __restrict__
 
 // =====================================================================================
 // K2  qWD apply (Alg. 2 l.5): w_model[jS + e] = bf16_rn(widen(w) + code*rn(s/q))
-// for every shard j (blockIdx.y) of the gathered units.  16 elements per thread.
+// for every shard j (blockIdx.y) of the gathered units.  Each thread updates two
+// 16-element vectors 4096 elements apart per iteration, all loads issued up front.
 // =====================================================================================
+template <int BITS>
+struct K2Vec {
+  static constexpr int CB = BITS == 32 ? 64 : 16 * BITS / 8;  // code bytes per 16 elements
+};
+
 template <typename TM, int BITS>
-__global__ void __launch_bounds__(256) k2_qwd_apply(const uint8_t* __restrict__ units,
-                                                    size_t unit_bytes, size_t S, int lg,
-                                                    TM* __restrict__ w_model) {
+__device__ __forceinline__ void k2_load(const uint8_t* unit, const float* scales, const TM* wm, size_t e, int lg,
+                                        uint4* cw, float& sc, uint4* mw) {
+  if constexpr (BITS == 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cw[i] = *reinterpret_cast<const uint4*>(unit + e * 4 + 16 * i);
+  } else if constexpr (BITS == 8) {
+    cw[0] = *reinterpret_cast<const uint4*>(unit + e);
+    sc = scales[e >> lg];
+  } else {
+    const uint2 w = *reinterpret_cast<const uint2*>(unit + e / 2);
+    cw[0] = make_uint4(w.x, w.y, 0u, 0u);
+    sc = scales[e >> lg];
+  }
+  if constexpr (sizeof(TM) == 2) {
+    mw[0] = *reinterpret_cast<const uint4*>(wm + e);
+    mw[1] = *reinterpret_cast<const uint4*>(wm + e + 8);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mw[i] = *reinterpret_cast<const uint4*>(wm + e + 4 * i);
+  }
+}
+
+template <typename TM, int BITS>
+__device__ __forceinline__ void k2_apply(const uint4* cw, float sc, uint4* mw, TM* wm, size_t e) {
   constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
+  float x[16];
+  if constexpr (BITS == 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[4 * i] = __uint_as_float(cw[i].x); x[4 * i + 1] = __uint_as_float(cw[i].y);
+      x[4 * i + 2] = __uint_as_float(cw[i].z); x[4 * i + 3] = __uint_as_float(cw[i].w);
+    }
+  } else {
+    const float ds = __fdiv_rn(sc, q);
+    float f[16];
+    if constexpr (BITS == 4) {
+      dec4x8(cw[0].x, f);
+      dec4x8(cw[0].y, f + 8);
+    } else {
+      dec8x4(cw[0].x, f); dec8x4(cw[0].y, f + 4); dec8x4(cw[0].z, f + 8); dec8x4(cw[0].w, f + 12);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = __fmul_rn(f[i], ds);  // scalar: the product is added next
+  }
+  if constexpr (sizeof(TM) == 2) {
+    uint32_t* w = &mw[0].x;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      w[i] = pack_bf16x2(__fadd_rn(bf16_lo(w[i]), x[2 * i]), __fadd_rn(bf16_hi(w[i]), x[2 * i + 1]));
+    reinterpret_cast<uint4*>(wm + e)[0] = mw[0];
+    reinterpret_cast<uint4*>(wm + e + 8)[0] = mw[1];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float4 t;
+      t.x = __fadd_rn(__uint_as_float(mw[i].x), x[4 * i]);
+      t.y = __fadd_rn(__uint_as_float(mw[i].y), x[4 * i + 1]);
+      t.z = __fadd_rn(__uint_as_float(mw[i].z), x[4 * i + 2]);
+      t.w = __fadd_rn(__uint_as_float(mw[i].w), x[4 * i + 3]);
+      reinterpret_cast<float4*>(wm + e + 4 * i)[0] = t;
+    }
+  }
+}
+
+template <typename TM, int BITS>
+__global__ void __launch_bounds__(256) k2_qwd_apply(const uint8_t* __restrict__ units, size_t unit_bytes, size_t S,
+                                                    int lg, TM* __restrict__ w_model) {
   const int j = blockIdx.y;
   const uint8_t* unit = units + (size_t)j * unit_bytes;
   const float* scales = reinterpret_cast<const float*>(unit + S * (BITS == 32 ? 4 : BITS) / 8);
   TM* wm = w_model + (size_t)j * S;
-  const size_t ntiles = (S + 4095) / 4096;
+  const size_t ntiles = (S + 8191) / 8192;
   for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const size_t e0 = tile * 4096 + threadIdx.x * 16;
-    if (e0 >= S) continue;
-    float x[16];
-    if constexpr (BITS == 32) {
-      const float4* src = reinterpret_cast<const float4*>(unit + e0 * 4);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float4 t = src[i];
-        x[4 * i] = t.x; x[4 * i + 1] = t.y; x[4 * i + 2] = t.z; x[4 * i + 3] = t.w;
-      }
-    } else {
-      const float ds = __fdiv_rn(scales[e0 >> lg], q);
-      float f[16];
-      if constexpr (BITS == 4) {
-        const uint2 w = *reinterpret_cast<const uint2*>(unit + e0 / 2);
-        dec4x8(w.x, f);
-        dec4x8(w.y, f + 8);
-      } else {
-        const uint4 w = *reinterpret_cast<const uint4*>(unit + e0);
-        dec8x4(w.x, f); dec8x4(w.y, f + 4); dec8x4(w.z, f + 8); dec8x4(w.w, f + 12);
-      }
-#pragma unroll
-      for (int i = 0; i < 16; ++i) x[i] = __fmul_rn(f[i], ds);
-    }
-    if constexpr (sizeof(TM) == 2) {
-      uint4* p = reinterpret_cast<uint4*>(wm + e0);
-      uint4 u0 = p[0], u1 = p[1];
-      uint32_t* w0 = &u0.x;
-      uint32_t* w1 = &u1.x;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        w0[i] = pack_bf16x2(__fadd_rn(bf16_lo(w0[i]), x[2 * i]), __fadd_rn(bf16_hi(w0[i]), x[2 * i + 1]));
-        w1[i] = pack_bf16x2(__fadd_rn(bf16_lo(w1[i]), x[8 + 2 * i]),
-                            __fadd_rn(bf16_hi(w1[i]), x[8 + 2 * i + 1]));
-      }
-      p[0] = u0;
-      p[1] = u1;
-    } else {
-      float4* p = reinterpret_cast<float4*>(wm + e0);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float4 t = p[i];
-        t.x = __fadd_rn(t.x, x[4 * i]);
-        t.y = __fadd_rn(t.y, x[4 * i + 1]);
-        t.z = __fadd_rn(t.z, x[4 * i + 2]);
-        t.w = __fadd_rn(t.w, x[4 * i + 3]);
-        p[i] = t;
-      }
-    }
+    const size_t ea = tile * 8192 + threadIdx.x * 16, eb = ea + 4096;
+    uint4 ca[4], cb[4], ma[4], mb[4];
+    float sa = 0.f, sb = 0.f;
+    const bool aa = ea < S, ab = eb < S;
+    if (aa) k2_load<TM, BITS>(unit, scales, wm, ea, lg, ca, sa, ma);
+    if (ab) k2_load<TM, BITS>(unit, scales, wm, eb, lg, cb, sb, mb);
+    if (aa) k2_apply<TM, BITS>(ca, sa, ma, wm, ea);
+    if (ab) k2_apply<TM, BITS>(cb, sb, mb, wm, eb);
   }
 }
 
@@ -424,6 +452,29 @@ __device__ __forceinline__ void fwht_pairs(float2* p) {
   }
 }
 
+// Code decoding with the exact magic subtraction done by FADD2 (add -> mul cannot contract).
+__device__ __forceinline__ void dec8x4_2(uint32_t w, float* f) {
+  const uint32_t x = w ^ 0x80808080u;
+  const float2 d = make_float2(-kDec8, -kDec8);
+  const float2 a = f2add(make_float2(__uint_as_float(__byte_perm(x, 0x4B000000u, 0x7540)),
+                                     __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7541))), d);
+  const float2 b = f2add(make_float2(__uint_as_float(__byte_perm(x, 0x4B000000u, 0x7542)),
+                                     __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7543))), d);
+  f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+}
+__device__ __forceinline__ void dec4x8_2(uint32_t w, float* f) {
+  const uint32_t x = w ^ 0x88888888u;
+  const uint32_t lo = x & 0x0F0F0F0Fu, hi = (x >> 4) & 0x0F0F0F0Fu;
+  const float2 d = make_float2(-kDec4, -kDec4);
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const float2 v = f2add(make_float2(__uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7540 + b)),
+                                       __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7540 + b))), d);
+    f[2 * b] = v.x;
+    f[2 * b + 1] = v.y;
+  }
+}
+
 // Decode the 64 codes of row t of a row tile (R = 64*BIN/8 bytes) and dequantize:
 // x[i] = {code_i * ds0, code_{i+32} * ds1} (ds0 for elements 0..31, ds1 for 32..63).
 template <int BIN, int R>
@@ -433,9 +484,11 @@ __device__ __forceinline__ void dequant_row(const uint8_t* tile, int t, float ds
   for (int c = 0; c < R / 16; ++c) {
     const uint4 u = *reinterpret_cast<const uint4*>(tile + tile_off<R>(t, c));
     if constexpr (BIN == 4) {
-      dec4x8(u.x, f + 32 * c); dec4x8(u.y, f + 32 * c + 8); dec4x8(u.z, f + 32 * c + 16); dec4x8(u.w, f + 32 * c + 24);
+      dec4x8_2(u.x, f + 32 * c); dec4x8_2(u.y, f + 32 * c + 8); dec4x8_2(u.z, f + 32 * c + 16);
+      dec4x8_2(u.w, f + 32 * c + 24);
     } else if constexpr (BIN == 8) {
-      dec8x4(u.x, f + 16 * c); dec8x4(u.y, f + 16 * c + 4); dec8x4(u.z, f + 16 * c + 8); dec8x4(u.w, f + 16 * c + 12);
+      dec8x4_2(u.x, f + 16 * c); dec8x4_2(u.y, f + 16 * c + 4); dec8x4_2(u.z, f + 16 * c + 8);
+      dec8x4_2(u.w, f + 16 * c + 12);
     } else {
       f[4 * c] = __uint_as_float(u.x); f[4 * c + 1] = __uint_as_float(u.y);
       f[4 * c + 2] = __uint_as_float(u.z); f[4 * c + 3] = __uint_as_float(u.w);
@@ -638,115 +691,74 @@ __global__ void __launch_bounds__(kTileRows, 1)
 
 // =====================================================================================
 // K4  TLq dequantize + reduce + requantize (Alg. 3 l.5, 7, 9, FP32 reduce P:344).
-// Vector layout: a tile is 8192 elements of sub-block m'; thread t owns elements
-// [16t, 16t+16) and [4096+16t, 4096+16t+16).  Thread 0 streams (tile, source l'') items
-// through a STAGES-deep ring of 1-D bulk copies (codes + scales); sources are summed in
-// order l'' = 0..N-1 (R8); the sum is requantized and stored coalesced to unit m' of the
-// inter send buffer.
+// Vector layout: a tile is 8192 elements of sub-block m'; thread t owns the 64 contiguous
+// elements [64t, 64t+64), read from smem as 16-byte chunks in XOR-permuted order
+// (slot c <- chunk c ^ f(t): conflict-free; the permutation is undone by the store
+// addresses).  Thread 0 streams (tile, source l'') items through a STAGES-deep ring of 1-D
+// bulk copies (codes + scales); sources are summed in order l'' = 0..N-1 (R8); the sum is
+// requantized (one division per group) and stored to unit m' of the inter send buffer.
 // =====================================================================================
-constexpr int kK4Tile = 8192;
+constexpr int kK4Threads = 128;
+constexpr int kK4Tile = kK4Threads * 64;
 
 template <int BIN>
 struct K4Cfg {
   static constexpr int CODE_BYTES = kK4Tile * BIN / 8;
   static constexpr int SC_BYTES = BIN == 32 ? 0 : kK4Tile / 32 * 4;
   static constexpr int STAGE = CODE_BYTES + SC_BYTES;
-  static constexpr int STAGES = BIN == 32 ? 2 : 4;
+  static constexpr int STAGES = BIN == 32 ? 2 : (BIN == 8 ? 6 : 8);
   static constexpr int SMEM = STAGES * STAGE + 64 + 128;
+  static constexpr int CPT = 64 * BIN / 8 / 16;   // 16-byte chunks per thread
+  static constexpr int EPC = 64 / CPT;            // elements per chunk
 };
 
-// 16 dequantized elements as 8 pairs of adjacent elements.
-template <int BIN>
-__device__ __forceinline__ void load_vec16(const uint8_t* codes, const float* sc, int e, int lg, float2* x) {
-  if constexpr (BIN == 32) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float4 f = *reinterpret_cast<const float4*>(codes + (e + 4 * i) * 4);
-      x[2 * i] = make_float2(f.x, f.y);
-      x[2 * i + 1] = make_float2(f.z, f.w);
-    }
-  } else {
-    constexpr float q = float((1 << (BIN - 1)) - 1);
-    const float d = __fdiv_rn(sc[e >> lg], q);
-    float f[16];
-    if constexpr (BIN == 8) {
-      const uint4 w = *reinterpret_cast<const uint4*>(codes + e);
-      dec8x4(w.x, f); dec8x4(w.y, f + 4); dec8x4(w.z, f + 8); dec8x4(w.w, f + 12);
-    } else {
-      const uint2 w = *reinterpret_cast<const uint2*>(codes + e / 2);
-      dec4x8(w.x, f); dec4x8(w.y, f + 8);
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = make_float2(__fmul_rn(f[2 * i], d), __fmul_rn(f[2 * i + 1], d));
+// Producer cursor over (tile, source) items of this CTA, advanced without divisions.
+struct ItemCursor {
+  uint32_t l, unit, ts;
+  __device__ void init(uint32_t tpu) {
+    l = 0;
+    unit = blockIdx.x / tpu;
+    ts = blockIdx.x - unit * tpu;
   }
-}
-
-template <int BOUT>
-__device__ __forceinline__ void store_vec16(const float2* acc, bool act, int lg, int tpg, float* red, uint8_t* out,
-                                            float* oscales, size_t e) {
-  if constexpr (BOUT == 32) {
-    if (act) {
-      float4* o = reinterpret_cast<float4*>(out + e * 4);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) o[i] = make_float4(acc[2 * i].x, acc[2 * i].y, acc[2 * i + 1].x, acc[2 * i + 1].y);
-    }
-  } else {
-    constexpr float q = float((1 << (BOUT - 1)) - 1);
-    float a = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) a = max_nan(a, max_nan(fabsf(acc[i].x), fabsf(acc[i].y)));
-    a = group_max(a, tpg, red);
-    const QP p = qparam(a, q);
-    if (act) {
-      const float2 inv = make_float2(p.inv, p.inv);
-      uint32_t r[16];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float2 y = f2rq(acc[i], inv);
-        r[2 * i] = __float_as_uint(y.x);
-        r[2 * i + 1] = __float_as_uint(y.y);
+  __device__ void next(uint32_t n_src, uint32_t tpu) {
+    if (++l == n_src) {
+      l = 0;
+      ts += gridDim.x;
+      while (ts >= tpu) {
+        ts -= tpu;
+        ++unit;
       }
-      if constexpr (BOUT == 4) {
-        uint2 w = make_uint2(pack4x8(r), pack4x8(r + 8));
-        if (!p.ok) w = make_uint2(0u, 0u);
-        *reinterpret_cast<uint2*>(out + e / 2) = w;
-      } else {
-        uint4 w = make_uint4(pack8x4(r[0], r[1], r[2], r[3]), pack8x4(r[4], r[5], r[6], r[7]),
-                             pack8x4(r[8], r[9], r[10], r[11]), pack8x4(r[12], r[13], r[14], r[15]));
-        if (!p.ok) w = make_uint4(0u, 0u, 0u, 0u);
-        *reinterpret_cast<uint4*>(out + e) = w;
-      }
-      if ((threadIdx.x & (tpg - 1)) == 0) oscales[e >> lg] = stored_scale(a, 1.f);
     }
   }
-}
+};
 
 template <int BIN, int BOUT>
-__global__ void __launch_bounds__(256) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
+__global__ void __launch_bounds__(kK4Threads) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
                                                           int N, int M, size_t S, int lg,
                                                           uint8_t* __restrict__ send, size_t out_unit_bytes,
                                                           uint32_t tpu, uint32_t ntiles) {
   using C = K4Cfg<BIN>;
-  constexpr int STAGES = C::STAGES;
+  constexpr int STAGES = C::STAGES, CPT = C::CPT, EPC = C::EPC;
+  constexpr float qin = float((1 << (BIN == 32 ? 1 : BIN - 1)) - 1);
+  constexpr float qout = float((1 << (BOUT == 32 ? 1 : BOUT - 1)) - 1);
+  constexpr float kDec = BIN == 8 ? kDec8 : kDec4;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
-  __shared__ float red[8];
   const int t = threadIdx.x;
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue = [&](uint32_t k) {
-    const uint32_t i = k / N, l = k % N;
-    const uint32_t tile = blockIdx.x + i * gridDim.x;
-    if (tile < ntiles) {
-      const int s = k % STAGES;
-      const uint32_t mp = tile / tpu, ts = tile % tpu;
-      const size_t e0 = (size_t)ts * kK4Tile;
+  ItemCursor pc;
+  uint32_t pk = 0;
+  auto issue = [&]() {  // thread 0: next item of the producer cursor into its ring slot
+    if (pc.unit < (uint32_t)M) {
+      const int s = pk % STAGES;
+      const size_t e0 = (size_t)pc.ts * kK4Tile;
       const uint32_t n = (uint32_t)min((size_t)kK4Tile, S - e0);
-      const uint8_t* unit = recv + ((size_t)l * M + mp) * in_unit_bytes;
+      const uint8_t* unit = recv + ((size_t)pc.l * M + pc.unit) * in_unit_bytes;
       const uint32_t cb = n * BIN / 8;
       uint32_t sb = 0;
       if constexpr (BIN != 32) sb = (((n >> lg) * 4) + 15) & ~15u;
@@ -755,53 +767,175 @@ __global__ void __launch_bounds__(256) k4_tlq_dq_reduce_q(const uint8_t* __restr
       if constexpr (BIN != 32)
         bulk_load(smem + s * C::STAGE + C::CODE_BYTES, unit + S * BIN / 8 + (e0 >> lg) * 4, sb, &bar[s]);
     }
+    ++pk;
+    pc.next(N, tpu);
   };
-  if (t == 0)
-    for (int k = 0; k < STAGES; ++k) issue(k);
+  if (t == 0) {
+    pc.init(tpu);
+    for (int k = 0; k < STAGES; ++k) issue();
+  }
 
-  const int tpg = (1 << lg) >> 4;
+  // slot c of this thread holds chunk c ^ f (f = 0 for the fp32 identity path)
+  const int f = BIN == 32 ? 0 : (CPT >= 8 ? (t & 7) : ((t / (8 / CPT)) & (CPT - 1)));
+  const int tpg = lg >= 6 ? (1 << (lg - 6)) : 1;  // threads per group
   TileIter it(tpu);
   uint32_t k = 0;
   for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i, it.next()) {
-    const uint32_t mp = it.unit, ts = it.ts;
-    const size_t e0 = (size_t)ts * kK4Tile;
-    const int n = (int)min((size_t)kK4Tile, S - e0);
-    const int ea = 16 * t, eb = 4096 + 16 * t;
-    const bool act_a = ea < n, act_b = eb < n;
-    float2 acc_a[8], acc_b[8];
+    const uint32_t mp = it.unit;
+    const size_t e0 = (size_t)it.ts * kK4Tile;
+    const bool act = e0 + 64 * t < S;
+    float2 acc[32];  // slot order: acc[i] = elements (2i, 2i+1) of the slot-ordered 64
     for (int l = 0; l < N; ++l, ++k) {
       const int s = k % STAGES;
       mbar_wait(&bar[s], (k / STAGES) & 1);
-      const uint8_t* codes = smem + s * C::STAGE;
-      const float* sc = reinterpret_cast<const float*>(codes + C::CODE_BYTES);
-      float2 xa[8], xb[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) xa[q] = xb[q] = make_float2(0.f, 0.f);
-      if (act_a) load_vec16<BIN>(codes, sc, ea, lg, xa);
-      if (act_b) load_vec16<BIN>(codes, sc, eb, lg, xb);
-      // R8: acc = 0; acc += x_l'' in order.  A dequantized code*ds is never -0 (a zero code
-      // gives +0), so for quantized inputs 0 + x_0 == x_0 and the first add is elided.
-      if (l == 0 && BIN != 32) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) { acc_a[q] = xa[q]; acc_b[q] = xb[q]; }
-      } else {
-        if (l == 0) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) acc_a[q] = acc_b[q] = make_float2(0.f, 0.f);
+      const uint8_t* codes = smem + s * C::STAGE + t * (64 * BIN / 8);
+      float ds0 = 1.f, ds1 = 1.f;
+      if constexpr (BIN != 32) {
+        const float* sc = reinterpret_cast<const float*>(smem + s * C::STAGE + C::CODE_BYTES);
+        if (lg >= 6) {
+          ds0 = ds1 = __fdiv_rn(sc[(64 * t) >> lg], qin);
+        } else {
+          ds0 = __fdiv_rn(sc[2 * t], qin);
+          ds1 = __fdiv_rn(sc[2 * t + 1], qin);
         }
+      }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          acc_a[q] = f2add(acc_a[q], xa[q]);
-          acc_b[q] = f2add(acc_b[q], xb[q]);
+      for (int c = 0; c < CPT; ++c) {
+        const uint4 u = *reinterpret_cast<const uint4*>(codes + 16 * (c ^ f));
+        float2 xs[EPC / 2];
+        if constexpr (BIN == 32) {
+          xs[0] = make_float2(__uint_as_float(u.x), __uint_as_float(u.y));
+          xs[1] = make_float2(__uint_as_float(u.z), __uint_as_float(u.w));
+        } else {
+          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+          const float2 dec = make_float2(-kDec, -kDec);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if constexpr (BIN == 8) {  // 4 codes
+              const uint32_t xw = w[q] ^ 0x80808080u;
+              xs[2 * q] = f2add(make_float2(__uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7540)),
+                                            __uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7541))), dec);
+              xs[2 * q + 1] = f2add(make_float2(__uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7542)),
+                                                __uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7543))), dec);
+            } else {  // 8 codes
+              const uint32_t xw = w[q] ^ 0x88888888u;
+              const uint32_t lo = xw & 0x0F0F0F0Fu, hi = (xw >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+              for (int b = 0; b < 4; ++b)
+                xs[4 * q + b] = f2add(make_float2(__uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7540 + b)),
+                                                  __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7540 + b))), dec);
+            }
+          }
+          // dequantize: rn(code * ds).  Chunk c holds elements of half ((c ^ f) * EPC) >> 5.
+          const float d = (((c ^ f) * EPC) >> 5) ? ds1 : ds0;
+          if (N == 1) {  // single source: the products are never added -> packed multiply is safe
+#pragma unroll
+            for (int q = 0; q < EPC / 2; ++q) xs[q] = f2mul(xs[q], make_float2(d, d));
+          } else {
+#pragma unroll
+            for (int q = 0; q < EPC / 2; ++q) xs[q] = make_float2(__fmul_rn(xs[q].x, d), __fmul_rn(xs[q].y, d));
+          }
+        }
+        // R8: acc = 0; acc += x_l'' in order.  A dequantized code*ds is never -0 (a zero code
+        // gives +0), so for quantized inputs 0 + x_0 == x_0 and the first add is elided.
+        float2* ac = acc + c * (EPC / 2);
+        if (l == 0 && BIN != 32) {
+#pragma unroll
+          for (int q = 0; q < EPC / 2; ++q) ac[q] = xs[q];
+        } else {
+          if (l == 0) {
+#pragma unroll
+            for (int q = 0; q < EPC / 2; ++q) ac[q] = make_float2(0.f, 0.f);
+          }
+#pragma unroll
+          for (int q = 0; q < EPC / 2; ++q) ac[q] = f2add(ac[q], xs[q]);
         }
       }
       __syncthreads();
-      if (t == 0) issue(k + STAGES);
+      if (t == 0) issue();
     }
+
+    // ---- requantize at BOUT bits; 16-element vectors v = 0..3 in slot order
     uint8_t* out = send + (size_t)mp * out_unit_bytes;
-    float* oscales = reinterpret_cast<float*>(out + S * BOUT / 8);
-    store_vec16<BOUT>(acc_a, act_a, lg, tpg, red, out, oscales, e0 + ea);
-    store_vec16<BOUT>(acc_b, act_b, lg, tpg, red, out, oscales, e0 + eb);
+    auto vbase = [&](int v) {  // element offset (within the thread's 64) of slot-order vector v
+      if constexpr (EPC >= 16) return (((16 * v) / EPC) ^ f) * EPC + (16 * v) % EPC;
+      else return 16 * v;
+    };
+    if constexpr (BOUT == 32) {
+      if (act) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          float4* o = reinterpret_cast<float4*>(out + (e0 + 64 * t + vbase(v)) * 4);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            o[q] = make_float4(acc[8 * v + 2 * q].x, acc[8 * v + 2 * q].y, acc[8 * v + 2 * q + 1].x,
+                               acc[8 * v + 2 * q + 1].y);
+        }
+      }
+    } else {
+      float am[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        float a = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a = max_nan(a, max_nan(fabsf(acc[8 * v + q].x), fabsf(acc[8 * v + q].y)));
+        am[v] = a;
+      }
+      QP p0, p1;
+      float a0, a1;
+      if (lg >= 6) {
+        a0 = max_nan(max_nan(am[0], am[1]), max_nan(am[2], am[3]));
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1)
+          if (off < tpg) a0 = max_nan(a0, __shfl_xor_sync(0xffffffffu, a0, off));
+        a1 = a0;
+        p0 = qparam(a0, qout);
+        p1 = p0;
+      } else {  // G == 32: two groups per thread (element halves)
+        a0 = 0.f;
+        a1 = 0.f;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          if (vbase(v) >> 5) a1 = max_nan(a1, am[v]);
+          else a0 = max_nan(a0, am[v]);
+        }
+        p0 = qparam(a0, qout);
+        p1 = qparam(a1, qout);
+      }
+      if (act) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const bool h = (vbase(v) >> 5) != 0;
+          const float iv = h ? p1.inv : p0.inv;
+          uint32_t r[16];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float2 y = f2rq(acc[8 * v + q], make_float2(iv, iv));
+            r[2 * q] = __float_as_uint(y.x);
+            r[2 * q + 1] = __float_as_uint(y.y);
+          }
+          const bool okv = h ? p1.ok : p0.ok;
+          const size_t e = e0 + 64 * t + vbase(v);
+          if constexpr (BOUT == 4) {
+            uint2 w = make_uint2(pack4x8(r), pack4x8(r + 8));
+            if (!okv) w = make_uint2(0u, 0u);
+            *reinterpret_cast<uint2*>(out + e / 2) = w;
+          } else {
+            uint4 w = make_uint4(pack8x4(r[0], r[1], r[2], r[3]), pack8x4(r[4], r[5], r[6], r[7]),
+                                 pack8x4(r[8], r[9], r[10], r[11]), pack8x4(r[12], r[13], r[14], r[15]));
+            if (!okv) w = make_uint4(0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(out + e) = w;
+          }
+        }
+        float* oscales = reinterpret_cast<float*>(out + S * BOUT / 8);
+        const size_t eg = e0 + 64 * t;
+        if (lg >= 6) {
+          if ((t & (tpg - 1)) == 0) oscales[eg >> lg] = stored_scale(a0, 1.f);
+        } else {
+          *reinterpret_cast<float2*>(oscales + (eg >> 5)) = make_float2(stored_scale(a0, 1.f), stored_scale(a1, 1.f));
+        }
+      }
+    }
   }
 }
 
@@ -1015,8 +1149,8 @@ cudaError_t k4_launch(const uint8_t* recv, size_t in_unit_bytes, int N, int M, s
   if (e != cudaSuccess) return e;
   const uint32_t tpu = (uint32_t)((S + kK4Tile - 1) / kK4Tile);
   const uint32_t ntiles = tpu * (uint32_t)M;
-  const int grid = grid_for(ntiles, grid_cap / 2);
-  k4_tlq_dq_reduce_q<BIN, BOUT><<<grid, 256, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G), send, out_unit_bytes, tpu,
+  const int grid = grid_for(ntiles, grid_cap / 8 * 3);
+  k4_tlq_dq_reduce_q<BIN, BOUT><<<grid, kK4Threads, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G), send, out_unit_bytes, tpu,
                                                          ntiles);
   return cudaGetLastError();
 }
@@ -1041,7 +1175,7 @@ cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, 
 
 cudaError_t launch_qwd_apply(const uint8_t* units, size_t unit_bytes, int P, size_t S, int bits,
                              int G, void* w_model, int model_dtype, int grid_cap, cudaStream_t st) {
-  const int gx = grid_for((S + 4095) / 4096, (grid_cap + P - 1) / P);
+  const int gx = grid_for((S + 8191) / 8192, (grid_cap + P - 1) / P);
   const dim3 grid(gx, P);
 #define K2(TM, B) \
   k2_qwd_apply<TM, B><<<grid, 256, 0, st>>>(units, unit_bytes, S, __builtin_ctz(G), static_cast<TM*>(w_model))

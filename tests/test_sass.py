@@ -1,0 +1,61 @@
+"""Static checks on the built sm_100a SASS of libsdp4.so (no GPU needed).
+
+ptxas 12.9 contracts an f32x2 multiply feeding an f32x2 add into FFMA2 even with .rn and
+--fmad=false, which would change roundings of the numeric contract (R3/R5/R8).
+The kernels therefore only ever issue FFMA2 for the quantizer's explicit fused
+RNE(x * inv) (addend 1.5 * 2^23 = 12582912, R3).  Any other FFMA2 means a product was
+fused into an addition.  Also checks the Blackwell-native evidence: TMA (UTMALDG /
+UTMASTG / UBLKCP) and mbarrier (SYNCS) instructions are present.
+"""
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from paper_2410_15526_b200.sdp4 import LIB_PATH
+
+
+@pytest.fixture(scope="module")
+def sass():
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    r = subprocess.run([exe, "-sass", LIB_PATH], capture_output=True, text=True)
+    if r.returncode != 0:
+        pytest.skip("cuobjdump unavailable: " + r.stderr[:200])
+    return r.stdout
+
+
+def functions(sass):
+    out, name = {}, None
+    for line in sass.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            name = m.group(1)
+            out[name] = []
+        elif name and re.match(r"\s+/\*[0-9a-f]{4}\*/", line):
+            out[name].append(line)
+    return out
+
+
+def test_no_contracted_products(sass):
+    fns = functions(sass)
+    assert fns, "no kernels found"
+    bad = []
+    for name, lines in fns.items():
+        for ln in lines:
+            if "FFMA2" in ln and "12582912" not in ln:
+                bad.append((name[:80], ln.strip()[:100]))
+    assert not bad, bad[:5]
+
+
+def test_blackwell_async_copy_present(sass):
+    fns = functions(sass)
+    k3 = [n for n in fns if "k3_tlq_had_quant" in n]
+    k5 = [n for n in fns if "k5_tlq_dq_reduce_had" in n]
+    k4 = [n for n in fns if "k4_tlq_dq_reduce_q" in n]
+    assert k3 and k4 and k5
+    for n in k3 + k5:
+        body = "\n".join(fns[n])
+        assert "UTMALDG" in body and "UTMASTG" in body and "SYNCS" in body, n
+    for n in k4:
+        assert "UBLKCP" in "\n".join(fns[n]), n
