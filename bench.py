@@ -47,6 +47,10 @@ def parse_args():
     p.add_argument("--bits-w", type=int, default=4)
     p.add_argument("--grad-dtype", default="bf16", choices=["bf16", "fp32"])
     p.add_argument("--model-dtype", default="bf16", choices=["bf16", "fp32"])
+    p.add_argument("--chunks", type=int, default=0, help="pipeline chunks (0 = library default, 1 = off)")
+    p.add_argument("--nccl-ctas", type=int, default=0, help="SMs left to NCCL while pipelining (0 = default)")
+    p.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
+                   help="exchange transport (auto = fused P2P push when available)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-comparators", action="store_true")
@@ -196,7 +200,7 @@ def run_reference(a, rank, world):
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -218,7 +222,9 @@ def run_sdp4(a, rank, world, local_rank):
     mdt = torch.bfloat16 if a.model_dtype == "bf16" else torch.float32
     g_bytes = 2 if gdt == torch.bfloat16 else 4
 
-    comm = Comm.from_process_group(a.groups, dev) if world > 1 else Comm()
+    comm = Comm.from_process_group(a.groups, dev, a.nccl_ctas, a.chunks) if world > 1 else Comm()
+    if world > 1 and a.transport != "auto":
+        comm.set_transport(a.transport)
     lr = synth.GPT_LR.get(a.model, 2e-4)
     # synthetic inputs: w_model identical on all ranks, w_main shard r, grad per rank
     w_model = synth.model_weights(D, seed=synth.seed_for(0, 1), device=dev, dtype=mdt)
@@ -280,10 +286,14 @@ def run_sdp4(a, rank, world, local_rank):
     peak, peak_src = peaks()
     kern = {}
     for name, (tms, cnt) in prof.items():
+        if name.startswith("nccl_"):
+            continue
         kb = kernel_bytes(name, D, S, P, M, N, a)
         avg = tms / max(cnt, 1)
         kern[name] = {"avg_ms": round(avg, 4), "launches": cnt, "share": None,
                       "alg_bytes": kb, "gbs": round(kb / (avg * 1e-3) / 1e9, 1) if kb and avg > 0 else None}
+    comm_ops = {n: {"ms_per_step": round(t / a.steps, 4), "calls": c} for n, (t, c) in prof.items()
+                if n.startswith("nccl_")}
     tot = sum(v["avg_ms"] * v["launches"] for v in kern.values()) or 1.0
     for v in kern.values():
         v["share_of_kernel_time"] = round(v["avg_ms"] * v["launches"] / tot, 4)
@@ -300,11 +310,13 @@ def run_sdp4(a, rank, world, local_rank):
     # unquantized NCCL comparators on the same buffers (sec. 2.1), N > 1 only
     comparators = None
     if world > 1 and not a.no_comparators:
+        # torch.distributed's own NCCL communicator (default configuration, not the
+        # CTA-capped one libsdp4 pipelines with)
         big = torch.empty(D, dtype=torch.float32, device=dev)
         d_shard = torch.empty(S, dtype=torch.float32, device=dev)
         rs_out = torch.empty(S, dtype=gdt, device=dev)
-        t_ag = timed(lambda: comm.nccl_all_gather(d_shard, big), max(3, a.steps // 2))
-        t_rs = timed(lambda: comm.nccl_reduce_scatter(grad, rs_out, True), max(3, a.steps // 2))
+        t_ag = timed(lambda: dist.all_gather_into_tensor(big, d_shard), max(3, a.steps // 2))
+        t_rs = timed(lambda: dist.reduce_scatter_tensor(rs_out, grad, op=dist.ReduceOp.AVG), max(3, a.steps // 2))
         del big
         comparators = {"nccl_all_gather_fp32_ms": round(t_ag, 3), "nccl_reduce_scatter_grad_ms": round(t_rs, 3),
                        "unquantized_ms_per_step": round(t_ag + t_rs, 3),
@@ -342,20 +354,35 @@ def run_sdp4(a, rank, world, local_rank):
                 "warmup": max(3, a.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": workload, "D": D, "D_unpadded": D0, "M": M, "N": N, "G": a.group,
+                           "pipeline_chunks": comm.chunks(D, a.group),
+                           "transport": comm.transport if world > 1 else "local",
                            "G_w": a.qwd_group, "hadamard_block": a.hadamard,
                            "bits": {"qwd": a.bits_w, "intra": a.bits_intra, "inter": a.bits_inter},
                            "grad_dtype": a.grad_dtype, "model_dtype": a.model_dtype,
                            "l2": "inputs larger than L2 (>= 2.6 GB per tensor), no flush",
                            "pre_quant_bytes_per_rank": pre_bytes_rank,
                            "storage": "bf16/fp32 storage, fp32 arithmetic, int8/int4 wire codes"},
-                "clocks": clk.summary(), "gpu_launches": int(launches), "kernels": kern,
+                "clocks": clk.summary(), "gpu_launches": int(launches), "kernels": kern, "comm_ops": comm_ops,
                 "ms_per_step_profiled": round(ms_prof, 4), "roofline": roofline,
                 "e2e": e2e, "comparators": comparators, "cpu_baseline": cpu}
-        print(json.dumps(line), flush=True)
+        emit(line)
     comm.close()
 
 
+_JSON_FD = None
+
+
+def emit(line: dict):
+    """The ONE JSON line of the contract, on the original stdout (library noise such as
+    NCCL's version banner is redirected to stderr in main())."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _JSON_FD
+    _JSON_FD = os.dup(1)
+    sys.stdout.flush()
+    os.dup2(2, 1)
     a = parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -66,9 +66,34 @@ sdp4_status sdp4_get_unique_id(unsigned char id[SDP4_UNIQUE_ID_BYTES]);
  * groups_M * group_size_N must equal world (P = M*N).  For world == 1 the
  * id may be NULL and no NCCL communicator is created.  intra = ncclCommSplit
  * (color = rank / N, key = rank % N); inter = ncclCommSplit(color = rank % N,
- * key = rank / N).  On success *out owns the communicators. */
+ * key = rank / N).  nccl_ctas (0 = default 16): NCCL is capped at that many CTAs
+ * (ncclConfig_t.maxCTAs) and, while a call is pipelined, libsdp4's persistent kernels
+ * leave that many SMs free so the NCCL exchanges run concurrently.
+ * On success *out owns the communicators and an internal high-priority stream. */
 sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, int world,
-                           int groups_M, int group_size_N);
+                           int groups_M, int group_size_N, int nccl_ctas);
+
+/* Host.  Pipelining: every shard is processed in `chunks` sub-ranges (0 = automatic,
+ * about 16M elements per chunk, at most 8; 1 = no pipelining; at most 16); the kernels of
+ * chunk c run on the caller's stream while the exchanges of other chunks run on the
+ * internal stream.  Results do not depend on the chunk count (R16).  World size 1 never
+ * pipelines.  sdp4_comm_chunks returns the chunk count a call with (numel, group) uses. */
+sdp4_status sdp4_comm_set_chunks(sdp4_comm_t comm, int chunks);
+int sdp4_comm_chunks(sdp4_comm_t comm, size_t numel, int group);
+
+/* Host.  Transport of the exchanges (world > 1):
+ *   0 NCCL: kernels write the caller's workspace; ncclAllGather / ncclAlltoAll move it
+ *     (with the chunked two-stream pipeline above);
+ *   1 P2P (default when available: N <= 8, M <= 16, P <= 16): the producing kernel IS the
+ *     exchange -- K1/K3/K4 store their quantized tiles straight into the receive buffers of
+ *     the ranks that own them over NVLink (CUDA IPC).  Those receive buffers are library-
+ *     owned, symmetric, double-buffered by call parity and allocated collectively on first
+ *     use (the caller's workspace is then unused); completion is signalled per source with
+ *     epoch flags (cuStreamWriteValue32 / cuStreamWaitValue32).  P2P never chunks.
+ * Results are bit-identical across transports (R16).  sdp4_comm_transport returns the
+ * current one. */
+sdp4_status sdp4_comm_set_transport(sdp4_comm_t comm, int transport);
+int sdp4_comm_transport(sdp4_comm_t comm);
 
 /* Host, collective.  Destroys the NCCL communicators and frees the comm. */
 sdp4_status sdp4_comm_destroy(sdp4_comm_t comm);
@@ -82,11 +107,14 @@ sdp4_status sdp4_comm_destroy(sdp4_comm_t comm);
  * ------------------------------------------------------------------------- */
 size_t sdp4_wire_unit_bytes(size_t n, int bits, int group);
 
-/* qWD workspace (Alg. 2 l.3-4): P consecutive wire units
- * W(S, bits, G); unit r is rank r's quantized weight difference.  0 on bad args. */
+/* qWD workspace (Alg. 2 l.3-4): per chunk (see sdp4_comm_set_chunks) P
+ * consecutive wire units W(len_chunk, bits, G), unit r = rank r's quantized weight
+ * difference; with one chunk simply P units W(S, bits, G).  The size returned covers any
+ * chunk count.  0 on bad args. */
 size_t sdp4_qwd_workspace_bytes(int world, size_t numel, int bits, int group);
 
-/* TLq-HS workspace (Alg. 3), four regions in this order:
+/* TLq-HS workspace (Alg. 3), per chunk four regions in this order (the size
+ * returned covers any chunk count; the offsets below are those of a one-chunk call):
  *   region 0 intra_send: N blocks of M units W(S, bits_intra, G); block l' unit m'
  *            holds shard m'*N + l' of H(grad) quantized (Alg. 3 l.2-3, R9)
  *   region 1 intra_recv: N blocks of M units (block l'' = from local rank l'')

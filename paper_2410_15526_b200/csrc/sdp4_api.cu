@@ -1,8 +1,31 @@
 // sdp4_api.cu -- the C ABI of include/sdp4.h: argument validation, workspace layout,
 // NCCL communicators (world + intra + inter via ncclCommSplit, sec. 2.3) and the
 // stream-ordered orchestration of Alg. 2 l.2-5 (qWD) and Alg. 3 (TLq-HS).
+//
+// Pipelining (row p of the hot path; the paper overlaps its two all-to-alls):
+// every shard is split into C chunks.  Chunk c is an independent instance of the path on
+// the sub-range [off_c, off_c + len_c) of every shard (groups never straddle chunks, R1),
+// with its own workspace regions.  Kernels run on the caller's stream, NCCL calls on an
+// internal high-priority side stream; CUDA events carry the per-chunk dependencies, and the
+// issue order is software-pipelined (K3(c) | K4(c-1) | K5(c-2) against the exchanges of the
+// chunks in between), so NVLink transfers overlap kernel work.  Kernels leave
+// `nccl_ctas` SMs free and NCCL is capped at that many CTAs, so both make progress.
+// Results are bit-identical for every C (tests/test_gpu_dist.py).
+//
+// Transports.  NCCL: kernels write local send buffers, NCCL moves them (the baseline).
+// P2P (default when world > 1): the producing kernel IS the exchange -- K1 stores its unit
+// into every rank's gather buffer, K3 stores each tile into the receive block of the local
+// rank that owns it, K4 stores each requantized unit into its node's receive slot, all
+// through CUDA-IPC-mapped peer memory over NVLink/NVSwitch, tile by tile while computing.
+// Receive buffers are library-owned, symmetric across ranks and double-buffered by call
+// parity; completion is signalled per (stage, source rank) with an epoch written into the
+// destination's flag word by cuStreamWriteValue32 after the producing kernel, and awaited
+// with cuStreamWaitValue32 before the consuming kernel (no spinning kernels).  Parity
+// double-buffering makes the write-after-read safe: a producer reuses a receive buffer two
+// calls later only after a flag the consumer raised after consuming it.
 #include "sdp4.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -11,12 +34,17 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include "sdp4_kernels.cuh"
 
 namespace {
+
+constexpr int kMaxChunks = 16;
+constexpr int kDefaultNcclCtas = 16;
 
 thread_local std::string g_err;
 
@@ -41,13 +69,78 @@ size_t unit_bytes(size_t n, int bits, int group) {
   return round_up(n * (size_t)bits / 8 + 4 * (n / (size_t)group), 256);
 }
 
+struct Chunk {
+  size_t off, len;
+};
+
+// Split a shard of S elements into at most C chunks aligned to lcm(G, 64) (and to the 16384-
+// element Hadamard tile when the chunks are large enough).
+std::vector<Chunk> plan_chunks(size_t S, int C, int group) {
+  const size_t a0 = (size_t)std::max(group, 64);
+  C = std::max(1, std::min(C, kMaxChunks));
+  size_t align = a0;
+  if (S / C >= 4 * (size_t)sdp4::kTileElems) align = std::max(a0, (size_t)sdp4::kTileElems);
+  const size_t base = round_up((S + C - 1) / C, align);
+  std::vector<Chunk> out;
+  for (size_t off = 0; off < S; off += base) out.push_back({off, std::min(base, S - off)});
+  if (out.empty()) out.push_back({0, S});
+  return out;
+}
+
+// Per-chunk TLq-HS regions (R9, R15): intra_send N*M units, intra_recv (aliased if N == 1),
+// inter_send M units, inter_recv (aliased if M == 1).
+struct TlqRegions {
+  size_t send8, recv8, send4, recv4, end;
+};
+TlqRegions tlq_regions(int M, int N, size_t len, int bi, int be, int group, size_t base) {
+  const size_t w8 = unit_bytes(len, bi, group), w4 = unit_bytes(len, be, group);
+  const size_t intra = (size_t)N * M * w8, inter = (size_t)M * w4;
+  TlqRegions r;
+  r.send8 = base;
+  r.recv8 = N > 1 ? r.send8 + intra : r.send8;
+  r.send4 = r.recv8 + intra;
+  r.recv4 = M > 1 ? r.send4 + inter : r.send4;
+  r.end = r.recv4 + inter;
+  return r;
+}
+
+size_t tlq_total(int M, int N, size_t S, int bi, int be, int group, int C) {
+  size_t base = 0;
+  for (const Chunk& ch : plan_chunks(S, C, group)) base = tlq_regions(M, N, ch.len, bi, be, group, base).end;
+  return base;
+}
+size_t qwd_total(int P, size_t S, int bits, int group, int C) {
+  size_t t = 0;
+  for (const Chunk& ch : plan_chunks(S, C, group)) t += (size_t)P * unit_bytes(ch.len, bits, group);
+  return t;
+}
+
 }  // namespace
+
+// Library-owned receive buffer, mapped on every rank (CUDA IPC).  Layout:
+// [flags: kFlagBytes][parity 0 region][parity 1 region].
+constexpr size_t kFlagBytes = 4096;  // flags[stage][src] uint32, stage < 4, src < 256
+struct SymBuf {
+  uint8_t* local = nullptr;
+  size_t bytes = 0, region = 0;
+  std::vector<uint8_t*> peer;  // peer[r]: rank r's buffer in this process (peer[rank] = local)
+};
+
+enum Transport { kTransportNccl = 0, kTransportP2P = 1 };
 
 struct sdp4_comm {
   int rank = 0, world = 1, M = 1, N = 1, m = 0, l = 0;
+  int transport = kTransportNccl;
+  SymBuf sym_qwd, sym_tlq;
+  uint32_t epoch_qwd = 0, epoch_tlq = 0;
+  PFN_cuStreamWriteValue32_v11070 write_value = nullptr;
+  PFN_cuStreamWaitValue32_v11070 wait_value = nullptr;
   int device = 0;
   int sm_count = 148;
+  int nccl_ctas = kDefaultNcclCtas;
+  int chunks_cfg = 0;  // 0 = auto
   ncclComm_t world_c = nullptr, intra = nullptr, inter = nullptr;
+  cudaStream_t side = nullptr;
   uint64_t launches = 0;
   bool profiling = false;
   struct Pending {
@@ -56,6 +149,8 @@ struct sdp4_comm {
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> pool;
+  std::vector<cudaEvent_t> deps;  // dependency events (timing disabled), reused round-robin
+  size_t dep_next = 0;
   std::map<std::string, std::pair<double, uint64_t>> acc;
   std::vector<std::string> names_keep;
 
@@ -69,7 +164,23 @@ struct sdp4_comm {
     cudaEventCreate(&e);
     return e;
   }
-  int grid_cap() const { return sm_count * 8; }
+  // A dependency event: record on `from`, make `to` wait for it.
+  void link(cudaStream_t from, cudaStream_t to) {
+    if (deps.empty()) {
+      deps.resize(64);
+      for (auto& e : deps) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    }
+    cudaEvent_t e = deps[dep_next++ % deps.size()];
+    cudaEventRecord(e, from);
+    cudaStreamWaitEvent(to, e, 0);
+  }
+  int chunks(size_t S) const {
+    if (world == 1 || transport == kTransportP2P) return 1;
+    if (chunks_cfg > 0) return std::min(chunks_cfg, kMaxChunks);
+    const size_t c = S / ((size_t)16 << 20);  // ~16M elements per chunk and shard
+    return (int)std::max<size_t>(1, std::min<size_t>(c, 8));
+  }
+  int sms(bool overlap) const { return overlap ? std::max(1, sm_count - nccl_ctas) : sm_count; }
 };
 
 namespace {
@@ -98,6 +209,24 @@ sdp4_status nccl_check(ncclResult_t r, const char* what) {
   return SDP4_OK;
 }
 
+// NCCL call on stream `st`, bracketed by profiling events like the kernels.
+template <typename F>
+sdp4_status nccl_op(sdp4_comm* c, const char* name, cudaStream_t st, F&& f) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->profiling) {
+    a = c->ev();
+    b = c->ev();
+    cudaEventRecord(a, st);
+  }
+  sdp4_status s = nccl_check(f(), name);
+  if (s != SDP4_OK) return s;
+  if (c->profiling) {
+    cudaEventRecord(b, st);
+    c->pending.push_back({name, a, b});
+  }
+  return SDP4_OK;
+}
+
 sdp4_status async_check(sdp4_comm* c) {
   ncclComm_t cs[3] = {c->world_c, c->intra, c->inter};
   for (ncclComm_t x : cs) {
@@ -106,6 +235,93 @@ sdp4_status async_check(sdp4_comm* c) {
     ncclCommGetAsyncError(x, &ar);
     if (ar != ncclSuccess && ar != ncclInProgress)
       return fail(SDP4_ENCCL, "asynchronous NCCL error: %s", ncclGetErrorString(ar));
+  }
+  return SDP4_OK;
+}
+
+// Collectively (re)allocate a symmetric buffer with two parity regions of `region` bytes.
+sdp4_status sym_ensure(sdp4_comm* c, SymBuf& b, size_t region, uint32_t* epoch) {
+  if (b.local && region <= b.region) return SDP4_OK;
+  region = round_up(region + region / 16, 1 << 21);
+  cudaError_t e = cudaDeviceSynchronize();  // no kernel of ours still touches the old buffers
+  if (e != cudaSuccess) return fail(SDP4_ECUDA, "sync before symmetric alloc: %s", cudaGetErrorString(e));
+  int* tok = nullptr;
+  cudaMalloc(&tok, sizeof(int) * 64);
+  if (b.local) {  // every rank reached this point: peers are done with the old buffers
+    ncclResult_t r = ncclAllReduce(tok, tok, 1, ncclInt32, ncclSum, c->world_c, c->side);
+    cudaStreamSynchronize(c->side);
+    if (r != ncclSuccess) return fail(SDP4_ENCCL, "barrier: %s", ncclGetErrorString(r));
+    for (int q = 0; q < c->world; ++q)
+      if (q != c->rank && b.peer[q]) cudaIpcCloseMemHandle(b.peer[q]);
+    cudaFree(b.local);
+    b = SymBuf();
+  }
+  const size_t bytes = kFlagBytes + 2 * region;
+  if ((e = cudaMalloc(&b.local, bytes)) != cudaSuccess) {
+    cudaFree(tok);
+    return fail(SDP4_ECUDA, "symmetric buffer of %zu bytes: %s", bytes, cudaGetErrorString(e));
+  }
+  cudaMemset(b.local, 0, kFlagBytes);
+  b.bytes = bytes;
+  b.region = region;
+  *epoch = 0;
+  cudaIpcMemHandle_t h;
+  if ((e = cudaIpcGetMemHandle(&h, b.local)) != cudaSuccess) return fail(SDP4_ECUDA, "ipc handle: %s", cudaGetErrorString(e));
+  uint8_t* dh = nullptr;
+  cudaMalloc(&dh, sizeof(h) * c->world);
+  cudaMemcpy(dh + sizeof(h) * c->rank, &h, sizeof(h), cudaMemcpyHostToDevice);
+  ncclResult_t r = ncclAllGather(dh + sizeof(h) * c->rank, dh, sizeof(h), ncclUint8, c->world_c, c->side);
+  cudaStreamSynchronize(c->side);
+  std::vector<cudaIpcMemHandle_t> all(c->world);
+  cudaMemcpy(all.data(), dh, sizeof(h) * c->world, cudaMemcpyDeviceToHost);
+  cudaFree(dh);
+  cudaFree(tok);
+  if (r != ncclSuccess) return fail(SDP4_ENCCL, "handle exchange: %s", ncclGetErrorString(r));
+  b.peer.assign(c->world, nullptr);
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) {
+      b.peer[q] = b.local;
+      continue;
+    }
+    void* p = nullptr;
+    if ((e = cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess)) != cudaSuccess)
+      return fail(SDP4_ECUDA, "open peer %d buffer: %s (no NVLink P2P? use the NCCL transport)", q,
+                  cudaGetErrorString(e));
+    b.peer[q] = static_cast<uint8_t*>(p);
+  }
+  e = cudaDeviceSynchronize();  // zeroed flags visible on every rank before any peer signals
+  int* tok2 = nullptr;
+  cudaMalloc(&tok2, sizeof(int));
+  ncclResult_t r2 = ncclAllReduce(tok2, tok2, 1, ncclInt32, ncclSum, c->world_c, c->side);
+  cudaStreamSynchronize(c->side);
+  cudaFree(tok2);
+  if (r2 != ncclSuccess) return fail(SDP4_ENCCL, "barrier: %s", ncclGetErrorString(r2));
+  return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "%s", cudaGetErrorString(e));
+}
+
+uint8_t* sym_region(const SymBuf& b, int rank, uint32_t epoch) {
+  return b.peer[rank] + kFlagBytes + (size_t)(epoch & 1) * b.region;
+}
+CUdeviceptr flag_ptr(const SymBuf& b, int owner, int stage, int src) {
+  return (CUdeviceptr)(b.peer[owner] + ((size_t)stage * 256 + src) * sizeof(uint32_t));
+}
+// After the producing kernel on `st`: raise flag[stage][me] on every destination rank.
+sdp4_status signal_peers(sdp4_comm* c, cudaStream_t st, const SymBuf& b, int stage, const std::vector<int>& dsts,
+                         uint32_t epoch) {
+  for (int q : dsts) {
+    if (q == c->rank) continue;
+    CUresult r = c->write_value((CUstream)st, flag_ptr(b, q, stage, c->rank), epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+  }
+  return SDP4_OK;
+}
+// Before the consuming kernel on `st`: wait until every source rank raised its flag.
+sdp4_status wait_peers(sdp4_comm* c, cudaStream_t st, const SymBuf& b, int stage, const std::vector<int>& srcs,
+                       uint32_t epoch) {
+  for (int q : srcs) {
+    if (q == c->rank) continue;
+    CUresult r = c->wait_value((CUstream)st, flag_ptr(b, c->rank, stage, q), epoch, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
   }
   return SDP4_OK;
 }
@@ -135,22 +351,6 @@ sdp4_status check_sizes(int P, size_t numel, int group) {
   return SDP4_OK;
 }
 
-size_t tlq_region(int M, int N, size_t numel, int bi, int be, int group, int region, size_t* total) {
-  const size_t P = (size_t)M * N, S = numel / P;
-  const size_t w8 = unit_bytes(S, bi, group), w4 = unit_bytes(S, be, group);
-  const size_t intra = (size_t)N * M * w8, inter = (size_t)M * w4;
-  size_t off[5];
-  off[0] = 0;
-  off[1] = off[0] + intra;
-  off[2] = off[1] + (N > 1 ? intra : 0);
-  off[3] = off[2] + inter;
-  off[4] = off[3] + (M > 1 ? inter : 0);
-  if (N == 1) off[1] = off[0];
-  if (M == 1) off[3] = off[2];
-  if (total) *total = off[4];
-  return off[region];
-}
-
 sdp4_status check_tlq_args(int P, size_t numel, int bi, int be, int group, int b) {
   if (!valid_bits(bi) || !valid_bits(be)) return fail(SDP4_EINVAL, "bits (%d, %d) not in {4, 8, 32}", bi, be);
   if (b != 0 && (!is_pow2(b) || b < 2 || b > 256))
@@ -174,11 +374,13 @@ int sm_count_current() {
   return n;
 }
 
+size_t esize(sdp4_dtype d) { return d == SDP4_BF16 ? 2 : 4; }
+
 }  // namespace
 
 extern "C" {
 
-int sdp4_version(void) { return 100; }
+int sdp4_version(void) { return 200; }
 
 const char* sdp4_last_error(void) { return g_err.c_str(); }
 
@@ -192,14 +394,15 @@ sdp4_status sdp4_get_unique_id(unsigned char id[SDP4_UNIQUE_ID_BYTES]) {
   return SDP4_OK;
 }
 
-sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, int world,
-                           int groups_M, int group_size_N) {
+sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, int world, int groups_M,
+                           int group_size_N, int nccl_ctas) {
   if (!out) return fail(SDP4_EINVAL, "out is NULL");
   *out = nullptr;
   if (world < 1 || rank < 0 || rank >= world) return fail(SDP4_EINVAL, "bad rank %d / world %d", rank, world);
   if (groups_M < 1 || group_size_N < 1 || groups_M * group_size_N != world)
     return fail(SDP4_EINVAL, "groups_M (%d) * group_size_N (%d) != world (%d)", groups_M, group_size_N, world);
   if (world > 1 && !id) return fail(SDP4_EINVAL, "id is NULL with world > 1");
+  if (nccl_ctas < 0) return fail(SDP4_EINVAL, "nccl_ctas must be >= 0");
   sdp4_comm* c = new sdp4_comm();
   c->rank = rank;
   c->world = world;
@@ -207,20 +410,44 @@ sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, 
   c->N = group_size_N;
   c->m = rank / group_size_N;
   c->l = rank % group_size_N;
+  c->nccl_ctas = nccl_ctas ? nccl_ctas : kDefaultNcclCtas;
   cudaGetDevice(&c->device);
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device);
+  if (c->nccl_ctas >= c->sm_count) c->nccl_ctas = c->sm_count / 2;
   if (world > 1) {
+    void* fw = nullptr;
+    void* fwt = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    cudaGetDriverEntryPoint("cuStreamWriteValue32", &fw, cudaEnableDefault, &q1);
+    cudaGetDriverEntryPoint("cuStreamWaitValue32", &fwt, cudaEnableDefault, &q2);
+    c->write_value = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(fw);
+    c->wait_value = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(fwt);
+    const bool p2p_ok = c->write_value && c->wait_value && group_size_N <= sdp4::kMaxN &&
+                        groups_M <= sdp4::kMaxDests && world <= sdp4::kMaxDests && world <= 256;
+    c->transport = p2p_ok ? kTransportP2P : kTransportNccl;
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi);
     ncclUniqueId u;
     memcpy(&u, id, sizeof(u));
-    sdp4_status s = nccl_check(ncclCommInitRank(&c->world_c, world, u, rank), "ncclCommInitRank");
-    if (s == SDP4_OK && group_size_N > 1)
-      s = nccl_check(ncclCommSplit(c->world_c, c->m, c->l, &c->intra, nullptr), "ncclCommSplit(intra)");
-    if (s == SDP4_OK && groups_M > 1)
-      s = nccl_check(ncclCommSplit(c->world_c, c->l, c->m, &c->inter, nullptr), "ncclCommSplit(inter)");
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.maxCTAs = c->nccl_ctas;
+    sdp4_status s = nccl_check(ncclCommInitRankConfig(&c->world_c, world, u, rank, &cfg), "ncclCommInitRankConfig");
+    if (s == SDP4_OK && group_size_N > 1) {
+      ncclConfig_t cfg2 = NCCL_CONFIG_INITIALIZER;
+      cfg2.maxCTAs = c->nccl_ctas;
+      s = nccl_check(ncclCommSplit(c->world_c, c->m, c->l, &c->intra, &cfg2), "ncclCommSplit(intra)");
+    }
+    if (s == SDP4_OK && groups_M > 1) {
+      ncclConfig_t cfg3 = NCCL_CONFIG_INITIALIZER;
+      cfg3.maxCTAs = c->nccl_ctas;
+      s = nccl_check(ncclCommSplit(c->world_c, c->l, c->m, &c->inter, &cfg3), "ncclCommSplit(inter)");
+    }
     if (s != SDP4_OK) {
       if (c->inter) ncclCommDestroy(c->inter);
       if (c->intra) ncclCommDestroy(c->intra);
       if (c->world_c) ncclCommDestroy(c->world_c);
+      if (c->side) cudaStreamDestroy(c->side);
       delete c;
       return s;
     }
@@ -231,16 +458,50 @@ sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, 
 
 sdp4_status sdp4_comm_destroy(sdp4_comm_t c) {
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
+  if (c->side) cudaStreamSynchronize(c->side);
   for (auto& p : c->pending) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
   }
   for (auto e : c->pool) cudaEventDestroy(e);
+  for (auto e : c->deps) cudaEventDestroy(e);
+  for (SymBuf* b : {&c->sym_qwd, &c->sym_tlq}) {
+    if (!b->local) continue;
+    cudaDeviceSynchronize();
+    for (int q = 0; q < c->world; ++q)
+      if (q != c->rank && b->peer[q]) cudaIpcCloseMemHandle(b->peer[q]);
+    cudaFree(b->local);
+  }
   if (c->inter) ncclCommDestroy(c->inter);
   if (c->intra) ncclCommDestroy(c->intra);
   if (c->world_c) ncclCommDestroy(c->world_c);
+  if (c->side) cudaStreamDestroy(c->side);
   delete c;
   return SDP4_OK;
+}
+
+sdp4_status sdp4_comm_set_chunks(sdp4_comm_t c, int chunks) {
+  if (!c) return fail(SDP4_EINVAL, "comm is NULL");
+  if (chunks < 0 || chunks > kMaxChunks) return fail(SDP4_EINVAL, "chunks %d not in [0, %d]", chunks, kMaxChunks);
+  c->chunks_cfg = chunks;
+  return SDP4_OK;
+}
+
+sdp4_status sdp4_comm_set_transport(sdp4_comm_t c, int transport) {
+  if (!c) return fail(SDP4_EINVAL, "comm is NULL");
+  if (transport != kTransportNccl && transport != kTransportP2P) return fail(SDP4_EINVAL, "bad transport %d", transport);
+  if (transport == kTransportP2P && (c->world == 1 || !c->write_value || c->N > sdp4::kMaxN ||
+                                     c->M > sdp4::kMaxDests || c->world > sdp4::kMaxDests))
+    return fail(SDP4_EINVAL, "P2P transport unavailable for this comm");
+  c->transport = transport;
+  return SDP4_OK;
+}
+
+int sdp4_comm_transport(sdp4_comm_t c) { return c ? c->transport : -1; }
+
+int sdp4_comm_chunks(sdp4_comm_t c, size_t numel, int group) {
+  if (!c || numel % (size_t)c->world) return 0;
+  return (int)plan_chunks(numel / c->world, c->chunks(numel / c->world), group).size();
 }
 
 size_t sdp4_wire_unit_bytes(size_t n, int bits, int group) {
@@ -250,26 +511,29 @@ size_t sdp4_wire_unit_bytes(size_t n, int bits, int group) {
 
 size_t sdp4_qwd_workspace_bytes(int world, size_t numel, int bits, int group) {
   if (world < 1 || !valid_bits(bits) || !is_pow2(group) || numel % (size_t)world) return 0;
-  return (size_t)world * unit_bytes(numel / world, bits, group);
+  size_t m = 0;
+  for (int C = 1; C <= kMaxChunks; ++C) m = std::max(m, qwd_total(world, numel / world, bits, group, C));
+  return m;
 }
 
 size_t sdp4_tlq_workspace_bytes(int M, int N, size_t numel, int bi, int be, int group) {
   if (M < 1 || N < 1 || !valid_bits(bi) || !valid_bits(be) || !is_pow2(group) || numel % ((size_t)M * N))
     return 0;
-  size_t total = 0;
-  tlq_region(M, N, numel, bi, be, group, 0, &total);
-  return total;
+  size_t m = 0;
+  for (int C = 1; C <= kMaxChunks; ++C) m = std::max(m, tlq_total(M, N, numel / ((size_t)M * N), bi, be, group, C));
+  return m;
 }
 
 size_t sdp4_tlq_workspace_offset(int M, int N, size_t numel, int bi, int be, int group, int region) {
   if (region < 0 || region > 3 || sdp4_tlq_workspace_bytes(M, N, numel, bi, be, group) == 0) return 0;
-  return tlq_region(M, N, numel, bi, be, group, region, nullptr);
+  const TlqRegions r = tlq_regions(M, N, numel / ((size_t)M * N), bi, be, group, 0);
+  const size_t offs[4] = {r.send8, r.recv8, r.send4, r.recv4};
+  return offs[region];
 }
 
 sdp4_status sdp4_qwd_quantize(sdp4_comm_t c, const float* w_main_shard, const void* w_model_full,
-                              sdp4_dtype model_dtype, size_t numel, int bits, int group,
-                              sdp4_round rnd, uint64_t seed, void* workspace, size_t workspace_bytes,
-                              void* stream) {
+                              sdp4_dtype model_dtype, size_t numel, int bits, int group, sdp4_round rnd,
+                              uint64_t seed, void* workspace, size_t workspace_bytes, void* stream) {
   (void)seed;
   g_err.clear();
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
@@ -285,19 +549,50 @@ sdp4_status sdp4_qwd_quantize(sdp4_comm_t c, const float* w_main_shard, const vo
   if (workspace_bytes < need) return fail(SDP4_ESTATE, "workspace %zu < %zu bytes", workspace_bytes, need);
   if ((s = async_check(c)) != SDP4_OK) return s;
   const size_t S = numel / c->world;
-  const size_t W = unit_bytes(S, bits, group);
-  const size_t esz = model_dtype == SDP4_BF16 ? 2 : 4;
-  const void* shard = static_cast<const uint8_t*>(w_model_full) + (size_t)c->rank * S * esz;
-  uint8_t* unit = static_cast<uint8_t*>(workspace) + (size_t)c->rank * W;
+  const size_t es = esize(model_dtype);
+  const auto chunks = plan_chunks(S, c->chunks(S), group);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return launch(c, "K1_qwd_quantize", st, [&] {
-    return sdp4::launch_qwd_quantize(w_main_shard, shard, model_dtype, S, bits, group, unit, c->grid_cap(), st);
-  });
+  const int sms = c->sms(chunks.size() > 1);
+  if (c->transport == kTransportP2P) {
+    // Alg. 2 l.2-4 fused: K1 stores unit `rank` into every rank's gather buffer (all-gather
+    // push over NVLink), then raises flag[0][rank] on each peer.
+    const size_t W = unit_bytes(S, bits, group);
+    if ((s = sym_ensure(c, c->sym_qwd, (size_t)c->world * W, &c->epoch_qwd)) != SDP4_OK) return s;
+    const uint32_t ep = ++c->epoch_qwd;
+    sdp4::Dests d;
+    d.n = c->world;
+    d.remote = 0;  // K1 stores are warp-contiguous and go direct to every destination
+    std::vector<int> all(c->world);
+    for (int q = 0; q < c->world; ++q) {
+      d.p[q] = sym_region(c->sym_qwd, q, ep) + (size_t)c->rank * W;
+      all[q] = q;
+    }
+    const void* shard = static_cast<const uint8_t*>(w_model_full) + (size_t)c->rank * S * es;
+    s = launch(c, "K1_qwd_quantize", st, [&] {
+      return sdp4::launch_qwd_quantize(w_main_shard, shard, model_dtype, S, bits, group, d, c->sm_count, st);
+    });
+    if (s != SDP4_OK) return s;
+    return signal_peers(c, st, c->sym_qwd, 0, all, ep);
+  }
+  uint8_t* region = static_cast<uint8_t*>(workspace);
+  for (const Chunk& ch : chunks) {  // Alg. 2 l.2-3 per chunk: unit (chunk, rank)
+    const size_t W = unit_bytes(ch.len, bits, group);
+    const void* shard = static_cast<const uint8_t*>(w_model_full) + ((size_t)c->rank * S + ch.off) * es;
+    sdp4::Dests d;
+    d.n = 1;
+    d.remote = 0;
+    d.p[0] = region + (size_t)c->rank * W;
+    s = launch(c, "K1_qwd_quantize", st, [&] {
+      return sdp4::launch_qwd_quantize(w_main_shard + ch.off, shard, model_dtype, ch.len, bits, group, d, sms, st);
+    });
+    if (s != SDP4_OK) return s;
+    region += (size_t)c->world * W;
+  }
+  return SDP4_OK;
 }
 
-sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes, size_t numel,
-                                     int bits, int group, void* w_model_full, sdp4_dtype model_dtype,
-                                     void* stream) {
+sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes, size_t numel, int bits,
+                                     int group, void* w_model_full, sdp4_dtype model_dtype, void* stream) {
   g_err.clear();
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (!valid_bits(bits)) return fail(SDP4_EINVAL, "bits %d not in {4, 8, 32}", bits);
@@ -310,22 +605,49 @@ sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t c, void* workspace, size_t work
   if (workspace_bytes < need) return fail(SDP4_ESTATE, "workspace %zu < %zu bytes", workspace_bytes, need);
   if ((s = async_check(c)) != SDP4_OK) return s;
   const size_t S = numel / c->world;
-  const size_t W = unit_bytes(S, bits, group);
-  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const size_t es = esize(model_dtype);
+  const auto chunks = plan_chunks(S, c->chunks(S), group);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (c->world > 1) {  // Alg. 2 l.4 AllGather, in place
-    s = nccl_check(ncclAllGather(ws + (size_t)c->rank * W, ws, W, ncclUint8, c->world_c, st), "ncclAllGather");
-    if (s != SDP4_OK) return s;
+  const bool overlap = chunks.size() > 1;
+  const int sms = c->sms(overlap);
+  const int P = c->world;
+  if (c->transport == kTransportP2P) {  // wait for every rank's unit, then K2 on the local copy
+    const size_t W = unit_bytes(S, bits, group);
+    const uint32_t ep = c->epoch_qwd;
+    std::vector<int> all(P);
+    for (int q = 0; q < P; ++q) all[q] = q;
+    if ((s = wait_peers(c, st, c->sym_qwd, 0, all, ep)) != SDP4_OK) return s;
+    uint8_t* units = sym_region(c->sym_qwd, c->rank, ep);
+    return launch(c, "K2_qwd_apply", st, [&] {
+      return sdp4::launch_qwd_apply(units, W, P, S, S, bits, group, w_model_full, model_dtype, c->sm_count, st);
+    });
   }
-  return launch(c, "K2_qwd_apply", st, [&] {
-    return sdp4::launch_qwd_apply(ws, W, c->world, S, bits, group, w_model_full, model_dtype, c->grid_cap(), st);
-  });
+  if (P > 1) c->link(st, c->side);  // the units of every chunk were written on st (K1)
+  uint8_t* region = static_cast<uint8_t*>(workspace);
+  for (const Chunk& ch : chunks) {
+    const size_t W = unit_bytes(ch.len, bits, group);
+    if (P > 1) {  // Alg. 2 l.4 AllGather of chunk c, in place, on the side stream
+      s = nccl_op(c, "nccl_allgather_qwd", c->side, [&] {
+        return ncclAllGather(region + (size_t)c->rank * W, region, W, ncclUint8, c->world_c, c->side);
+      });
+      if (s != SDP4_OK) return s;
+      c->link(c->side, st);
+    }
+    // Alg. 2 l.5 for chunk c: every shard j's sub-range [j*S + off, +len) of the replica
+    uint8_t* wm = static_cast<uint8_t*>(w_model_full) + ch.off * es;
+    s = launch(c, "K2_qwd_apply", st, [&] {
+      return sdp4::launch_qwd_apply(region, W, P, ch.len, S, bits, group, wm, model_dtype, sms, st);
+    });
+    if (s != SDP4_OK) return s;
+    region += (size_t)P * W;
+  }
+  return SDP4_OK;
 }
 
 sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dtype grad_dtype, size_t numel,
-                                       int bits_intra, int bits_inter, int group, int hadamard_block,
-                                       int average, sdp4_round rnd, uint64_t seed, float* out_shard,
-                                       void* workspace, size_t workspace_bytes, void* stream) {
+                                       int bits_intra, int bits_inter, int group, int hadamard_block, int average,
+                                       sdp4_round rnd, uint64_t seed, float* out_shard, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
   (void)seed;
   g_err.clear();
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
@@ -338,49 +660,119 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
   if ((s = check_ptr(out_shard, "out_shard")) != SDP4_OK) return s;
   if ((s = check_ptr(workspace, "workspace")) != SDP4_OK) return s;
   const int M = c->M, N = c->N, P = c->world;
-  size_t need = 0;
-  tlq_region(M, N, numel, bits_intra, bits_inter, group, 0, &need);
+  const size_t need = sdp4_tlq_workspace_bytes(M, N, numel, bits_intra, bits_inter, group);
   if (workspace_bytes < need) return fail(SDP4_ESTATE, "workspace %zu < %zu bytes", workspace_bytes, need);
   if ((s = async_check(c)) != SDP4_OK) return s;
 
   const size_t S = numel / P;
-  const size_t w8 = unit_bytes(S, bits_intra, group), w4 = unit_bytes(S, bits_inter, group);
-  uint8_t* ws = static_cast<uint8_t*>(workspace);
-  uint8_t* intra_send = ws + tlq_region(M, N, numel, bits_intra, bits_inter, group, 0, nullptr);
-  uint8_t* intra_recv = ws + tlq_region(M, N, numel, bits_intra, bits_inter, group, 1, nullptr);
-  uint8_t* inter_send = ws + tlq_region(M, N, numel, bits_intra, bits_inter, group, 2, nullptr);
-  uint8_t* inter_recv = ws + tlq_region(M, N, numel, bits_intra, bits_inter, group, 3, nullptr);
+  const size_t es = esize(grad_dtype);
+  const auto chunks = plan_chunks(S, c->chunks(S), group);
+  const int C = (int)chunks.size();
+  const bool overlap = C > 1;
+  const int sms = c->sms(overlap);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-
+  cudaStream_t cs = P > 1 ? c->side : st;  // communication stream
   const float cb = hadamard_cb(b), kappa = final_kappa(b, P, average);
+  if (c->transport == kTransportP2P) {
+    // Alg. 3 with both all-to-alls fused into the producing kernels (P2P push).
+    const size_t w8 = unit_bytes(S, bits_intra, group), w4 = unit_bytes(S, bits_inter, group);
+    const size_t intra_bytes = (size_t)N * M * w8, inter_bytes = (size_t)M * w4;
+    if ((s = sym_ensure(c, c->sym_tlq, intra_bytes + inter_bytes, &c->epoch_tlq)) != SDP4_OK) return s;
+    const uint32_t ep = ++c->epoch_tlq;
+    const int m = c->m, l = c->l;
+    std::vector<int> group_ranks(N), node_ranks(M);
+    for (int q = 0; q < N; ++q) group_ranks[q] = m * N + q;
+    for (int q = 0; q < M; ++q) node_ranks[q] = q * N + l;
+    // K3: shard m'N + l' -> unit m' of block l (this rank) in rank (m, l')'s intra receive region
+    uint8_t* blocks[sdp4::kMaxN];
+    for (int lp = 0; lp < N; ++lp) blocks[lp] = sym_region(c->sym_tlq, m * N + lp, ep) + (size_t)l * M * w8;
+    const uint32_t remote = ((1u << N) - 1u) & ~(1u << l);
+    s = launch(c, "K3_tlq_had_quant", st, [&] {
+      return sdp4::launch_tlq_had_quant(grad, S, grad_dtype, S, M, N, group, b, cb, bits_intra, blocks, remote, w8,
+                                        c->sm_count, st);
+    });
+    if (s != SDP4_OK) return s;
+    if ((s = signal_peers(c, st, c->sym_tlq, 1, group_ranks, ep)) != SDP4_OK) return s;
+    if ((s = wait_peers(c, st, c->sym_tlq, 1, group_ranks, ep)) != SDP4_OK) return s;
+    // K4: unit m' -> slot m (this node) of rank (m', l)'s inter receive region
+    sdp4::Dests d4;
+    d4.n = M;
+    d4.remote = ((1u << M) - 1u) & ~(1u << m);
+    for (int mp = 0; mp < M; ++mp)
+      d4.p[mp] = sym_region(c->sym_tlq, mp * N + l, ep) + intra_bytes + (size_t)m * w4;
+    uint8_t* my = sym_region(c->sym_tlq, c->rank, ep);
+    s = launch(c, "K4_tlq_dq_reduce_q", st, [&] {
+      return sdp4::launch_tlq_dq_reduce_q(my, w8, bits_intra, N, M, S, group, d4, bits_inter, c->sm_count, st);
+    });
+    if (s != SDP4_OK) return s;
+    if ((s = signal_peers(c, st, c->sym_tlq, 2, node_ranks, ep)) != SDP4_OK) return s;
+    if ((s = wait_peers(c, st, c->sym_tlq, 2, node_ranks, ep)) != SDP4_OK) return s;
+    return launch(c, "K5_tlq_dq_reduce_had", st, [&] {
+      return sdp4::launch_tlq_dq_reduce_had(my + intra_bytes, w4, bits_inter, M, S, group, b, kappa, out_shard,
+                                            c->sm_count, st);
+    });
+  }
+  std::vector<TlqRegions> reg;
+  size_t base = 0;
+  for (const Chunk& ch : chunks) {
+    reg.push_back(tlq_regions(M, N, ch.len, bits_intra, bits_inter, group, base));
+    base = reg.back().end;
+  }
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  if (P > 1) c->link(st, cs);  // order the side stream after the caller's prior work
 
-  // Alg. 3 l.2-3: Hadamard + Quantize8Bit into the intra send layout (K3)
-  s = launch(c, "K3_tlq_had_quant", st, [&] {
-    return sdp4::launch_tlq_had_quant(grad, grad_dtype, S, M, N, group, b, cb, bits_intra, intra_send, w8,
-                                      c->grid_cap(), st);
-  });
-  if (s != SDP4_OK) return s;
-  // Alg. 3 l.4 IntraAlltoAll
-  if (N > 1) {
-    s = nccl_check(ncclAlltoAll(intra_send, intra_recv, (size_t)M * w8, ncclUint8, c->intra, st), "ncclAlltoAll(intra)");
-    if (s != SDP4_OK) return s;
+  auto stage_k3 = [&](int k) -> sdp4_status {  // Alg. 3 l.2-3 + l.4 IntraAlltoAll
+    const Chunk& ch = chunks[k];
+    const size_t w8 = unit_bytes(ch.len, bits_intra, group);
+    uint8_t* blocks[sdp4::kMaxN];
+    for (int lp = 0; lp < N && lp < sdp4::kMaxN; ++lp) blocks[lp] = ws + reg[k].send8 + (size_t)lp * M * w8;
+    sdp4_status r = launch(c, "K3_tlq_had_quant", st, [&] {
+      return sdp4::launch_tlq_had_quant(static_cast<const uint8_t*>(grad) + ch.off * es, S, grad_dtype, ch.len, M, N,
+                                        group, b, cb, bits_intra, blocks, 0u, w8, sms, st);
+    });
+    if (r != SDP4_OK || N == 1) return r;
+    c->link(st, cs);
+    r = nccl_op(c, "nccl_alltoall_intra", cs, [&] {
+      return ncclAlltoAll(ws + reg[k].send8, ws + reg[k].recv8, (size_t)M * w8, ncclUint8, c->intra, cs);
+    });
+    if (r == SDP4_OK) c->link(cs, st);
+    return r;
+  };
+  auto stage_k4 = [&](int k) -> sdp4_status {  // Alg. 3 l.5, 7, 9 + l.10 InterAlltoAll
+    const Chunk& ch = chunks[k];
+    const size_t w8 = unit_bytes(ch.len, bits_intra, group), w4 = unit_bytes(ch.len, bits_inter, group);
+    sdp4::Dests d4;
+    d4.n = M;
+    d4.remote = 0;
+    for (int mp = 0; mp < M && mp < sdp4::kMaxDests; ++mp) d4.p[mp] = ws + reg[k].send4 + (size_t)mp * w4;
+    sdp4_status r = launch(c, "K4_tlq_dq_reduce_q", st, [&] {
+      return sdp4::launch_tlq_dq_reduce_q(ws + reg[k].recv8, w8, bits_intra, N, M, ch.len, group, d4, bits_inter, sms,
+                                          st);
+    });
+    if (r != SDP4_OK || M == 1) return r;
+    c->link(st, cs);
+    r = nccl_op(c, "nccl_alltoall_inter", cs, [&] {
+      return ncclAlltoAll(ws + reg[k].send4, ws + reg[k].recv4, w4, ncclUint8, c->inter, cs);
+    });
+    if (r == SDP4_OK) c->link(cs, st);
+    return r;
+  };
+  auto stage_k5 = [&](int k) -> sdp4_status {  // Alg. 3 l.11-13
+    const Chunk& ch = chunks[k];
+    const size_t w4 = unit_bytes(ch.len, bits_inter, group);
+    return launch(c, "K5_tlq_dq_reduce_had", st, [&] {
+      return sdp4::launch_tlq_dq_reduce_had(ws + reg[k].recv4, w4, bits_inter, M, ch.len, group, b, kappa,
+                                            out_shard + ch.off, sms, st);
+    });
+  };
+  // Software pipeline: at step i issue K3(i), K4(i-1), K5(i-2).  Each stream executes in
+  // order; every wait targets an event recorded earlier in issue order (no cycles).
+  for (int i = 0; i < C + 2; ++i) {
+    if (i < C && (s = stage_k3(i)) != SDP4_OK) return s;
+    if (i - 1 >= 0 && i - 1 < C && (s = stage_k4(i - 1)) != SDP4_OK) return s;
+    if (i - 2 >= 0 && i - 2 < C && (s = stage_k5(i - 2)) != SDP4_OK) return s;
   }
-  // Alg. 3 l.5, 7, 9: Dequantize + Reduction + Quantize4Bit (K4)
-  s = launch(c, "K4_tlq_dq_reduce_q", st, [&] {
-    return sdp4::launch_tlq_dq_reduce_q(intra_recv, w8, bits_intra, N, M, S, group, inter_send, w4, bits_inter,
-                                        c->grid_cap(), st);
-  });
-  if (s != SDP4_OK) return s;
-  // Alg. 3 l.10 InterAlltoAll
-  if (M > 1) {
-    s = nccl_check(ncclAlltoAll(inter_send, inter_recv, w4, ncclUint8, c->inter, st), "ncclAlltoAll(inter)");
-    if (s != SDP4_OK) return s;
-  }
-  // Alg. 3 l.11-13: Dequantize + Reduction + Hadamard (K5)
-  return launch(c, "K5_tlq_dq_reduce_had", st, [&] {
-    return sdp4::launch_tlq_dq_reduce_had(inter_recv, w4, bits_inter, M, S, group, b, kappa, out_shard,
-                                          c->grid_cap(), st);
-  });
+  return SDP4_OK;
 }
 
 sdp4_status sdp4_tlq_stage_quantize(const void* grad, sdp4_dtype grad_dtype, size_t numel, int M, int N,
@@ -394,10 +786,13 @@ sdp4_status sdp4_tlq_stage_quantize(const void* grad, sdp4_dtype grad_dtype, siz
   if ((s = check_ptr(intra_send, "intra_send")) != SDP4_OK) return s;
   const size_t S = numel / ((size_t)M * N);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = sdp4::launch_tlq_had_quant(grad, grad_dtype, S, M, N, group, hadamard_block,
-                                             hadamard_cb(hadamard_block), bits_intra,
-                                             static_cast<uint8_t*>(intra_send), unit_bytes(S, bits_intra, group),
-                                             sm_count_current() * 8, st);
+  if (N > sdp4::kMaxN) return fail(SDP4_EINVAL, "group_size_N %d > %d", N, sdp4::kMaxN);
+  const size_t w8 = unit_bytes(S, bits_intra, group);
+  uint8_t* blocks[sdp4::kMaxN];
+  for (int lp = 0; lp < N; ++lp) blocks[lp] = static_cast<uint8_t*>(intra_send) + (size_t)lp * M * w8;
+  cudaError_t e = sdp4::launch_tlq_had_quant(grad, S, grad_dtype, S, M, N, group, hadamard_block,
+                                             hadamard_cb(hadamard_block), bits_intra, blocks, 0u, w8,
+                                             sm_count_current(), st);
   return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "K3 launch failed: %s", cudaGetErrorString(e));
 }
 
@@ -411,10 +806,14 @@ sdp4_status sdp4_tlq_stage_reduce(const void* intra_recv, size_t numel, int M, i
   if ((s = check_ptr(inter_send, "inter_send")) != SDP4_OK) return s;
   const size_t S = numel / ((size_t)M * N);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (M > sdp4::kMaxDests) return fail(SDP4_EINVAL, "groups_M %d > %d", M, sdp4::kMaxDests);
+  sdp4::Dests d4;
+  d4.n = M;
+  d4.remote = 0;
+  for (int mp = 0; mp < M; ++mp) d4.p[mp] = static_cast<uint8_t*>(inter_send) + (size_t)mp * unit_bytes(S, bits_inter, group);
   cudaError_t e = sdp4::launch_tlq_dq_reduce_q(static_cast<const uint8_t*>(intra_recv),
-                                               unit_bytes(S, bits_intra, group), bits_intra, N, M, S, group,
-                                               static_cast<uint8_t*>(inter_send), unit_bytes(S, bits_inter, group),
-                                               bits_inter, sm_count_current() * 8, st);
+                                               unit_bytes(S, bits_intra, group), bits_intra, N, M, S, group, d4,
+                                               bits_inter, sm_count_current(), st);
   return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "K4 launch failed: %s", cudaGetErrorString(e));
 }
 
@@ -431,7 +830,7 @@ sdp4_status sdp4_tlq_stage_final(const void* inter_recv, size_t numel, int M, in
   cudaError_t e = sdp4::launch_tlq_dq_reduce_had(static_cast<const uint8_t*>(inter_recv),
                                                  unit_bytes(S, bits_inter, group), bits_inter, M, S, group,
                                                  hadamard_block, final_kappa(hadamard_block, M * N, average),
-                                                 out_shard, sm_count_current() * 8, st);
+                                                 out_shard, sm_count_current(), st);
   return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "K5 launch failed: %s", cudaGetErrorString(e));
 }
 
@@ -485,8 +884,7 @@ sdp4_status sdp4_nccl_reduce_scatter(sdp4_comm_t c, const void* send, void* recv
   const ncclDataType_t dt = dtype == SDP4_BF16 ? ncclBfloat16 : ncclFloat32;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (c->world == 1) {
-    const size_t bytes = numel * (dtype == SDP4_BF16 ? 2 : 4);
-    cudaError_t e = cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st);
+    cudaError_t e = cudaMemcpyAsync(recv, send, numel * esize(dtype), cudaMemcpyDeviceToDevice, st);
     return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "%s", cudaGetErrorString(e));
   }
   return nccl_check(ncclReduceScatter(send, recv, numel / c->world, dt, average ? ncclAvg : ncclSum, c->world_c, st),
@@ -500,8 +898,7 @@ sdp4_status sdp4_nccl_all_gather(sdp4_comm_t c, const void* send, void* recv, si
   const ncclDataType_t dt = dtype == SDP4_BF16 ? ncclBfloat16 : ncclFloat32;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (c->world == 1) {
-    const size_t bytes = numel * (dtype == SDP4_BF16 ? 2 : 4);
-    cudaError_t e = cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st);
+    cudaError_t e = cudaMemcpyAsync(recv, send, numel * esize(dtype), cudaMemcpyDeviceToDevice, st);
     return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "%s", cudaGetErrorString(e));
   }
   return nccl_check(ncclAllGather(send, recv, numel / c->world, dt, c->world_c, st), "ncclAllGather");

@@ -20,6 +20,7 @@
 #include "sdp4_kernels.cuh"
 
 #include <cfloat>
+#include <cstring>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -112,173 +113,6 @@ __device__ __forceinline__ float group_max(float v, int tpg, float* red) {
 }
 
 // =====================================================================================
-// K1  qWD quantize (Alg. 2 l.2-3, P:259-260): d = rn(w_main - widen(w_model)),
-// per G-group s = max|d|, codes = RNE(d * rn(q/s)).  8 elements per thread, a group is
-// G/8 consecutive threads.  Output: one wire unit [codes][scales].
-// =====================================================================================
-template <typename TM, int BITS>
-__global__ void __launch_bounds__(256) k1_qwd_quantize(const float* __restrict__ w_main,
-                                                       const TM* __restrict__ w_model, size_t S,
-                                                       int lg, uint8_t* __restrict__ unit) {
-  __shared__ float red[8];
-  constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
-  const int tpg = (1 << lg) >> 3;
-  const size_t ntiles = (S + 2047) / 2048;
-  float* scales = reinterpret_cast<float*>(unit + S * (BITS == 32 ? 4 : BITS) / 8);
-  for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const size_t e0 = tile * 2048 + threadIdx.x * 8;
-    const bool act = e0 < S;
-    float d[8];
-    if (act) {
-      const float4 a0 = *reinterpret_cast<const float4*>(w_main + e0);
-      const float4 a1 = *reinterpret_cast<const float4*>(w_main + e0 + 4);
-      float m[8];
-      if constexpr (sizeof(TM) == 2) {
-        const uint4 u = *reinterpret_cast<const uint4*>(w_model + e0);
-        m[0] = bf16_lo(u.x); m[1] = bf16_hi(u.x); m[2] = bf16_lo(u.y); m[3] = bf16_hi(u.y);
-        m[4] = bf16_lo(u.z); m[5] = bf16_hi(u.z); m[6] = bf16_lo(u.w); m[7] = bf16_hi(u.w);
-      } else {
-        const float4 b0 = *reinterpret_cast<const float4*>(w_model + e0);
-        const float4 b1 = *reinterpret_cast<const float4*>(w_model + e0 + 4);
-        m[0] = b0.x; m[1] = b0.y; m[2] = b0.z; m[3] = b0.w;
-        m[4] = b1.x; m[5] = b1.y; m[6] = b1.z; m[7] = b1.w;
-      }
-      d[0] = __fsub_rn(a0.x, m[0]); d[1] = __fsub_rn(a0.y, m[1]);
-      d[2] = __fsub_rn(a0.z, m[2]); d[3] = __fsub_rn(a0.w, m[3]);
-      d[4] = __fsub_rn(a1.x, m[4]); d[5] = __fsub_rn(a1.y, m[5]);
-      d[6] = __fsub_rn(a1.z, m[6]); d[7] = __fsub_rn(a1.w, m[7]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) d[i] = 0.f;
-    }
-    if constexpr (BITS == 32) {  // identity codec (R12): the wire carries d itself
-      if (act) {
-        float4* o = reinterpret_cast<float4*>(unit + e0 * 4);
-        o[0] = make_float4(d[0], d[1], d[2], d[3]);
-        o[1] = make_float4(d[4], d[5], d[6], d[7]);
-      }
-      continue;
-    } else {
-      float a = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a = max_nan(a, fabsf(d[i]));
-      a = group_max(a, tpg, red);
-      const QP p = qparam(a, q);
-      if (act) {
-        uint32_t r[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) r[i] = rq(d[i], p.inv);
-        if constexpr (BITS == 4) {
-          uint32_t w = pack4x8(r);
-          if (!p.ok) w = 0u;
-          *reinterpret_cast<uint32_t*>(unit + e0 / 2) = w;
-        } else {
-          uint2 w = make_uint2(pack8x4(r[0], r[1], r[2], r[3]), pack8x4(r[4], r[5], r[6], r[7]));
-          if (!p.ok) w = make_uint2(0u, 0u);
-          *reinterpret_cast<uint2*>(unit + e0) = w;
-        }
-        if ((threadIdx.x & (tpg - 1)) == 0) scales[e0 >> lg] = stored_scale(a, 1.f);
-      }
-    }
-  }
-}
-
-// =====================================================================================
-// K2  qWD apply (Alg. 2 l.5, P:262): w_model[jS + e] = bf16_rn(widen(w) + code*rn(s/q))
-// for every shard j (blockIdx.y) of the gathered units.  Each thread updates two
-// 16-element vectors 4096 elements apart per iteration, all loads issued up front.
-// =====================================================================================
-template <int BITS>
-struct K2Vec {
-  static constexpr int CB = BITS == 32 ? 64 : 16 * BITS / 8;  // code bytes per 16 elements
-};
-
-template <typename TM, int BITS>
-__device__ __forceinline__ void k2_load(const uint8_t* unit, const float* scales, const TM* wm, size_t e, int lg,
-                                        uint4* cw, float& sc, uint4* mw) {
-  if constexpr (BITS == 32) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) cw[i] = *reinterpret_cast<const uint4*>(unit + e * 4 + 16 * i);
-  } else if constexpr (BITS == 8) {
-    cw[0] = *reinterpret_cast<const uint4*>(unit + e);
-    sc = scales[e >> lg];
-  } else {
-    const uint2 w = *reinterpret_cast<const uint2*>(unit + e / 2);
-    cw[0] = make_uint4(w.x, w.y, 0u, 0u);
-    sc = scales[e >> lg];
-  }
-  if constexpr (sizeof(TM) == 2) {
-    mw[0] = *reinterpret_cast<const uint4*>(wm + e);
-    mw[1] = *reinterpret_cast<const uint4*>(wm + e + 8);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) mw[i] = *reinterpret_cast<const uint4*>(wm + e + 4 * i);
-  }
-}
-
-template <typename TM, int BITS>
-__device__ __forceinline__ void k2_apply(const uint4* cw, float sc, uint4* mw, TM* wm, size_t e) {
-  constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
-  float x[16];
-  if constexpr (BITS == 32) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      x[4 * i] = __uint_as_float(cw[i].x); x[4 * i + 1] = __uint_as_float(cw[i].y);
-      x[4 * i + 2] = __uint_as_float(cw[i].z); x[4 * i + 3] = __uint_as_float(cw[i].w);
-    }
-  } else {
-    const float ds = __fdiv_rn(sc, q);
-    float f[16];
-    if constexpr (BITS == 4) {
-      dec4x8(cw[0].x, f);
-      dec4x8(cw[0].y, f + 8);
-    } else {
-      dec8x4(cw[0].x, f); dec8x4(cw[0].y, f + 4); dec8x4(cw[0].z, f + 8); dec8x4(cw[0].w, f + 12);
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) x[i] = __fmul_rn(f[i], ds);  // scalar: the product is added next
-  }
-  if constexpr (sizeof(TM) == 2) {
-    uint32_t* w = &mw[0].x;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      w[i] = pack_bf16x2(__fadd_rn(bf16_lo(w[i]), x[2 * i]), __fadd_rn(bf16_hi(w[i]), x[2 * i + 1]));
-    reinterpret_cast<uint4*>(wm + e)[0] = mw[0];
-    reinterpret_cast<uint4*>(wm + e + 8)[0] = mw[1];
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float4 t;
-      t.x = __fadd_rn(__uint_as_float(mw[i].x), x[4 * i]);
-      t.y = __fadd_rn(__uint_as_float(mw[i].y), x[4 * i + 1]);
-      t.z = __fadd_rn(__uint_as_float(mw[i].z), x[4 * i + 2]);
-      t.w = __fadd_rn(__uint_as_float(mw[i].w), x[4 * i + 3]);
-      reinterpret_cast<float4*>(wm + e + 4 * i)[0] = t;
-    }
-  }
-}
-
-template <typename TM, int BITS>
-__global__ void __launch_bounds__(256) k2_qwd_apply(const uint8_t* __restrict__ units, size_t unit_bytes, size_t S,
-                                                    int lg, TM* __restrict__ w_model) {
-  const int j = blockIdx.y;
-  const uint8_t* unit = units + (size_t)j * unit_bytes;
-  const float* scales = reinterpret_cast<const float*>(unit + S * (BITS == 32 ? 4 : BITS) / 8);
-  TM* wm = w_model + (size_t)j * S;
-  const size_t ntiles = (S + 8191) / 8192;
-  for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const size_t ea = tile * 8192 + threadIdx.x * 16, eb = ea + 4096;
-    uint4 ca[4], cb[4], ma[4], mb[4];
-    float sa = 0.f, sb = 0.f;
-    const bool aa = ea < S, ab = eb < S;
-    if (aa) k2_load<TM, BITS>(unit, scales, wm, ea, lg, ca, sa, ma);
-    if (ab) k2_load<TM, BITS>(unit, scales, wm, eb, lg, cb, sb, mb);
-    if (aa) k2_apply<TM, BITS>(ca, sa, ma, wm, ea);
-    if (ab) k2_apply<TM, BITS>(cb, sb, mb, wm, eb);
-  }
-}
-
-// =====================================================================================
 // TMA (cp.async.bulk[.tensor]) + mbarrier primitives (sm_90+ PTX, used on sm_100a).
 // =====================================================================================
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -333,6 +167,13 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// 1-D bulk copy shared -> global (local or peer memory over NVLink; 16-byte aligned,
+// size a multiple of 16)
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -345,6 +186,22 @@ __device__ __forceinline__ void bulk_wait() {
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// Store a finished output tile staged in smem -- `cbytes` code bytes and `nsc` fp32 scales
+// -- to one destination unit with 1-D bulk copies issued by thread 0 (the 16-byte multiple
+// prefix of the scales; the < 4 trailing scales are stored by lanes of warp 1).  The caller
+// has done fence_proxy_async + __syncthreads, and thread 0 commits the bulk group after
+// the last destination.  Contiguous bulk stores keep NVLink transfers at full efficiency.
+__device__ __forceinline__ void store_tile(const uint8_t* s_codes, uint32_t cbytes, const float* s_sc, uint32_t nsc,
+                                           uint8_t* g_codes, float* g_sc) {
+  const uint32_t n16 = nsc & ~3u;
+  if (threadIdx.x == 0) {
+    bulk_store(g_codes, s_codes, cbytes);
+    if (n16) bulk_store(g_sc, s_sc, n16 * 4);
+  }
+  const int k = (int)threadIdx.x - 32;
+  if (k >= 0 && k < (int)(nsc - n16)) g_sc[n16 + k] = s_sc[n16 + k];
 }
 
 // Row tiles: kTileRows rows of R bytes of one unit.  R <= 128: one TMA box {R, 256, 1},
@@ -411,9 +268,20 @@ __device__ __forceinline__ float2 f2rq(float2 a, float2 inv) {
       : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(inv.x), "f"(inv.y), "f"(kMagic));
   return r;
 }
-// NOTE: ptxas (12.9) contracts an f32x2 multiply feeding an f32x2 add into FFMA2 even with
-// .rn and --fmad=false.  Products that feed additions are therefore computed with scalar
-// __fmul_rn (scalar .rn is honoured); f2mul is used only where its result is not added.
+// NOTE: ptxas (12.9) contracts a multiply feeding an add into FFMA2 even with .rn and
+// --fmad=false (it also re-vectorizes scalar __fmul_rn/__fadd_rn pairs and then fuses them).
+// Every product that is later added is therefore computed as fma(a, b, z) with z = -0.0f
+// passed as a kernel argument: bit-identical to rn(a*b) (x + -0 == x, +0 + -0 == +0), and
+// ptxas can neither drop the unknown addend nor fuse an FMA into the following add.
+// tests/test_sass.py rejects any FFMA2 whose addend is a packed accumulator.
+__device__ __forceinline__ float2 f2mulz(float2 a, float2 b, float z) {
+  float2 r;
+  asm("{\n\t.reg .b64 pa, pb, pc, pd;\n\tmov.b64 pa, {%2, %3};\n\tmov.b64 pb, {%4, %5};\n\t"
+      "mov.b64 pc, {%6, %6};\n\tfma.rn.f32x2 pd, pa, pb, pc;\n\tmov.b64 {%0, %1}, pd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(z));
+  return r;
+}
+__device__ __forceinline__ float mulz(float a, float b, float z) { return __fmaf_rn(a, b, z); }
 
 // A 64-element row lives in 32 f32x2 registers p[i] = {v[i], v[i+32]}.
 //
@@ -478,7 +346,7 @@ __device__ __forceinline__ void dec4x8_2(uint32_t w, float* f) {
 // Decode the 64 codes of row t of a row tile (R = 64*BIN/8 bytes) and dequantize:
 // x[i] = {code_i * ds0, code_{i+32} * ds1} (ds0 for elements 0..31, ds1 for 32..63).
 template <int BIN, int R>
-__device__ __forceinline__ void dequant_row(const uint8_t* tile, int t, float ds0, float ds1, float2* x) {
+__device__ __forceinline__ void dequant_row(const uint8_t* tile, int t, float ds0, float ds1, float z, float2* x) {
   float f[64];
 #pragma unroll
   for (int c = 0; c < R / 16; ++c) {
@@ -499,14 +367,15 @@ __device__ __forceinline__ void dequant_row(const uint8_t* tile, int t, float ds
     for (int i = 0; i < 32; ++i) x[i] = make_float2(f[i], f[i + 32]);
   } else {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = make_float2(__fmul_rn(f[i], ds0), __fmul_rn(f[i + 32], ds1));
+    for (int i = 0; i < 32; ++i) x[i] = f2mulz(make_float2(f[i], f[i + 32]), make_float2(ds0, ds1), z);
   }
 }
 
-// Quantize a 64-element row held as pairs (R2, R3) into codes in an output row tile; the
-// group's first row writes the scale rn(s * c) (R6) straight to global.  lg = log2 G:
+// Quantize a 64-element row held as pairs (R2, R3) into codes in an output row tile (LINEAR:
+// row-major for a 1-D bulk store to a peer; else the TMA-swizzled layout for a tensor store);
+// the group's first row writes the scale rn(s * c) (R6) to scales_tile.  lg = log2 G:
 // G >= 64 -> a group spans G/64 rows (lanes); G == 32 -> two groups per row (one per half).
-template <int BITS, int R>
+template <int BITS, int R, bool LINEAR>
 __device__ __forceinline__ void quant_row(const float2* p, int t, int lg, float c, bool act, uint8_t* out_tile,
                                           float* scales_tile) {
   constexpr float q = float((1 << (BITS - 1)) - 1);
@@ -544,7 +413,7 @@ __device__ __forceinline__ void quant_row(const float2* p, int t, int lg, float 
       uint4 w = make_uint4(pack8x4(r[0], r[1], r[2], r[3]), pack8x4(r[4], r[5], r[6], r[7]),
                            pack8x4(r[8], r[9], r[10], r[11]), pack8x4(r[12], r[13], r[14], r[15]));
       if (!(k < 2 ? p0.ok : p1.ok)) w = make_uint4(0u, 0u, 0u, 0u);
-      *reinterpret_cast<uint4*>(out_tile + tile_off<R>(t, k)) = w;
+      *reinterpret_cast<uint4*>(out_tile + (LINEAR ? t * R + 16 * k : tile_off<R>(t, k))) = w;
     }
   } else {
 #pragma unroll
@@ -552,31 +421,215 @@ __device__ __forceinline__ void quant_row(const float2* p, int t, int lg, float 
       const uint32_t* r = k == 0 ? rx : ry;
       uint4 w = make_uint4(pack4x8(r), pack4x8(r + 8), pack4x8(r + 16), pack4x8(r + 24));
       if (!(k == 0 ? p0.ok : p1.ok)) w = make_uint4(0u, 0u, 0u, 0u);
-      *reinterpret_cast<uint4*>(out_tile + tile_off<R>(t, k)) = w;
+      *reinterpret_cast<uint4*>(out_tile + (LINEAR ? t * R + 16 * k : tile_off<R>(t, k))) = w;
     }
   }
 }
 
-// Incremental (unit, tile-in-unit) coordinates of tile = blockIdx.x + i * gridDim.x.
+// Incremental (unit, tile-in-unit) coordinates of tile = blockIdx.x + i * gridDim.x with the
+// unit index fastest (tile = ts * U + unit): consecutive tiles go to different destinations,
+// so local (HBM) and peer (NVLink) stores of a pushing kernel overlap instead of forming
+// phases.
 struct TileIter {
-  uint32_t unit, ts, per;
-  __device__ TileIter(uint32_t per_unit) : per(per_unit) {
-    unit = blockIdx.x / per;
-    ts = blockIdx.x - unit * per;
+  uint32_t unit, ts, U, gq, gr;
+  __device__ explicit TileIter(uint32_t units) : U(units) {
+    ts = blockIdx.x / U;
+    unit = blockIdx.x - ts * U;
+    gq = gridDim.x / U;
+    gr = gridDim.x - gq * U;
   }
   __device__ void next() {
-    ts += gridDim.x;
-    while (ts >= per) {
-      ts -= per;
-      ++unit;
+    unit += gr;
+    ts += gq;
+    if (unit >= U) {
+      unit -= U;
+      ++ts;
     }
   }
 };
 
+// =====================================================================================
+// K1  qWD quantize (Alg. 2 l.2-3, P:259-260): d = rn(w_main - widen(w_model)),
+// per G-group s = max|d|, codes = RNE(d * rn(q/s)) (R3: fused, exact product).  8 elements per
+// thread, a group is G/8 consecutive threads.  Output: one wire unit [codes][scales].
+// =====================================================================================
+constexpr int kVecThreads = 256;  // K1 / K2: 256-thread CTAs, kVecCtas per SM (persistent)
+constexpr int kVecCtas = 8;
+
+template <typename TM, int BITS>
+__global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __restrict__ w_main,
+                                                                   const TM* __restrict__ w_model, size_t S,
+                                                                   int lg, const Dests dst) {
+  constexpr int TILE = kVecThreads * 8;
+  __shared__ float red[kVecThreads / 32];
+  constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
+  const int tpg = (1 << lg) >> 3;
+  const size_t ntiles = (S + TILE - 1) / TILE;
+  const size_t sc_off = S * (BITS == 32 ? 4 : BITS) / 8;
+  const int t = threadIdx.x;
+  for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const size_t e0 = tile * TILE + t * 8;
+    const bool act = e0 < S;
+    float d[8];
+    if (act) {
+      const float4 a0 = *reinterpret_cast<const float4*>(w_main + e0);
+      const float4 a1 = *reinterpret_cast<const float4*>(w_main + e0 + 4);
+      float m[8];
+      if constexpr (sizeof(TM) == 2) {
+        const uint4 u = *reinterpret_cast<const uint4*>(w_model + e0);
+        m[0] = bf16_lo(u.x); m[1] = bf16_hi(u.x); m[2] = bf16_lo(u.y); m[3] = bf16_hi(u.y);
+        m[4] = bf16_lo(u.z); m[5] = bf16_hi(u.z); m[6] = bf16_lo(u.w); m[7] = bf16_hi(u.w);
+      } else {
+        const float4 b0 = *reinterpret_cast<const float4*>(w_model + e0);
+        const float4 b1 = *reinterpret_cast<const float4*>(w_model + e0 + 4);
+        m[0] = b0.x; m[1] = b0.y; m[2] = b0.z; m[3] = b0.w;
+        m[4] = b1.x; m[5] = b1.y; m[6] = b1.z; m[7] = b1.w;
+      }
+      d[0] = __fsub_rn(a0.x, m[0]); d[1] = __fsub_rn(a0.y, m[1]);
+      d[2] = __fsub_rn(a0.z, m[2]); d[3] = __fsub_rn(a0.w, m[3]);
+      d[4] = __fsub_rn(a1.x, m[4]); d[5] = __fsub_rn(a1.y, m[5]);
+      d[6] = __fsub_rn(a1.z, m[6]); d[7] = __fsub_rn(a1.w, m[7]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d[i] = 0.f;
+    }
+    if constexpr (BITS == 32) {  // identity codec (R12): the wire carries d itself
+      if (act)
+        for (int k = 0; k < dst.n; ++k) {
+          float4* o = reinterpret_cast<float4*>(dst.p[k] + e0 * 4);
+          o[0] = make_float4(d[0], d[1], d[2], d[3]);
+          o[1] = make_float4(d[4], d[5], d[6], d[7]);
+        }
+    } else {
+      float a = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a = max_nan(a, fabsf(d[i]));
+      a = group_max(a, tpg, red);
+      const QP p = qparam(a, q);
+      if (act) {
+        uint32_t r[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] = rq(d[i], p.inv);
+        // every destination unit (all-gather push, Alg. 2 l.4): warp-contiguous stores
+        if constexpr (BITS == 4) {
+          uint32_t w = pack4x8(r);
+          if (!p.ok) w = 0u;
+          for (int k = 0; k < dst.n; ++k) *reinterpret_cast<uint32_t*>(dst.p[k] + e0 / 2) = w;
+        } else {
+          uint2 w = make_uint2(pack8x4(r[0], r[1], r[2], r[3]), pack8x4(r[4], r[5], r[6], r[7]));
+          if (!p.ok) w = make_uint2(0u, 0u);
+          for (int k = 0; k < dst.n; ++k) *reinterpret_cast<uint2*>(dst.p[k] + e0) = w;
+        }
+        if ((t & (tpg - 1)) == 0) {
+          const float sv = stored_scale(a, 1.f);
+          for (int k = 0; k < dst.n; ++k) reinterpret_cast<float*>(dst.p[k] + sc_off)[e0 >> lg] = sv;
+        }
+      }
+    }
+  }
+}
+
+// =====================================================================================
+// K2  qWD apply (Alg. 2 l.5, P:262): w_model[jS + e] = bf16_rn(widen(w) + code*rn(s/q))
+// for every shard j of the gathered units (w_model shard j at w_model + j*stride).  Each
+// thread updates two 16-element vectors per tile, all loads issued up front.
+// =====================================================================================
+template <int BITS>
+struct K2Vec {
+  static constexpr int CB = BITS == 32 ? 64 : 16 * BITS / 8;  // code bytes per 16 elements
+};
+
+template <typename TM, int BITS>
+__device__ __forceinline__ void k2_load(const uint8_t* unit, const float* scales, const TM* wm, size_t e, int lg,
+                                        uint4* cw, float& sc, uint4* mw) {
+  if constexpr (BITS == 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cw[i] = *reinterpret_cast<const uint4*>(unit + e * 4 + 16 * i);
+  } else if constexpr (BITS == 8) {
+    cw[0] = *reinterpret_cast<const uint4*>(unit + e);
+    sc = scales[e >> lg];
+  } else {
+    const uint2 w = *reinterpret_cast<const uint2*>(unit + e / 2);
+    cw[0] = make_uint4(w.x, w.y, 0u, 0u);
+    sc = scales[e >> lg];
+  }
+  if constexpr (sizeof(TM) == 2) {
+    mw[0] = *reinterpret_cast<const uint4*>(wm + e);
+    mw[1] = *reinterpret_cast<const uint4*>(wm + e + 8);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mw[i] = *reinterpret_cast<const uint4*>(wm + e + 4 * i);
+  }
+}
+
+template <typename TM, int BITS>
+__device__ __forceinline__ void k2_apply(const uint4* cw, float sc, uint4* mw, TM* wm, size_t e, float z) {
+  constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
+  float x[16];
+  if constexpr (BITS == 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[4 * i] = __uint_as_float(cw[i].x); x[4 * i + 1] = __uint_as_float(cw[i].y);
+      x[4 * i + 2] = __uint_as_float(cw[i].z); x[4 * i + 3] = __uint_as_float(cw[i].w);
+    }
+  } else {
+    const float ds = __fdiv_rn(sc, q);
+    float f[16];
+    if constexpr (BITS == 4) {
+      dec4x8(cw[0].x, f);
+      dec4x8(cw[0].y, f + 8);
+    } else {
+      dec8x4(cw[0].x, f); dec8x4(cw[0].y, f + 4); dec8x4(cw[0].z, f + 8); dec8x4(cw[0].w, f + 12);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = mulz(f[i], ds, z);  // the product is added next: fusion barrier
+  }
+  if constexpr (sizeof(TM) == 2) {
+    uint32_t* w = &mw[0].x;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      w[i] = pack_bf16x2(__fadd_rn(bf16_lo(w[i]), x[2 * i]), __fadd_rn(bf16_hi(w[i]), x[2 * i + 1]));
+    reinterpret_cast<uint4*>(wm + e)[0] = mw[0];
+    reinterpret_cast<uint4*>(wm + e + 8)[0] = mw[1];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float4 t;
+      t.x = __fadd_rn(__uint_as_float(mw[i].x), x[4 * i]);
+      t.y = __fadd_rn(__uint_as_float(mw[i].y), x[4 * i + 1]);
+      t.z = __fadd_rn(__uint_as_float(mw[i].z), x[4 * i + 2]);
+      t.w = __fadd_rn(__uint_as_float(mw[i].w), x[4 * i + 3]);
+      reinterpret_cast<float4*>(wm + e + 4 * i)[0] = t;
+    }
+  }
+}
+
+template <typename TM, int BITS>
+__global__ void __launch_bounds__(kVecThreads) k2_qwd_apply(const uint8_t* __restrict__ units,
+                                                               size_t unit_bytes, size_t S, size_t stride, int P,
+                                                               int lg, TM* __restrict__ w_model, float z) {
+  constexpr int TILE = kVecThreads * 32;
+  const size_t tpu = (S + TILE - 1) / TILE;
+  for (size_t tile = blockIdx.x; tile < tpu * P; tile += gridDim.x) {
+    const size_t j = tile / tpu, ts = tile - j * tpu;
+    const uint8_t* unit = units + j * unit_bytes;
+    const float* scales = reinterpret_cast<const float*>(unit + S * (BITS == 32 ? 4 : BITS) / 8);
+    TM* wm = w_model + j * stride;
+    const size_t ea = ts * TILE + threadIdx.x * 16, eb = ea + TILE / 2;
+    uint4 ca[4], cb[4], ma[4], mb[4];
+    float sa = 0.f, sb = 0.f;
+    const bool aa = ea < S, ab = eb < S;
+    if (aa) k2_load<TM, BITS>(unit, scales, wm, ea, lg, ca, sa, ma);
+    if (ab) k2_load<TM, BITS>(unit, scales, wm, eb, lg, cb, sb, mb);
+    if (aa) k2_apply<TM, BITS>(ca, sa, ma, wm, ea, z);
+    if (ab) k2_apply<TM, BITS>(cb, sb, mb, wm, eb, z);
+  }
+}
+
 template <int IN_R, int OUT_R>
 struct K3Cfg {
   static constexpr int IN_TILE = kTileRows * IN_R;
-  static constexpr int OUT_TILE = kTileRows * OUT_R;
+  static constexpr int OUT_TILE = kTileRows * OUT_R + kTileElems / 32 * 4;  // codes + scales (G >= 32)
   static constexpr int BUDGET = 200 * 1024;
   static constexpr int S0 = (BUDGET - 2 * OUT_TILE) / IN_TILE;
   static constexpr int STAGES = S0 > 4 ? 4 : (S0 < 1 ? 1 : S0);
@@ -587,15 +640,23 @@ struct K3Cfg {
 // K3  TLq-HS Hadamard + quantize (Alg. 3 l.2-3; fused per P:394-395).
 // Persistent CTAs (one per SM); tile = 256 rows of 64 elements of one shard j.  Thread 0
 // keeps a STAGES-deep ring of TMA tensor loads in flight (mbarrier complete_tx); every
-// thread butterflies its own row in f32x2 registers, quantizes it and writes its codes
-// into a double-buffered swizzled smem tile that thread 0 TMA-stores to unit
-// (l' = j % N, m' = j / N) of the intra send buffer (R9).  Scales go straight to global.
+// thread butterflies its own row in f32x2 registers, quantizes it and writes its codes and
+// scales into a double-buffered linear smem tile that thread 0 bulk-stores to unit m' = j / N
+// of the block for local rank l' = j % N (R9) -- with the P2P transport that block is the
+// peer's receive buffer, so the store IS the intra all-to-all (Alg. 3 l.4) over NVLink.
 // =====================================================================================
+// Output of K3: per destination local rank l', the block this rank sends to l' (peer
+// receive buffer or local send buffer); unit m' at blk + m' * unit_bytes.
+struct K3Out {
+  CUtensorMap map[kMaxN];  // valid for local blocks: M units of that block
+  uint8_t* blk[kMaxN];
+  uint32_t remote;         // bit l': block l' lives in a peer's memory (P2P push)
+};
+
 template <int IN_R, int BITS, int B>
 __global__ void __launch_bounds__(kTileRows, 1)
-    k3_tlq_had_quant(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
-                     size_t S, int M, int N, int lg, float cb, uint8_t* __restrict__ intra_send, size_t unit_bytes,
-                     uint32_t tps, uint32_t ntiles) {
+    k3_tlq_had_quant(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ K3Out out, size_t S, int M,
+                     int N, int lg, float cb, size_t unit_bytes, uint32_t tps, uint32_t ntiles) {
   constexpr int OUT_R = kRowElems * BITS / 8;
   using C = K3Cfg<IN_R, OUT_R>;
   constexpr int STAGES = C::STAGES;
@@ -617,14 +678,14 @@ __global__ void __launch_bounds__(kTileRows, 1)
     if (tile < ntiles) {
       const int s = i % STAGES;
       mbar_arrive_tx(&bar[s], C::IN_TILE);
-      tma_load_tile<IN_R>(in_buf + s * C::IN_TILE, &in_map, &bar[s], (int)((tile % tps) * kTileRows),
-                          (int)(tile / tps));
+      tma_load_tile<IN_R>(in_buf + s * C::IN_TILE, &in_map, &bar[s], (int)((tile / (uint32_t)(M * N)) * kTileRows),
+                          (int)(tile % (uint32_t)(M * N)));
     }
   };
   if (t == 0)
     for (int i = 0; i < STAGES; ++i) issue(i);
 
-  TileIter it(tps);
+  TileIter it((uint32_t)(M * N));
   for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i, it.next()) {
     const int s = i % STAGES;
     const uint32_t j = it.unit, ts = it.ts;
@@ -662,8 +723,11 @@ __global__ void __launch_bounds__(kTileRows, 1)
 
     fwht_pairs<B>(p);
 
-    const uint32_t unit = (j % N) * M + j / N;
+    const uint32_t lp = j % N, mp = j / N;  // shard j = m'N + l' goes to local rank l', unit m' (R9)
     uint8_t* ot = out_buf + (i & 1) * C::OUT_TILE;
+    float* osc = reinterpret_cast<float*>(ot + kTileRows * OUT_R);
+    uint8_t* unit = out.blk[lp] + mp * unit_bytes;
+    const bool remote = (out.remote >> lp) & 1u;  // CTA-uniform
     if constexpr (BITS == 32) {  // identity codec (R12): rn(u * c_b)
       const float2 cc = make_float2(cb, cb);
 #pragma unroll
@@ -671,18 +735,25 @@ __global__ void __launch_bounds__(kTileRows, 1)
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         const float2* q = p + 4 * (c & 7);
-        *reinterpret_cast<float4*>(ot + tile_off<256>(t, c)) =
+        *reinterpret_cast<float4*>(ot + (remote ? t * 256 + 16 * c : tile_off<256>(t, c))) =
             c < 8 ? make_float4(q[0].x, q[1].x, q[2].x, q[3].x) : make_float4(q[0].y, q[1].y, q[2].y, q[3].y);
       }
-    } else {
-      float* scales = reinterpret_cast<float*>(intra_send + unit * unit_bytes + S * BITS / 8) +
-                      (((size_t)ts * kTileElems) >> lg);
-      quant_row<BITS, OUT_R>(p, t, lg, cb, act, ot, scales);
+    } else if (remote) {  // peer block: linear tile, codes + scales bulk-stored over NVLink
+      quant_row<BITS, OUT_R, true>(p, t, lg, cb, act, ot, osc);
+    } else {              // local block: swizzled tile for the TMA tensor store, scales direct
+      float* gsc = reinterpret_cast<float*>(unit + S * BITS / 8) + (((size_t)ts * kTileElems) >> lg);
+      quant_row<BITS, OUT_R, false>(p, t, lg, cb, act, ot, gsc);
     }
     fence_proxy_async();
     __syncthreads();
-    if (t == 0) {
-      tma_store_tile<OUT_R>(&out_map, ot, (int)(ts * kTileRows), (int)unit);
+    if (remote) {
+      const uint32_t rows = min((uint32_t)kTileRows, rows_per_shard - ts * kTileRows);
+      const uint32_t nsc = BITS == 32 ? 0u : ((rows * kRowElems) >> lg);
+      store_tile(ot, rows * OUT_R, osc, nsc, unit + (size_t)ts * kTileRows * OUT_R,
+                 reinterpret_cast<float*>(unit + S * BITS / 8) + (((size_t)ts * kTileElems) >> lg));
+      if (t == 0) bulk_commit();
+    } else if (t == 0) {
+      tma_store_tile<OUT_R>(&out.map[lp], ot, (int)(ts * kTileRows), (int)mp);
       bulk_commit();
     }
   }
@@ -696,69 +767,66 @@ __global__ void __launch_bounds__(kTileRows, 1)
 // (slot c <- chunk c ^ f(t): conflict-free; the permutation is undone by the store
 // addresses).  Thread 0 streams (tile, source l'') items through a STAGES-deep ring of 1-D
 // bulk copies (codes + scales); sources are summed in order l'' = 0..N-1 (R8); the sum is
-// requantized (one division per group) and stored to unit m' of the inter send buffer.
+// requantized (one division per group) into a staged smem tile that thread 0 bulk-stores to
+// unit m' (P2P transport: the receive slot of node m' itself -- the inter all-to-all).
 // =====================================================================================
 constexpr int kK4Threads = 128;
+constexpr int kK4Ctas = 3;
 constexpr int kK4Tile = kK4Threads * 64;
 
-template <int BIN>
+template <int BIN, int BOUT>
 struct K4Cfg {
   static constexpr int CODE_BYTES = kK4Tile * BIN / 8;
   static constexpr int SC_BYTES = BIN == 32 ? 0 : kK4Tile / 32 * 4;
   static constexpr int STAGE = CODE_BYTES + SC_BYTES;
-  static constexpr int STAGES = BIN == 32 ? 2 : (BIN == 8 ? 6 : 8);
-  static constexpr int SMEM = STAGES * STAGE + 64 + 128;
+  static constexpr int OUT_TILE = kK4Tile * BOUT / 8 + kK4Tile / 32 * 4;  // staged output: codes + scales
+  static constexpr int S0 = (72 * 1024 - 2 * OUT_TILE) / STAGE;  // ~72 KB per CTA: kK4Ctas per SM
+  static constexpr int STAGES = S0 > 8 ? 8 : (S0 < 1 ? 1 : S0);
+  static constexpr int SMEM = STAGES * STAGE + 2 * OUT_TILE + 64 + 128;
   static constexpr int CPT = 64 * BIN / 8 / 16;   // 16-byte chunks per thread
   static constexpr int EPC = 64 / CPT;            // elements per chunk
 };
 
 // Producer cursor over (tile, source) items of this CTA, advanced without divisions.
 struct ItemCursor {
-  uint32_t l, unit, ts;
-  __device__ void init(uint32_t tpu) {
-    l = 0;
-    unit = blockIdx.x / tpu;
-    ts = blockIdx.x - unit * tpu;
-  }
-  __device__ void next(uint32_t n_src, uint32_t tpu) {
+  uint32_t l;
+  TileIter it;
+  __device__ explicit ItemCursor(uint32_t units) : l(0), it(units) {}
+  __device__ void next(uint32_t n_src) {
     if (++l == n_src) {
       l = 0;
-      ts += gridDim.x;
-      while (ts >= tpu) {
-        ts -= tpu;
-        ++unit;
-      }
+      it.next();
     }
   }
 };
 
 template <int BIN, int BOUT>
-__global__ void __launch_bounds__(kK4Threads) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
-                                                          int N, int M, size_t S, int lg,
-                                                          uint8_t* __restrict__ send, size_t out_unit_bytes,
-                                                          uint32_t tpu, uint32_t ntiles) {
-  using C = K4Cfg<BIN>;
+__global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
+                                                          int N, int M, size_t S, int lg, const Dests dst,
+                                                          uint32_t tpu, uint32_t ntiles, float z) {
+  using C = K4Cfg<BIN, BOUT>;
   constexpr int STAGES = C::STAGES, CPT = C::CPT, EPC = C::EPC;
   constexpr float qin = float((1 << (BIN == 32 ? 1 : BIN - 1)) - 1);
   constexpr float qout = float((1 << (BOUT == 32 ? 1 : BOUT - 1)) - 1);
   constexpr float kDec = BIN == 8 ? kDec8 : kDec4;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
+  uint8_t* out_buf = smem + STAGES * C::STAGE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(out_buf + 2 * C::OUT_TILE);
   const int t = threadIdx.x;
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  ItemCursor pc;
+  ItemCursor pc((uint32_t)M);
   uint32_t pk = 0;
   auto issue = [&]() {  // thread 0: next item of the producer cursor into its ring slot
-    if (pc.unit < (uint32_t)M) {
+    if (pc.it.ts < tpu) {
       const int s = pk % STAGES;
-      const size_t e0 = (size_t)pc.ts * kK4Tile;
+      const size_t e0 = (size_t)pc.it.ts * kK4Tile;
       const uint32_t n = (uint32_t)min((size_t)kK4Tile, S - e0);
-      const uint8_t* unit = recv + ((size_t)pc.l * M + pc.unit) * in_unit_bytes;
+      const uint8_t* unit = recv + ((size_t)pc.l * M + pc.it.unit) * in_unit_bytes;
       const uint32_t cb = n * BIN / 8;
       uint32_t sb = 0;
       if constexpr (BIN != 32) sb = (((n >> lg) * 4) + 15) & ~15u;
@@ -768,17 +836,15 @@ __global__ void __launch_bounds__(kK4Threads) k4_tlq_dq_reduce_q(const uint8_t* 
         bulk_load(smem + s * C::STAGE + C::CODE_BYTES, unit + S * BIN / 8 + (e0 >> lg) * 4, sb, &bar[s]);
     }
     ++pk;
-    pc.next(N, tpu);
+    pc.next(N);
   };
-  if (t == 0) {
-    pc.init(tpu);
+  if (t == 0)
     for (int k = 0; k < STAGES; ++k) issue();
-  }
 
   // slot c of this thread holds chunk c ^ f (f = 0 for the fp32 identity path)
   const int f = BIN == 32 ? 0 : (CPT >= 8 ? (t & 7) : ((t / (8 / CPT)) & (CPT - 1)));
   const int tpg = lg >= 6 ? (1 << (lg - 6)) : 1;  // threads per group
-  TileIter it(tpu);
+  TileIter it((uint32_t)M);
   uint32_t k = 0;
   for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i, it.next()) {
     const uint32_t mp = it.unit;
@@ -828,13 +894,8 @@ __global__ void __launch_bounds__(kK4Threads) k4_tlq_dq_reduce_q(const uint8_t* 
           }
           // dequantize: rn(code * ds).  Chunk c holds elements of half ((c ^ f) * EPC) >> 5.
           const float d = (((c ^ f) * EPC) >> 5) ? ds1 : ds0;
-          if (N == 1) {  // single source: the products are never added -> packed multiply is safe
 #pragma unroll
-            for (int q = 0; q < EPC / 2; ++q) xs[q] = f2mul(xs[q], make_float2(d, d));
-          } else {
-#pragma unroll
-            for (int q = 0; q < EPC / 2; ++q) xs[q] = make_float2(__fmul_rn(xs[q].x, d), __fmul_rn(xs[q].y, d));
-          }
+          for (int q = 0; q < EPC / 2; ++q) xs[q] = f2mulz(xs[q], make_float2(d, d), z);
         }
         // R8: acc = 0; acc += x_l'' in order.  A dequantized code*ds is never -0 (a zero code
         // gives +0), so for quantized inputs 0 + x_0 == x_0 and the first add is elided.
@@ -855,8 +916,19 @@ __global__ void __launch_bounds__(kK4Threads) k4_tlq_dq_reduce_q(const uint8_t* 
       if (t == 0) issue();
     }
 
-    // ---- requantize at BOUT bits; 16-element vectors v = 0..3 in slot order
-    uint8_t* out = send + (size_t)mp * out_unit_bytes;
+    // ---- requantize at BOUT bits into the staged output tile; 16-element vectors v = 0..3
+    // in slot order, written at their element positions (undoing the slot permutation)
+    // local destination: write global memory directly (L2 merges the partial sectors);
+    // peer destination: stage the tile in smem and bulk-store it (contiguous NVLink writes)
+    const bool remote = (dst.remote >> mp) & 1u;  // CTA-uniform
+    uint8_t* gout = dst.p[mp];
+    uint8_t* ot = remote ? out_buf + (i & 1) * C::OUT_TILE : gout + e0 * BOUT / 8;
+    float* osc = remote ? reinterpret_cast<float*>(ot + kK4Tile * BOUT / 8)
+                        : reinterpret_cast<float*>(gout + S * BOUT / 8) + (e0 >> lg);
+    if (remote) {
+      if (t == 0) bulk_wait_read<1>();  // the stores issued two tiles ago have left out_buf[i & 1]
+      __syncthreads();
+    }
     auto vbase = [&](int v) {  // element offset (within the thread's 64) of slot-order vector v
       if constexpr (EPC >= 16) return (((16 * v) / EPC) ^ f) * EPC + (16 * v) % EPC;
       else return 16 * v;
@@ -865,7 +937,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_tlq_dq_reduce_q(const uint8_t* 
       if (act) {
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-          float4* o = reinterpret_cast<float4*>(out + (e0 + 64 * t + vbase(v)) * 4);
+          float4* o = reinterpret_cast<float4*>(ot + (64 * t + vbase(v)) * 4);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             o[q] = make_float4(acc[8 * v + 2 * q].x, acc[8 * v + 2 * q].y, acc[8 * v + 2 * q + 1].x,
@@ -915,28 +987,35 @@ __global__ void __launch_bounds__(kK4Threads) k4_tlq_dq_reduce_q(const uint8_t* 
             r[2 * q + 1] = __float_as_uint(y.y);
           }
           const bool okv = h ? p1.ok : p0.ok;
-          const size_t e = e0 + 64 * t + vbase(v);
+          const int e = 64 * t + vbase(v);
           if constexpr (BOUT == 4) {
             uint2 w = make_uint2(pack4x8(r), pack4x8(r + 8));
             if (!okv) w = make_uint2(0u, 0u);
-            *reinterpret_cast<uint2*>(out + e / 2) = w;
+            *reinterpret_cast<uint2*>(ot + e / 2) = w;
           } else {
             uint4 w = make_uint4(pack8x4(r[0], r[1], r[2], r[3]), pack8x4(r[4], r[5], r[6], r[7]),
                                  pack8x4(r[8], r[9], r[10], r[11]), pack8x4(r[12], r[13], r[14], r[15]));
             if (!okv) w = make_uint4(0u, 0u, 0u, 0u);
-            *reinterpret_cast<uint4*>(out + e) = w;
+            *reinterpret_cast<uint4*>(ot + e) = w;
           }
         }
-        float* oscales = reinterpret_cast<float*>(out + S * BOUT / 8);
-        const size_t eg = e0 + 64 * t;
         if (lg >= 6) {
-          if ((t & (tpg - 1)) == 0) oscales[eg >> lg] = stored_scale(a0, 1.f);
+          if ((t & (tpg - 1)) == 0) osc[(64 * t) >> lg] = stored_scale(a0, 1.f);
         } else {
-          *reinterpret_cast<float2*>(oscales + (eg >> 5)) = make_float2(stored_scale(a0, 1.f), stored_scale(a1, 1.f));
+          *reinterpret_cast<float2*>(osc + 2 * t) = make_float2(stored_scale(a0, 1.f), stored_scale(a1, 1.f));
         }
       }
     }
+    if (remote) {  // unit m' -> node m' (P2P: the peer's receive slot -- Alg. 3 l.10)
+      fence_proxy_async();
+      __syncthreads();
+      const uint32_t n = (uint32_t)min((size_t)kK4Tile, S - e0);
+      store_tile(ot, n * BOUT / 8, osc, BOUT == 32 ? 0u : (n >> lg), gout + e0 * BOUT / 8,
+                 reinterpret_cast<float*>(gout + S * BOUT / 8) + (e0 >> lg));
+      if (t == 0) bulk_commit();
+    }
   }
+  if (t == 0) bulk_wait<0>();
 }
 
 // =====================================================================================
@@ -961,7 +1040,7 @@ template <int IN_R, int B>
 __global__ void __launch_bounds__(kTileRows, 1)
     k5_tlq_dq_reduce_had(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
                          const uint8_t* __restrict__ recv, size_t in_unit_bytes, int M, size_t S, int lg, float kappa,
-                         uint32_t ntiles) {
+                         uint32_t ntiles, float z) {
   constexpr int BIN = IN_R * 8 / kRowElems;
   using C = K5Cfg<IN_R>;
   constexpr int STAGES = C::STAGES;
@@ -1019,7 +1098,7 @@ __global__ void __launch_bounds__(kTileRows, 1)
         }
       }
       float2 x[32];
-      dequant_row<BIN, IN_R>(st, t, ds0, ds1, x);
+      dequant_row<BIN, IN_R>(st, t, ds0, ds1, z, x);
       // R8 order; the first add 0 + x_0 is exact for quantized inputs (x_0 != -0).
       if (m == 0 && BIN != 32) {
 #pragma unroll
@@ -1119,13 +1198,12 @@ cudaError_t make_row_map(CUtensorMap* map, const void* base, int R, uint64_t row
   }
 
 template <int IN_R, int BITS, int B>
-cudaError_t k3_launch(const CUtensorMap& in_map, const CUtensorMap& out_map, size_t S, int M, int N, int G, float cb,
-                      uint8_t* intra_send, size_t unit_bytes, uint32_t tps, uint32_t ntiles, int grid,
-                      cudaStream_t st) {
+cudaError_t k3_launch(const CUtensorMap& in_map, const K3Out& out, size_t S, int M, int N, int G, float cb,
+                      size_t unit_bytes, uint32_t tps, uint32_t ntiles, int grid, cudaStream_t st) {
   constexpr int SMEM = K3Cfg<IN_R, kRowElems * BITS / 8>::SMEM;
   cudaError_t e = set_smem(k3_tlq_had_quant<IN_R, BITS, B>, SMEM);
   if (e != cudaSuccess) return e;
-  k3_tlq_had_quant<IN_R, BITS, B><<<grid, kTileRows, SMEM, st>>>(in_map, out_map, S, M, N, __builtin_ctz(G), cb, intra_send,
+  k3_tlq_had_quant<IN_R, BITS, B><<<grid, kTileRows, SMEM, st>>>(in_map, out, S, M, N, __builtin_ctz(G), cb,
                                                                   unit_bytes, tps, ntiles);
   return cudaGetLastError();
 }
@@ -1137,21 +1215,21 @@ cudaError_t k5_launch(const CUtensorMap& in_map, const CUtensorMap& out_map, con
   cudaError_t e = set_smem(k5_tlq_dq_reduce_had<IN_R, B>, SMEM);
   if (e != cudaSuccess) return e;
   k5_tlq_dq_reduce_had<IN_R, B><<<grid, kTileRows, SMEM, st>>>(in_map, out_map, recv, unit_bytes, M, S, __builtin_ctz(G), kappa,
-                                                                ntiles);
+                                                                ntiles, -0.0f);
   return cudaGetLastError();
 }
 
 template <int BIN, int BOUT>
-cudaError_t k4_launch(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, uint8_t* send,
-                      size_t out_unit_bytes, int grid_cap, cudaStream_t st) {
-  constexpr int SMEM = K4Cfg<BIN>::SMEM;
+cudaError_t k4_launch(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
+                      int sms, cudaStream_t st) {
+  constexpr int SMEM = K4Cfg<BIN, BOUT>::SMEM;
   cudaError_t e = set_smem(k4_tlq_dq_reduce_q<BIN, BOUT>, SMEM);
   if (e != cudaSuccess) return e;
   const uint32_t tpu = (uint32_t)((S + kK4Tile - 1) / kK4Tile);
   const uint32_t ntiles = tpu * (uint32_t)M;
-  const int grid = grid_for(ntiles, grid_cap / 8 * 3);
-  k4_tlq_dq_reduce_q<BIN, BOUT><<<grid, kK4Threads, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G), send, out_unit_bytes, tpu,
-                                                         ntiles);
+  const int grid = grid_for(ntiles, sms * kK4Ctas);
+  k4_tlq_dq_reduce_q<BIN, BOUT><<<grid, kK4Threads, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G), dst, tpu,
+                                                         ntiles, -0.0f);
   return cudaGetLastError();
 }
 
@@ -1159,11 +1237,11 @@ cudaError_t k4_launch(const uint8_t* recv, size_t in_unit_bytes, int N, int M, s
 
 // ------------------------------- launchers -------------------------------------------
 cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, int model_dtype,
-                                size_t S, int bits, int G, uint8_t* unit, int grid_cap,
+                                size_t S, int bits, int G, const Dests& dst, int sms,
                                 cudaStream_t st) {
-  const int grid = grid_for((S + 2047) / 2048, grid_cap);
+  const int grid = grid_for((S + kVecThreads * 8 - 1) / (kVecThreads * 8), sms * kVecCtas);
 #define K1(TM, B) \
-  k1_qwd_quantize<TM, B><<<grid, 256, 0, st>>>(w_main, static_cast<const TM*>(w_model_shard), S, __builtin_ctz(G), unit)
+  k1_qwd_quantize<TM, B><<<grid, kVecThreads, 0, st>>>(w_main, static_cast<const TM*>(w_model_shard), S, __builtin_ctz(G), dst)
   if (model_dtype == kBF16) {
     if (bits == 4) K1(uint16_t, 4); else if (bits == 8) K1(uint16_t, 8); else K1(uint16_t, 32);
   } else {
@@ -1173,12 +1251,12 @@ cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_qwd_apply(const uint8_t* units, size_t unit_bytes, int P, size_t S, int bits,
-                             int G, void* w_model, int model_dtype, int grid_cap, cudaStream_t st) {
-  const int gx = grid_for((S + 8191) / 8192, (grid_cap + P - 1) / P);
-  const dim3 grid(gx, P);
-#define K2(TM, B) \
-  k2_qwd_apply<TM, B><<<grid, 256, 0, st>>>(units, unit_bytes, S, __builtin_ctz(G), static_cast<TM*>(w_model))
+cudaError_t launch_qwd_apply(const uint8_t* units, size_t unit_bytes, int P, size_t S, size_t stride, int bits,
+                             int G, void* w_model, int model_dtype, int sms, cudaStream_t st) {
+  const int grid = grid_for((S + kVecThreads * 32 - 1) / (kVecThreads * 32) * P, sms * kVecCtas);
+#define K2(TM, B)                                                                                  \
+  k2_qwd_apply<TM, B><<<grid, kVecThreads, 0, st>>>(units, unit_bytes, S, stride, P, __builtin_ctz(G), \
+                                                    static_cast<TM*>(w_model), -0.0f)
   if (model_dtype == kBF16) {
     if (bits == 4) K2(uint16_t, 4); else if (bits == 8) K2(uint16_t, 8); else K2(uint16_t, 32);
   } else {
@@ -1188,22 +1266,31 @@ cudaError_t launch_qwd_apply(const uint8_t* units, size_t unit_bytes, int P, siz
   return cudaGetLastError();
 }
 
-cudaError_t launch_tlq_had_quant(const void* grad, int grad_dtype, size_t S, int M, int N, int G,
-                                 int b, float cb, int bits, uint8_t* intra_send, size_t unit_bytes,
-                                 int grid_cap, cudaStream_t st) {
+cudaError_t launch_tlq_had_quant(const void* grad, size_t grad_stride, int grad_dtype, size_t S, int M, int N,
+                                 int G, int b, float cb, int bits, uint8_t* const* blocks, uint32_t remote_mask,
+                                 size_t unit_bytes, int sms, cudaStream_t st) {
+  if (N > kMaxN) return cudaErrorInvalidValue;
   const uint64_t rows = S / kRowElems;
   const uint32_t tps = (uint32_t)((rows + kTileRows - 1) / kTileRows);
   const uint32_t ntiles = tps * (uint32_t)(M * N);
-  const int grid = grid_for(ntiles, grid_cap / 8);
+  const int grid = grid_for(ntiles, sms);
   const int in_r = grad_dtype == kBF16 ? 128 : 256;
   const int out_r = kRowElems * bits / 8;
-  CUtensorMap in_map, out_map;
-  cudaError_t e = make_row_map(&in_map, grad, in_r, rows, (uint64_t)M * N, (uint64_t)S * (in_r / kRowElems));
+  CUtensorMap in_map;
+  K3Out out;
+  memset(&out, 0, sizeof(out));
+  cudaError_t e = make_row_map(&in_map, grad, in_r, rows, (uint64_t)M * N, (uint64_t)grad_stride * (in_r / kRowElems));
   if (e != cudaSuccess) return e;
-  e = make_row_map(&out_map, intra_send, out_r, rows, (uint64_t)M * N, unit_bytes);
-  if (e != cudaSuccess) return e;
-#define K3(IR, BT) SDP4_B_SWITCH(b, return (k3_launch<IR, BT, BB>(in_map, out_map, S, M, N, G, cb, intra_send, \
-                                                                  unit_bytes, tps, ntiles, grid, st)))
+  out.remote = remote_mask;
+  for (int lp = 0; lp < N; ++lp) {
+    out.blk[lp] = blocks[lp];
+    if (!((remote_mask >> lp) & 1u)) {
+      e = make_row_map(&out.map[lp], blocks[lp], out_r, rows, (uint64_t)M, unit_bytes);
+      if (e != cudaSuccess) return e;
+    }
+  }
+#define K3(IR, BT) SDP4_B_SWITCH(b, return (k3_launch<IR, BT, BB>(in_map, out, S, M, N, G, cb, unit_bytes, tps, ntiles, \
+                                                                  grid, st)))
   if (in_r == 128) {
     if (bits == 4) { K3(128, 4); } else if (bits == 8) { K3(128, 8); } else { K3(128, 32); }
   } else {
@@ -1214,11 +1301,10 @@ cudaError_t launch_tlq_had_quant(const void* grad, int grad_dtype, size_t S, int
 }
 
 cudaError_t launch_tlq_dq_reduce_q(const uint8_t* intra_recv, size_t in_unit_bytes, int bits_in,
-                                   int N, int M, size_t S, int G, uint8_t* inter_send,
-                                   size_t out_unit_bytes, int bits_out, int grid_cap,
+                                   int N, int M, size_t S, int G, const Dests& dst, int bits_out, int sms,
                                    cudaStream_t st) {
-#define K4(BI, BO) return k4_launch<BI, BO>(intra_recv, in_unit_bytes, N, M, S, G, inter_send, out_unit_bytes, \
-                                            grid_cap, st)
+  if (M > kMaxDests) return cudaErrorInvalidValue;
+#define K4(BI, BO) return k4_launch<BI, BO>(intra_recv, in_unit_bytes, N, M, S, G, dst, sms, st)
 #define K4O(BI) \
   if (bits_out == 4) { K4(BI, 4); } else if (bits_out == 8) { K4(BI, 8); } else { K4(BI, 32); }
   if (bits_in == 4) { K4O(4); } else if (bits_in == 8) { K4O(8); } else { K4O(32); }
@@ -1228,10 +1314,10 @@ cudaError_t launch_tlq_dq_reduce_q(const uint8_t* intra_recv, size_t in_unit_byt
 
 cudaError_t launch_tlq_dq_reduce_had(const uint8_t* inter_recv, size_t in_unit_bytes, int bits_in,
                                      int M, size_t S, int G, int b, float kappa, float* out,
-                                     int grid_cap, cudaStream_t st) {
+                                     int sms, cudaStream_t st) {
   const uint64_t rows = S / kRowElems;
   const uint32_t ntiles = (uint32_t)((rows + kTileRows - 1) / kTileRows);
-  const int grid = grid_for(ntiles, grid_cap / 8);
+  const int grid = grid_for(ntiles, sms);
   const int in_r = kRowElems * bits_in / 8;
   CUtensorMap in_map, out_map;
   cudaError_t e = make_row_map(&in_map, inter_recv, in_r, rows, (uint64_t)M, in_unit_bytes);

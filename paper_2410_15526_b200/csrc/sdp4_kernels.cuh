@@ -7,6 +7,8 @@
 
 namespace sdp4 {
 
+// Every kernel is a persistent grid of at most `sms` CTAs, one CTA per SM (the rest of the
+// SMs stay free for concurrent NCCL kernels).
 // Rows of 64 elements are the unit of the Hadamard kernels (one row per thread).
 constexpr int kRowElems = 64;
 constexpr int kTileRows = 256;                       // rows per CTA tile = threads per CTA
@@ -14,33 +16,45 @@ constexpr int kTileElems = kTileRows * kRowElems;    // 16384 elements
 
 enum Dtype { kF32 = 0, kBF16 = 1 };
 
-// K1: Alg. 2 l.2-3 -- d = w_main - w_model (this shard), k-bit group quantization
-// into one wire unit.  Returns cudaGetLastError() of the launch.
-cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, int model_dtype,
-                                size_t S, int bits, int G, uint8_t* unit, int grid_cap,
-                                cudaStream_t st);
+// Destination wire units (or blocks) of a producing kernel: local send buffers for the
+// NCCL transport, or peers' receive buffers (CUDA IPC over NVLink) for the fused P2P
+// transport, where the producing kernel is the exchange (all-gather / all-to-all push).
+constexpr int kMaxDests = 16;
+constexpr int kMaxN = 8;  // max local ranks per group (K3 keeps one tensor map per destination)
+struct Dests {
+  uint8_t* p[kMaxDests];
+  int n;
+  uint32_t remote;  // bit k: p[k] is peer memory (store via staged 1-D bulk copies)
+};
 
-// K2: Alg. 2 l.5 -- for every shard j < P: w_model[jS..] += dequant(unit j), in place.
-cudaError_t launch_qwd_apply(const uint8_t* units, size_t unit_bytes, int P, size_t S, int bits,
-                             int G, void* w_model, int model_dtype, int grid_cap, cudaStream_t st);
+// K1: Alg. 2 l.2-3 -- d = w_main - w_model (this shard), k-bit group quantization
+// into the wire unit at every destination dst.p[0..n) (n = 1: local; n = P: all-gather push).
+cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, int model_dtype,
+                                size_t S, int bits, int G, const Dests& dst, int sms, cudaStream_t st);
+
+// K2: Alg. 2 l.5 -- for every shard j < P: w_model[j*stride ..+S] += dequant(unit j), in place.
+cudaError_t launch_qwd_apply(const uint8_t* units, size_t unit_bytes, int P, size_t S, size_t stride, int bits,
+                             int G, void* w_model, int model_dtype, int sms, cudaStream_t st);
 
 // K3: Alg. 3 l.2-3 -- blockwise Hadamard (b, in {0,2,..,256}) + bits_intra quantization
-// of the full gradient into the intra send layout (N blocks x M units).
-cudaError_t launch_tlq_had_quant(const void* grad, int grad_dtype, size_t S, int M, int N, int G,
-                                 int b, float cb, int bits, uint8_t* intra_send, size_t unit_bytes,
-                                 int grid_cap, cudaStream_t st);
+// of S elements of each of the P shards (shard j at grad + j*grad_stride elements); shard
+// m'N + l' goes to unit m' of blocks[l'] (M units of unit_bytes; blocks[l'] is the local send
+// block or the receive block of local rank l' itself; remote_mask bit l' = peer memory).
+cudaError_t launch_tlq_had_quant(const void* grad, size_t grad_stride, int grad_dtype, size_t S, int M, int N,
+                                 int G, int b, float cb, int bits, uint8_t* const* blocks, uint32_t remote_mask,
+                                 size_t unit_bytes, int sms, cudaStream_t st);
 
 // K4: Alg. 3 l.5,7,9 -- dequantize N received units per sub-block m', fp32 reduce in
-// source order, requantize at bits_out into the inter send layout (M units).
+// source order, requantize at bits_out into unit dst.p[m'] (local send unit or the
+// receive slot of node m' itself).
 cudaError_t launch_tlq_dq_reduce_q(const uint8_t* intra_recv, size_t in_unit_bytes, int bits_in,
-                                   int N, int M, size_t S, int G, uint8_t* inter_send,
-                                   size_t out_unit_bytes, int bits_out, int grid_cap,
+                                   int N, int M, size_t S, int G, const Dests& dst, int bits_out, int sms,
                                    cudaStream_t st);
 
 // K5: Alg. 3 l.11-13 -- dequantize M received units, fp32 reduce in source order,
 // inverse blockwise Hadamard, scale by kappa, write the fp32 shard.
 cudaError_t launch_tlq_dq_reduce_had(const uint8_t* inter_recv, size_t in_unit_bytes, int bits_in,
                                      int M, size_t S, int G, int b, float kappa, float* out,
-                                     int grid_cap, cudaStream_t st);
+                                     int sms, cudaStream_t st);
 
 }  // namespace sdp4

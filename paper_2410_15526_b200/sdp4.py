@@ -34,8 +34,12 @@ SIGNATURES = {
     "sdp4_version": (_ci, []),
     "sdp4_last_error": (ctypes.c_char_p, []),
     "sdp4_get_unique_id": (_ci, [ctypes.c_char_p]),
-    "sdp4_comm_init": (_ci, [ctypes.POINTER(_vp), ctypes.c_char_p, _ci, _ci, _ci, _ci]),
+    "sdp4_comm_init": (_ci, [ctypes.POINTER(_vp), ctypes.c_char_p, _ci, _ci, _ci, _ci, _ci]),
     "sdp4_comm_destroy": (_ci, [_vp]),
+    "sdp4_comm_set_chunks": (_ci, [_vp, _ci]),
+    "sdp4_comm_chunks": (_ci, [_vp, _c_size, _ci]),
+    "sdp4_comm_set_transport": (_ci, [_vp, _ci]),
+    "sdp4_comm_transport": (_ci, [_vp]),
     "sdp4_wire_unit_bytes": (_c_size, [_c_size, _ci, _ci]),
     "sdp4_qwd_workspace_bytes": (_c_size, [_ci, _c_size, _ci, _ci]),
     "sdp4_tlq_workspace_bytes": (_c_size, [_ci, _ci, _c_size, _ci, _ci, _ci]),
@@ -146,14 +150,34 @@ class Comm:
     """sdp4_comm_t: world + intra (N) + inter (M) NCCL communicators."""
 
     def __init__(self, rank: int = 0, world: int = 1, groups: int = 1, group_size: int = 1,
-                 unique_id: Optional[bytes] = None):
+                 unique_id: Optional[bytes] = None, nccl_ctas: int = 0, chunks: int = 0):
         self.rank, self.world, self.M, self.N = rank, world, groups, group_size
         self._h = ctypes.c_void_p()
         uid = None if unique_id is None else ctypes.create_string_buffer(unique_id, UNIQUE_ID_BYTES)
-        _check(lib().sdp4_comm_init(ctypes.byref(self._h), uid, rank, world, groups, group_size))
+        _check(lib().sdp4_comm_init(ctypes.byref(self._h), uid, rank, world, groups, group_size, nccl_ctas))
+        if chunks:
+            self.set_chunks(chunks)
+
+    def set_chunks(self, chunks: int):
+        """Pipeline chunk count (0 = automatic, 1 = off); see sdp4_comm_set_chunks."""
+        _check(lib().sdp4_comm_set_chunks(self._h, chunks))
+
+    TRANSPORTS = {"nccl": 0, "p2p": 1}
+
+    def set_transport(self, transport):
+        """'nccl' or 'p2p' (fused NVLink push); see sdp4_comm_set_transport."""
+        _check(lib().sdp4_comm_set_transport(self._h, self.TRANSPORTS.get(transport, transport)))
+
+    @property
+    def transport(self) -> str:
+        return {0: "nccl", 1: "p2p"}.get(lib().sdp4_comm_transport(self._h), "?")
+
+    def chunks(self, numel: int, group: int = 128) -> int:
+        return int(lib().sdp4_comm_chunks(self._h, numel, group))
 
     @classmethod
-    def from_process_group(cls, groups: Optional[int] = None, device=None) -> "Comm":
+    def from_process_group(cls, groups: Optional[int] = None, device=None, nccl_ctas: int = 0,
+                           chunks: int = 0) -> "Comm":
         """Bootstrap from torch.distributed: rank 0 draws an NCCL unique id and broadcasts
         it; groups defaults to the topology of topology.default_split."""
         import torch.distributed as dist
@@ -169,7 +193,7 @@ class Comm:
                 t = t.to(device or torch.device("cuda", torch.cuda.current_device()))
             dist.broadcast(t, 0)
             uid = bytes(t.cpu().tolist())
-        return cls(rank, world, M, N, uid)
+        return cls(rank, world, M, N, uid, nccl_ctas, chunks)
 
     def close(self):
         if self._h:

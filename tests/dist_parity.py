@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--groups", type=int, default=None)
     ap.add_argument("--G", type=int, default=128)
     ap.add_argument("--b", type=int, default=64)
+    ap.add_argument("--chunks", type=str, default="1,3,0", help="NCCL pipeline chunk counts to check (0 = auto)")
+    ap.add_argument("--transports", type=str, default="p2p,nccl")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -37,8 +39,27 @@ def main():
     M, N = default_split(world, a.groups)
     comm = Comm.from_process_group(a.groups)
     P, G, b = world, a.G, a.b
-    S = 16384 * 2 + 64 * 5 * max(1, G // 64)
-    S -= S % max(G, 64)
+    ok = True
+    msgs = []
+    runs = []
+    for tr in a.transports.split(","):
+        runs += [(tr, ch) for ch in ([int(x) for x in a.chunks.split(",")] if tr == "nccl" else [0])]
+    for tr, chunks in runs:
+        comm.set_transport(tr)
+        comm.set_chunks(chunks)
+        for S in (16384 * 2 + 64 * 5 * max(1, G // 64), 16384 * 12 + 640):
+            S -= S % max(G, 64)
+            ok_c, m_c = run_checks(comm, rank, P, M, N, G, b, S)
+            ok &= ok_c
+            msgs += [f"{tr} chunks={chunks} S={S} ({comm.chunks(P * S, G)} used): {m}" for m in m_c]
+    comm.close()
+    print(f"rank {rank}/{world} ({M}x{N}) {'PASS' if ok else 'FAIL'} runs={runs} {'; '.join(msgs)}", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+def run_checks(comm, rank, P, M, N, G, b, S):
     D = P * S
     ok = True
     msgs = []
@@ -78,11 +99,7 @@ def main():
         if not same.all():
             ok = False
             msgs.append(f"TLq-HS {dtype} out shard: {int((~same).sum())} of {S} elements differ")
-    comm.close()
-    print(f"rank {rank}/{world} ({M}x{N}) {'PASS' if ok else 'FAIL'} {'; '.join(msgs)}", flush=True)
-    dist.barrier()
-    dist.destroy_process_group()
-    sys.exit(0 if ok else 1)
+    return ok, msgs
 
 
 if __name__ == "__main__":

@@ -43,9 +43,12 @@ def test_workspace_layout(M, N):
     off = [sdp4.tlq_workspace_offset(M, N, D, 8, 4, 128, r) for r in range(4)]
     assert off[0] == 0
     assert off[1] == (0 if N == 1 else N * M * w8)
+    one_chunk = (2 if N > 1 else 1) * N * M * w8 + (2 if M > 1 else 1) * M * w4
     total = sdp4.tlq_workspace_bytes(M, N, D, 8, 4, 128)
-    assert total == (2 if N > 1 else 1) * N * M * w8 + (2 if M > 1 else 1) * M * w4
-    assert sdp4.qwd_workspace_bytes(P, D, 4, 128) == P * w4
+    # the size covers any pipeline chunk count (<= 16 chunks, each unit padded to 256 B)
+    assert one_chunk <= total <= one_chunk + 16 * (2 * N * M + 2 * M) * 256
+    q1 = P * w4
+    assert q1 <= sdp4.qwd_workspace_bytes(P, D, 4, 128) <= q1 + 16 * P * 256
 
 
 def test_validation_errors_before_any_launch():
@@ -65,7 +68,9 @@ def test_validation_errors_before_any_launch():
     st = L.sdp4_qwd_quantize(c._h, None, None, 1, 4096, 4, 128, 1, 0, None, 0, None)
     assert st == sdp4.EINVAL                      # stochastic rounding not implemented
     bad = ctypes.c_void_p()
-    assert L.sdp4_comm_init(ctypes.byref(bad), None, 0, 8, 3, 3) == sdp4.EINVAL
+    assert L.sdp4_comm_init(ctypes.byref(bad), None, 0, 8, 3, 3, 0) == sdp4.EINVAL
+    assert L.sdp4_comm_set_chunks(c._h, 17) == sdp4.EINVAL
+    assert c.chunks(16384 * 64) == 1          # world 1 never pipelines
     c.close()
 
 
