@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--b", type=int, default=64)
     ap.add_argument("--chunks", type=str, default="1,3,0", help="NCCL pipeline chunk counts to check (0 = auto)")
     ap.add_argument("--transports", type=str, default="p2p,nccl")
+    ap.add_argument("--full", action="store_true", help="GPT-1.3B-sized buffer, sampled windows (bench config)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -41,6 +42,14 @@ def main():
     P, G, b = world, a.G, a.b
     ok = True
     msgs = []
+    if a.full:
+        ok, msgs = run_full(comm, rank, P, M, N)
+        comm.close()
+        print(f"rank {rank}/{world} ({M}x{N}) {'PASS' if ok else 'FAIL'} full-size {comm.transport} {'; '.join(msgs)}",
+              flush=True)
+        dist.barrier()
+        dist.destroy_process_group()
+        sys.exit(0 if ok else 1)
     runs = []
     for tr in a.transports.split(","):
         runs += [(tr, ch) for ch in ([int(x) for x in a.chunks.split(",")] if tr == "nccl" else [0])]
@@ -57,6 +66,59 @@ def main():
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
+
+
+def run_full(comm, rank, P, M, N, G=128, b=64, win=16384, nwin=6):
+    """bench.py's workload and calls (GPT-1.3B-shaped, bf16 grads/model, G=128, b=64, 4/8/4
+    bits); windows of every shard checked against the oracle (groups are position-local)."""
+    from paper_2410_15526_b200 import pad_numel
+    dev = torch.device("cuda", torch.cuda.current_device())
+    D = pad_numel(synth.gpt_numel("1.3B"), P, G)
+    S = D // P
+    lr = synth.GPT_LR["1.3B"]
+    w_model = synth.model_weights(D, seed=synth.seed_for(0, 1), device=dev)
+    w_model0 = w_model.clone()
+    w_main = synth.main_weights(w_model[rank * S:(rank + 1) * S], seed=synth.seed_for(rank, 2), lr=lr)
+    grad = synth.gradient(D, seed=synth.seed_for(rank, 3), device=dev, dtype=torch.bfloat16)
+    ws_q = torch.empty(comm.qwd_workspace_bytes(D, 4, G), dtype=torch.uint8, device=dev)
+    ws_t = torch.empty(comm.tlq_workspace_bytes(D, 8, 4, G), dtype=torch.uint8, device=dev)
+    out = torch.empty(S, dtype=torch.float32, device=dev)
+    comm.qwd_quantize(w_main, w_model, ws_q, 4, G)
+    comm.qwd_allgather_apply(ws_q, w_model, 4, G)
+    comm.tlq_hs_reduce_scatter(grad, out, ws_t, 8, 4, G, b, True)
+    torch.cuda.synchronize()
+    del grad, ws_q, ws_t
+    rng = np.random.default_rng(7)
+    offs = sorted(set(int(x) * win for x in rng.integers(0, S // win - 1, size=nwin)) | {0, S - win})
+    ok, msgs = True, []
+    # qWD: replica windows inside every shard j need rank j's main weights
+    for j in range(P):
+        mj = synth.main_weights(w_model0[j * S:(j + 1) * S], seed=synth.seed_for(j, 2), lr=lr)
+        for o in offs[:3] + offs[-1:]:
+            e = j * S + o
+            _, want = oracle.qwd_step([mj[o:o + win].cpu().numpy()], synth.bf16_bits(w_model0[e:e + win]), 4, G,
+                                      model_bf16=True)
+            if not np.array_equal(synth.bf16_bits(w_model[e:e + win]), want):
+                ok = False
+                msgs.append(f"qWD replica window shard {j} +{o}")
+        del mj
+    # TLq-HS: windows of this rank's output shard need every rank's gradient at shard `rank`
+    pieces = {o: [] for o in offs}
+    for q in range(P):
+        gq = synth.gradient(D, seed=synth.seed_for(q, 3), device=dev, dtype=torch.bfloat16)
+        for o in offs:
+            # a P-shard mini problem whose shard j holds the window of shard j (all shards are
+            # needed only for the layout; the oracle's output shard `rank` uses column `rank`)
+            pieces[o].append(torch.cat([gq[j * S + o:j * S + o + win] for j in range(P)]).float().cpu().numpy())
+        del gq
+    for o in offs:
+        tr = oracle.tlq_hs_reduce_scatter(pieces[o], oracle.Topology(M, N), G, b, 8, 4, True)
+        got = out[o:o + win].cpu().numpy()
+        if not np.array_equal(got.view(np.uint32), tr.out[rank].view(np.uint32)):
+            ok = False
+            msgs.append(f"TLq-HS output window +{o}: {int((got != tr.out[rank]).sum())} differ")
+    msgs.append(f"{len(offs)} windows of {win}")
+    return ok, msgs
 
 
 def run_checks(comm, rank, P, M, N, G, b, S):

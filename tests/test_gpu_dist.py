@@ -20,3 +20,17 @@ def test_dist_parity(nproc, groups):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("PASS") == nproc, r.stdout
+
+
+@pytest.mark.parametrize("groups", [None])
+def test_dist_parity_fullsize(groups):
+    """bench.py's GPT-1.3B workload on every visible GPU (2 x (P/2) split), sampled windows."""
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    nproc = 8 if n >= 8 else (4 if n >= 4 else 2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", "--master-port=29777", os.path.join(ROOT, "tests", "dist_parity.py"), "--full"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("PASS") == nproc, r.stdout
