@@ -84,9 +84,10 @@ int sdp4_comm_chunks(sdp4_comm_t comm, size_t numel, int group);
 /* Host.  Transport of the exchanges (world > 1):
  *   0 NCCL: kernels write the caller's workspace; ncclAllGather / ncclAlltoAll move it
  *     (with the chunked two-stream pipeline above);
- *   1 P2P (default when available: N <= 8, M <= 16, P <= 16): the producing kernel IS the
- *     exchange -- K1/K3/K4 store their quantized tiles straight into the receive buffers of
- *     the ranks that own them over NVLink (CUDA IPC).  Those receive buffers are library-
+ *   1 P2P (default when available: N <= 8, P <= 64): the exchanges are fused into the
+ *     kernels over NVLink (CUDA IPC): K3 and K4 push their quantized tiles straight into the
+ *     receive buffers of the ranks that own them; the qWD all-gather is a pull inside K2
+ *     (unit j read from rank j's buffer while the replica update streams HBM).  Those receive buffers are library-
  *     owned, symmetric, double-buffered by call parity and allocated collectively on first
  *     use (the caller's workspace is then unused); completion is signalled per source with
  *     epoch flags (cuStreamWriteValue32 / cuStreamWaitValue32).  P2P never chunks.

@@ -423,7 +423,7 @@ sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, 
     c->write_value = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(fw);
     c->wait_value = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(fwt);
     const bool p2p_ok = c->write_value && c->wait_value && group_size_N <= sdp4::kMaxN &&
-                        groups_M <= sdp4::kMaxDests && world <= sdp4::kMaxDests && world <= 256;
+                        groups_M <= sdp4::kMaxDests && world <= sdp4::kMaxDests;
     c->transport = p2p_ok ? kTransportP2P : kTransportNccl;
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -554,19 +554,17 @@ sdp4_status sdp4_qwd_quantize(sdp4_comm_t c, const float* w_main_shard, const vo
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int sms = c->sms(chunks.size() > 1);
   if (c->transport == kTransportP2P) {
-    // Alg. 2 l.2-4 fused: K1 stores unit `rank` into every rank's gather buffer (all-gather
-    // push over NVLink), then raises flag[0][rank] on each peer.
+    // Alg. 2 l.2-3: K1 writes unit `rank` into this rank's own symmetric buffer and raises
+    // flag[0][rank] on every peer; the all-gather (l.4) is the pull inside each rank's K2.
     const size_t W = unit_bytes(S, bits, group);
-    if ((s = sym_ensure(c, c->sym_qwd, (size_t)c->world * W, &c->epoch_qwd)) != SDP4_OK) return s;
+    if ((s = sym_ensure(c, c->sym_qwd, W, &c->epoch_qwd)) != SDP4_OK) return s;
     const uint32_t ep = ++c->epoch_qwd;
     sdp4::Dests d;
-    d.n = c->world;
-    d.remote = 0;  // K1 stores are warp-contiguous and go direct to every destination
+    d.n = 1;
+    d.remote = 0;
+    d.p[0] = sym_region(c->sym_qwd, c->rank, ep);
     std::vector<int> all(c->world);
-    for (int q = 0; q < c->world; ++q) {
-      d.p[q] = sym_region(c->sym_qwd, q, ep) + (size_t)c->rank * W;
-      all[q] = q;
-    }
+    for (int q = 0; q < c->world; ++q) all[q] = q;
     const void* shard = static_cast<const uint8_t*>(w_model_full) + (size_t)c->rank * S * es;
     s = launch(c, "K1_qwd_quantize", st, [&] {
       return sdp4::launch_qwd_quantize(w_main_shard, shard, model_dtype, S, bits, group, d, c->sm_count, st);
@@ -611,15 +609,18 @@ sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t c, void* workspace, size_t work
   const bool overlap = chunks.size() > 1;
   const int sms = c->sms(overlap);
   const int P = c->world;
-  if (c->transport == kTransportP2P) {  // wait for every rank's unit, then K2 on the local copy
-    const size_t W = unit_bytes(S, bits, group);
+  if (P > sdp4::kMaxDests) return fail(SDP4_EINVAL, "world %d > %d", P, sdp4::kMaxDests);
+  if (c->transport == kTransportP2P) {  // wait for every rank's unit; K2 pulls unit j from rank j
     const uint32_t ep = c->epoch_qwd;
     std::vector<int> all(P);
     for (int q = 0; q < P; ++q) all[q] = q;
     if ((s = wait_peers(c, st, c->sym_qwd, 0, all, ep)) != SDP4_OK) return s;
-    uint8_t* units = sym_region(c->sym_qwd, c->rank, ep);
+    sdp4::Dests u;
+    u.n = P;
+    u.remote = 0;
+    for (int q = 0; q < P; ++q) u.p[q] = sym_region(c->sym_qwd, q, ep);
     return launch(c, "K2_qwd_apply", st, [&] {
-      return sdp4::launch_qwd_apply(units, W, P, S, S, bits, group, w_model_full, model_dtype, c->sm_count, st);
+      return sdp4::launch_qwd_apply(u, P, S, S, bits, group, w_model_full, model_dtype, c->sm_count, st);
     });
   }
   if (P > 1) c->link(st, c->side);  // the units of every chunk were written on st (K1)
@@ -635,8 +636,12 @@ sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t c, void* workspace, size_t work
     }
     // Alg. 2 l.5 for chunk c: every shard j's sub-range [j*S + off, +len) of the replica
     uint8_t* wm = static_cast<uint8_t*>(w_model_full) + ch.off * es;
+    sdp4::Dests u;
+    u.n = P;
+    u.remote = 0;
+    for (int q = 0; q < P && q < sdp4::kMaxDests; ++q) u.p[q] = region + (size_t)q * W;
     s = launch(c, "K2_qwd_apply", st, [&] {
-      return sdp4::launch_qwd_apply(region, W, P, ch.len, S, bits, group, wm, model_dtype, sms, st);
+      return sdp4::launch_qwd_apply(u, P, ch.len, S, bits, group, wm, model_dtype, sms, st);
     });
     if (s != SDP4_OK) return s;
     region += (size_t)P * W;

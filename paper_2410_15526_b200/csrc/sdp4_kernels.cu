@@ -531,8 +531,11 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
 
 // =====================================================================================
 // K2  qWD apply (Alg. 2 l.5): w_model[jS + e] = bf16_rn(widen(w) + code*rn(s/q))
-// for every shard j of the gathered units (w_model shard j at w_model + j*stride).  Each
-// thread updates two 16-element vectors per tile, all loads issued up front.
+// for every shard j (w_model shard j at w_model + j*stride), unit j read through units.p[j]:
+// the gathered local copy (NCCL transport) or, with the P2P transport, rank j's own buffer
+// over NVLink -- the all-gather (Alg. 2 l.4) fused into the consumer as a pull, so the
+// NVLink ingress overlaps the HBM-bound replica update.  Each thread updates two 16-element
+// vectors per tile, all loads issued up front.
 // =====================================================================================
 template <int BITS>
 struct K2Vec {
@@ -605,14 +608,13 @@ __device__ __forceinline__ void k2_apply(const uint4* cw, float sc, uint4* mw, T
 }
 
 template <typename TM, int BITS>
-__global__ void __launch_bounds__(kVecThreads) k2_qwd_apply(const uint8_t* __restrict__ units,
-                                                               size_t unit_bytes, size_t S, size_t stride, int P,
+__global__ void __launch_bounds__(kVecThreads) k2_qwd_apply(const Dests units, size_t S, size_t stride, int P,
                                                                int lg, TM* __restrict__ w_model, float z) {
   constexpr int TILE = kVecThreads * 32;
   const size_t tpu = (S + TILE - 1) / TILE;
   for (size_t tile = blockIdx.x; tile < tpu * P; tile += gridDim.x) {
     const size_t j = tile / tpu, ts = tile - j * tpu;
-    const uint8_t* unit = units + j * unit_bytes;
+    const uint8_t* unit = units.p[j];  // unit j: local, or rank j's own buffer (P2P pull over NVLink)
     const float* scales = reinterpret_cast<const float*>(unit + S * (BITS == 32 ? 4 : BITS) / 8);
     TM* wm = w_model + j * stride;
     const size_t ea = ts * TILE + threadIdx.x * 16, eb = ea + TILE / 2;
@@ -1251,11 +1253,11 @@ cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_qwd_apply(const uint8_t* units, size_t unit_bytes, int P, size_t S, size_t stride, int bits,
-                             int G, void* w_model, int model_dtype, int sms, cudaStream_t st) {
+cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride, int bits, int G, void* w_model,
+                             int model_dtype, int sms, cudaStream_t st) {
   const int grid = grid_for((S + kVecThreads * 32 - 1) / (kVecThreads * 32) * P, sms * kVecCtas);
 #define K2(TM, B)                                                                                  \
-  k2_qwd_apply<TM, B><<<grid, kVecThreads, 0, st>>>(units, unit_bytes, S, stride, P, __builtin_ctz(G), \
+  k2_qwd_apply<TM, B><<<grid, kVecThreads, 0, st>>>(units, S, stride, P, __builtin_ctz(G), \
                                                     static_cast<TM*>(w_model), -0.0f)
   if (model_dtype == kBF16) {
     if (bits == 4) K2(uint16_t, 4); else if (bits == 8) K2(uint16_t, 8); else K2(uint16_t, 32);

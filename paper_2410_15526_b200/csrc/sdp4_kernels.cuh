@@ -19,7 +19,7 @@ enum Dtype { kF32 = 0, kBF16 = 1 };
 // Destination wire units (or blocks) of a producing kernel: local send buffers for the
 // NCCL transport, or peers' receive buffers (CUDA IPC over NVLink) for the fused P2P
 // transport, where the producing kernel is the exchange (all-gather / all-to-all push).
-constexpr int kMaxDests = 16;
+constexpr int kMaxDests = 64;
 constexpr int kMaxN = 8;  // max local ranks per group (K3 keeps one tensor map per destination)
 struct Dests {
   uint8_t* p[kMaxDests];
@@ -32,9 +32,10 @@ struct Dests {
 cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, int model_dtype,
                                 size_t S, int bits, int G, const Dests& dst, int sms, cudaStream_t st);
 
-// K2: Alg. 2 l.5 -- for every shard j < P: w_model[j*stride ..+S] += dequant(unit j), in place.
-cudaError_t launch_qwd_apply(const uint8_t* units, size_t unit_bytes, int P, size_t S, size_t stride, int bits,
-                             int G, void* w_model, int model_dtype, int sms, cudaStream_t st);
+// K2: Alg. 2 l.5 -- for every shard j < P: w_model[j*stride ..+S] += dequant(unit units.p[j])
+// (local or peer memory), in place.
+cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride, int bits, int G, void* w_model,
+                             int model_dtype, int sms, cudaStream_t st);
 
 // K3: Alg. 3 l.2-3 -- blockwise Hadamard (b, in {0,2,..,256}) + bits_intra quantization
 // of S elements of each of the P shards (shard j at grad + j*grad_stride elements); shard
