@@ -209,27 +209,27 @@ __device__ __forceinline__ void store_tile(const uint8_t* s_codes, uint32_t cbyt
 // index XOR address bits 7..); R == 256: two boxes (halves) {128, 1, 256, 1}, smem
 // [2][256][128], SWIZZLE_128B.  Thread r touching chunk c of its own row is conflict-free
 // (8 consecutive rows of a quarter-warp hit 8 distinct bank groups).
-template <int R>
+template <int R, int ROWS = kTileRows>
 __device__ __forceinline__ uint32_t tile_off(int r, int c) {
-  if constexpr (R == 256) return (c >> 3) * (kTileRows * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+  if constexpr (R == 256) return (c >> 3) * (ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4);
   else if constexpr (R == 128) return r * 128 + ((c ^ (r & 7)) << 4);
   else if constexpr (R == 64) return r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
   else return r * 32 + ((c ^ ((r >> 2) & 1)) << 4);
 }
-template <int R>
+template <int R, int ROWS = kTileRows>
 __device__ __forceinline__ void tma_load_tile(void* dst, const CUtensorMap* map, uint64_t* bar, int row, int unit) {
   if constexpr (R == 256) {
     tma_load_4d(dst, map, bar, 0, 0, row, unit);
-    tma_load_4d(static_cast<uint8_t*>(dst) + kTileRows * 128, map, bar, 0, 1, row, unit);
+    tma_load_4d(static_cast<uint8_t*>(dst) + ROWS * 128, map, bar, 0, 1, row, unit);
   } else {
     tma_load_3d(dst, map, bar, 0, row, unit);
   }
 }
-template <int R>
+template <int R, int ROWS = kTileRows>
 __device__ __forceinline__ void tma_store_tile(const CUtensorMap* map, const void* src, int row, int unit) {
   if constexpr (R == 256) {
     tma_store_4d(map, src, 0, 0, row, unit);
-    tma_store_4d(map, static_cast<const uint8_t*>(src) + kTileRows * 128, 0, 1, row, unit);
+    tma_store_4d(map, static_cast<const uint8_t*>(src) + ROWS * 128, 0, 1, row, unit);
   } else {
     tma_store_3d(map, src, 0, row, unit);
   }
@@ -345,12 +345,12 @@ __device__ __forceinline__ void dec4x8_2(uint32_t w, float* f) {
 
 // Decode the 64 codes of row t of a row tile (R = 64*BIN/8 bytes) and dequantize:
 // x[i] = {code_i * ds0, code_{i+32} * ds1} (ds0 for elements 0..31, ds1 for 32..63).
-template <int BIN, int R>
+template <int BIN, int R, int ROWS>
 __device__ __forceinline__ void dequant_row(const uint8_t* tile, int t, float ds0, float ds1, float z, float2* x) {
   float f[64];
 #pragma unroll
   for (int c = 0; c < R / 16; ++c) {
-    const uint4 u = *reinterpret_cast<const uint4*>(tile + tile_off<R>(t, c));
+    const uint4 u = *reinterpret_cast<const uint4*>(tile + tile_off<R, ROWS>(t, c));
     if constexpr (BIN == 4) {
       dec4x8_2(u.x, f + 32 * c); dec4x8_2(u.y, f + 32 * c + 8); dec4x8_2(u.z, f + 32 * c + 16);
       dec4x8_2(u.w, f + 32 * c + 24);
@@ -1027,19 +1027,22 @@ __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const 
 // sources summed in order m'' = 0..M-1 (R8); out = rn(H_unnorm(acc) * kappa) (R8) is
 // written into a double-buffered swizzled smem tile that thread 0 TMA-stores.
 // =====================================================================================
+constexpr int kK5Rows = 128;  // K5 tile rows = threads per CTA (two CTAs per SM)
+constexpr int kK5Ctas = 2;
+
 template <int IN_R>
 struct K5Cfg {
-  static constexpr int IN_TILE = kTileRows * IN_R;
-  static constexpr int SC_BYTES = 2048;  // kTileElems / 32 groups * 4 bytes (G >= 32)
+  static constexpr int IN_TILE = kK5Rows * IN_R;
+  static constexpr int SC_BYTES = kK5Rows * 64 / 32 * 4;  // G >= 32
   static constexpr int STAGE = IN_TILE + SC_BYTES;
-  static constexpr int OUT_TILE = kTileRows * 256;
-  static constexpr int S0 = (200 * 1024 - 2 * OUT_TILE) / STAGE;
+  static constexpr int OUT_TILE = kK5Rows * 256;
+  static constexpr int S0 = (100 * 1024 - 2 * OUT_TILE) / STAGE;
   static constexpr int STAGES = S0 > 6 ? 6 : (S0 < 1 ? 1 : S0);
   static constexpr int SMEM = STAGES * STAGE + 2 * OUT_TILE + 64 + 1024;
 };
 
 template <int IN_R, int B>
-__global__ void __launch_bounds__(kTileRows, 1)
+__global__ void __launch_bounds__(kK5Rows, kK5Ctas)
     k5_tlq_dq_reduce_had(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
                          const uint8_t* __restrict__ recv, size_t in_unit_bytes, int M, size_t S, int lg, float kappa,
                          uint32_t ntiles, float z) {
@@ -1064,14 +1067,14 @@ __global__ void __launch_bounds__(kTileRows, 1)
       const int s = k % STAGES;
       uint32_t sb = 0;
       if constexpr (BIN != 32) {
-        const uint32_t rows = min((uint32_t)kTileRows, rows_per_shard - tile * kTileRows);
+        const uint32_t rows = min((uint32_t)kK5Rows, rows_per_shard - tile * kK5Rows);
         sb = (((rows * kRowElems) >> lg) * 4 + 15) & ~15u;
       }
       mbar_arrive_tx(&bar[s], C::IN_TILE + sb);
-      tma_load_tile<IN_R>(smem + s * C::STAGE, &in_map, &bar[s], (int)(tile * kTileRows), (int)m);
+      tma_load_tile<IN_R, kK5Rows>(smem + s * C::STAGE, &in_map, &bar[s], (int)(tile * kK5Rows), (int)m);
       if constexpr (BIN != 32)
         bulk_load(smem + s * C::STAGE + C::IN_TILE,
-                  recv + (size_t)m * in_unit_bytes + S * BIN / 8 + (((size_t)tile * kTileElems) >> lg) * 4, sb,
+                  recv + (size_t)m * in_unit_bytes + S * BIN / 8 + (((size_t)tile * kK5Rows * kRowElems) >> lg) * 4, sb,
                   &bar[s]);
     }
   };
@@ -1100,7 +1103,7 @@ __global__ void __launch_bounds__(kTileRows, 1)
         }
       }
       float2 x[32];
-      dequant_row<BIN, IN_R>(st, t, ds0, ds1, z, x);
+      dequant_row<BIN, IN_R, kK5Rows>(st, t, ds0, ds1, z, x);
       // R8 order; the first add 0 + x_0 is exact for quantized inputs (x_0 != -0).
       if (m == 0 && BIN != 32) {
 #pragma unroll
@@ -1125,13 +1128,13 @@ __global__ void __launch_bounds__(kTileRows, 1)
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const float2* q = acc + 4 * (c & 7);
-      *reinterpret_cast<float4*>(ot + tile_off<256>(t, c)) =
+      *reinterpret_cast<float4*>(ot + tile_off<256, kK5Rows>(t, c)) =
           c < 8 ? make_float4(q[0].x, q[1].x, q[2].x, q[3].x) : make_float4(q[0].y, q[1].y, q[2].y, q[3].y);
     }
     fence_proxy_async();
     __syncthreads();
     if (t == 0) {
-      tma_store_tile<256>(&out_map, ot, (int)(tile * kTileRows), 0);
+      tma_store_tile<256, kK5Rows>(&out_map, ot, (int)(tile * kK5Rows), 0);
       bulk_commit();
     }
   }
@@ -1161,7 +1164,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // Tensor map over `units` units of `rows` rows of R bytes (row tiles of kTileRows rows).
 cudaError_t make_row_map(CUtensorMap* map, const void* base, int R, uint64_t rows, uint64_t units,
-                         uint64_t unit_stride) {
+                         uint64_t unit_stride, int box_rows = kTileRows) {
   auto fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;
   cuuint32_t estr[4] = {1, 1, 1, 1};
@@ -1171,13 +1174,13 @@ cudaError_t make_row_map(CUtensorMap* map, const void* base, int R, uint64_t row
         R == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : (R == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
     cuuint64_t dims[3] = {(cuuint64_t)R, rows, units};
     cuuint64_t strides[2] = {(cuuint64_t)R, unit_stride};
-    cuuint32_t box[3] = {(cuuint32_t)R, (cuuint32_t)kTileRows, 1};
+    cuuint32_t box[3] = {(cuuint32_t)R, (cuuint32_t)box_rows, 1};
     r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
     cuuint64_t dims[4] = {128, 2, rows, units};
     cuuint64_t strides[3] = {128, (cuuint64_t)R, unit_stride};
-    cuuint32_t box[4] = {128, 1, (cuuint32_t)kTileRows, 1};
+    cuuint32_t box[4] = {128, 1, (cuuint32_t)box_rows, 1};
     r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, estr,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1216,7 +1219,7 @@ cudaError_t k5_launch(const CUtensorMap& in_map, const CUtensorMap& out_map, con
   constexpr int SMEM = K5Cfg<IN_R>::SMEM;
   cudaError_t e = set_smem(k5_tlq_dq_reduce_had<IN_R, B>, SMEM);
   if (e != cudaSuccess) return e;
-  k5_tlq_dq_reduce_had<IN_R, B><<<grid, kTileRows, SMEM, st>>>(in_map, out_map, recv, unit_bytes, M, S, __builtin_ctz(G), kappa,
+  k5_tlq_dq_reduce_had<IN_R, B><<<grid, kK5Rows, SMEM, st>>>(in_map, out_map, recv, unit_bytes, M, S, __builtin_ctz(G), kappa,
                                                                 ntiles, -0.0f);
   return cudaGetLastError();
 }
@@ -1318,13 +1321,13 @@ cudaError_t launch_tlq_dq_reduce_had(const uint8_t* inter_recv, size_t in_unit_b
                                      int M, size_t S, int G, int b, float kappa, float* out,
                                      int sms, cudaStream_t st) {
   const uint64_t rows = S / kRowElems;
-  const uint32_t ntiles = (uint32_t)((rows + kTileRows - 1) / kTileRows);
-  const int grid = grid_for(ntiles, sms);
+  const uint32_t ntiles = (uint32_t)((rows + kK5Rows - 1) / kK5Rows);
+  const int grid = grid_for(ntiles, sms * kK5Ctas);
   const int in_r = kRowElems * bits_in / 8;
   CUtensorMap in_map, out_map;
-  cudaError_t e = make_row_map(&in_map, inter_recv, in_r, rows, (uint64_t)M, in_unit_bytes);
+  cudaError_t e = make_row_map(&in_map, inter_recv, in_r, rows, (uint64_t)M, in_unit_bytes, kK5Rows);
   if (e != cudaSuccess) return e;
-  e = make_row_map(&out_map, out, 256, rows, 1, (uint64_t)S * 4);
+  e = make_row_map(&out_map, out, 256, rows, 1, (uint64_t)S * 4, kK5Rows);
   if (e != cudaSuccess) return e;
 #define K5(IR) SDP4_B_SWITCH(b, return (k5_launch<IR, BB>(in_map, out_map, inter_recv, in_unit_bytes, M, S, G, \
                                                           kappa, ntiles, grid, st)))
