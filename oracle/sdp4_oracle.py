@@ -32,7 +32,8 @@ __all__ = [
     "group_scales", "quantize", "dequantize", "fwht_unnormalized", "hadamard_normalized",
     "pack_codes", "unpack_codes", "wire_unit_bytes", "wire_unit", "wire_unit_decode",
     "Topology", "qwd_quantize", "qwd_allgather_apply", "qwd_step",
-    "TlqTrace", "tlq_hs_reduce_scatter", "naive_tlq_hs_reduce_scatter",
+    "TlqTrace", "tlq_hs_reduce_scatter", "naive_tlq_hs_reduce_scatter", "mix32", "sr_key", "sr_uniform",
+    "STAGE_QWD", "STAGE_INTRA", "STAGE_INTER",
     "exact_reduce_scatter_f64", "comm_bits_per_param",
 ]
 
@@ -82,7 +83,43 @@ def group_scales(x: np.ndarray, G: int) -> np.ndarray:
     return np.max(np.abs(X), axis=1).astype(F32)
 
 
-def quantize(x: np.ndarray, k: int, G: int, c: np.float32 = F32(1.0)):
+# --------------------------------------------------------------------------
+# Stochastic rounding (NEXT-2; reading R14): the convergence theory assumes an
+# unbiased gradient compressor E[U(v)] = v (Def. 1; Remark 2).
+# Counter-based: the uniform draw of element i is a pure function of (seed, stage,
+# rank, i), so any schedule reproduces it.  Stages: qWD = 1, intra = 2, inter = 3.
+# --------------------------------------------------------------------------
+STAGE_QWD, STAGE_INTRA, STAGE_INTER = 1, 2, 3
+_U32 = np.uint32
+
+
+def mix32(x):
+    """32-bit finalizer: x ^= x>>16; x *= 0x7feb352d; x ^= x>>15; x *= 0x846ca68b; x ^= x>>16
+    (all arithmetic mod 2^32)."""
+    x = np.asarray(x, dtype=np.uint64) & 0xFFFFFFFF
+    x ^= x >> 16
+    x = (x * 0x7FEB352D) & 0xFFFFFFFF
+    x ^= x >> 15
+    x = (x * 0x846CA68B) & 0xFFFFFFFF
+    x ^= x >> 16
+    return x.astype(np.uint32)
+
+
+def sr_key(seed: int, stage: int, rank: int) -> int:
+    lo, hi = seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF
+    return int(mix32(lo ^ int(mix32(hi ^ ((stage << 24) & 0xFFFFFFFF) ^ rank))))
+
+
+def sr_uniform(index: np.ndarray, key: int) -> np.ndarray:
+    """U_i = (h_i >> 8) * 2^-24 in [0, 1), h_i = mix32(lo32(i) ^ mix32(hi32(i) ^ key))."""
+    i = np.asarray(index, dtype=np.uint64)
+    lo = (i & np.uint64(0xFFFFFFFF)).astype(np.uint64)
+    hi = (i >> np.uint64(32)).astype(np.uint64)
+    h = mix32(lo ^ mix32(hi ^ np.uint64(key)).astype(np.uint64))
+    return ((h >> 8).astype(np.float64) * 2.0 ** -24).astype(F32)
+
+
+def quantize(x: np.ndarray, k: int, G: int, c: np.float32 = F32(1.0), sr=None):
     """Group-wise k-bit quantization of x.
 
     Returns (codes, scales).  codes: int32 in [-q_k, q_k] (R4: -2^(k-1) is never
@@ -98,6 +135,9 @@ def quantize(x: np.ndarray, k: int, G: int, c: np.float32 = F32(1.0)):
     of a tiny group is stored as 0 and of a non-finite group as rn(s*c) (NaN or
     +Inf), so that dequantization poisons the group (R2, R5).
     k = 32 is the identity codec (R12): returns (rn(x*c) as fp32, None).
+    sr = (base_index, key): stochastic rounding (R14) of element j with the uniform draw of
+    global index base_index + j: y = rn(x*inv), fl = floor(y), fr = rn(y - fl),
+    code = clamp(fl + [U < fr], +-q_k).
     """
     x = np.asarray(x, dtype=F32)
     if k == IDENTITY_BITS:
@@ -108,9 +148,18 @@ def quantize(x: np.ndarray, k: int, G: int, c: np.float32 = F32(1.0)):
     ok = np.isfinite(s) & (s >= TINY)
     with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
         inv = np.where(ok, q / np.where(ok, s, F32(1.0)), F32(0.0)).astype(F32)
-        y = X.astype(np.float64) * inv.astype(np.float64)[:, None]     # exact product
-        y = np.where(ok[:, None], y, 0.0)
-        codes = np.clip(np.rint(y), -q, q).astype(np.int32)
+        if sr is None:
+            y = X.astype(np.float64) * inv.astype(np.float64)[:, None]     # exact product
+            y = np.where(ok[:, None], y, 0.0)
+            codes = np.clip(np.rint(y), -q, q).astype(np.int32)
+        else:
+            base, key = sr
+            y = (X * inv[:, None]).astype(F32)                            # rn(x * inv)
+            y = np.where(ok[:, None], y, F32(0.0))
+            fl = np.floor(y).astype(F32)
+            fr = (y - fl).astype(F32)
+            u = sr_uniform(base + np.arange(X.size, dtype=np.uint64), key).reshape(X.shape)
+            codes = np.clip(fl + (u < fr).astype(F32), -q, q).astype(np.int32)
         scales = np.where(s < TINY, F32(0.0), s * F32(c)).astype(F32)
     return codes.reshape(-1), scales
 
@@ -245,14 +294,14 @@ class Topology:
 # --------------------------------------------------------------------------
 # qWD: quantized weight differences (sec. 3.1; Alg. 2 l.2-5)
 # --------------------------------------------------------------------------
-def qwd_quantize(w_main_shard: np.ndarray, w_model_shard: np.ndarray, k: int, G: int):
+def qwd_quantize(w_main_shard: np.ndarray, w_model_shard: np.ndarray, k: int, G: int, sr=None):
     """Alg. 2 l.2-3 on worker p:
          d[p] = w_main[p] - w_model[p]                  (fp32, R11)
          d~[p] = QuantizeWeightsDiff(d[p])              (k-bit group quantizer)
     w_model_shard is the fp32 value of the stored model weights (bf16 widened
     exactly, or fp32).  Returns (codes, scales, d)."""
     d = (np.asarray(w_main_shard, dtype=F32) - np.asarray(w_model_shard, dtype=F32)).astype(F32)
-    codes, scales = quantize(d, k, G)
+    codes, scales = quantize(d, k, G, sr=sr)
     return codes, scales, d
 
 
@@ -269,15 +318,17 @@ def qwd_allgather_apply(units, w_model: np.ndarray, k: int, G: int, model_bf16: 
     return bf16_round(acc) if model_bf16 else acc
 
 
-def qwd_step(w_main_shards, w_model, k: int, G: int, model_bf16: bool):
+def qwd_step(w_main_shards, w_model, k: int, G: int, model_bf16: bool, seed=None):
     """One qWD iteration over all P simulated workers (Alg. 2 l.2-5).
     w_main_shards: list of P fp32 shards; w_model: replica (uint16 bf16 bits if
-    model_bf16 else fp32).  Returns (units, new_w_model)."""
+    model_bf16 else fp32).  seed: stochastic rounding (R14, stage qWD, element index = the
+    global index p*S + j of d).  Returns (units, new_w_model)."""
     wm = bf16_widen(w_model) if model_bf16 else np.asarray(w_model, dtype=F32)
     S = len(w_main_shards[0])
     units = []
     for p, shard in enumerate(w_main_shards):
-        c, s, _ = qwd_quantize(shard, wm[p * S:(p + 1) * S], k, G)
+        sr = None if seed is None else (p * S, sr_key(seed, STAGE_QWD, p))
+        c, s, _ = qwd_quantize(shard, wm[p * S:(p + 1) * S], k, G, sr)
         units.append((c, s))
     return units, qwd_allgather_apply(units, wm, k, G, model_bf16)
 
@@ -300,10 +351,13 @@ class TlqTrace:
 
 
 def tlq_hs_reduce_scatter(grads, topo: Topology, G: int, b: int,
-                          k_intra: int = 8, k_inter: int = 4, average: bool = True) -> TlqTrace:
+                          k_intra: int = 8, k_inter: int = 4, average: bool = True, seed=None) -> TlqTrace:
     """Alg. 3 with the sec. 3.3 pruning, simulated for all P = M*N workers.
 
     grads: list of P fp32 arrays (the local gradients g^p_model, each of length D).
+    seed: stochastic rounding (R14) for both quantizers: the intra message of rank r for
+    shard j draws with key (seed, intra, r) at the gradient's global index j*S + e; the inter
+    message of rank r for shard j with key (seed, inter, r) at index j*S + e.
     Returns a TlqTrace whose out[r] is g_main[r] (Alg. 2 l.9).
     """
     M, N, P = topo.M, topo.N, topo.P
@@ -325,7 +379,8 @@ def tlq_hs_reduce_scatter(grads, topo: Topology, G: int, b: int,
             sub = []
             for mp in range(M):
                 j = mp * N + lp
-                sub.append(quantize(u[j * S:(j + 1) * S], k_intra, G, cb))
+                sr = None if seed is None else (j * S, sr_key(seed, STAGE_INTRA, r))
+                sub.append(quantize(u[j * S:(j + 1) * S], k_intra, G, cb, sr))
             blocks.append(sub)
         tr.intra_send.append(blocks)
 
@@ -341,7 +396,9 @@ def tlq_hs_reduce_scatter(grads, topo: Topology, G: int, b: int,
             for lpp in range(N):
                 codes, scales = tr.intra_send[topo.rank(m, lpp)][l][mp]
                 acc = (acc + dequantize(codes, scales, k_intra, G)).astype(F32)
-            sends.append(quantize(acc, k_inter, G))
+            j = mp * N + l
+            sr = None if seed is None else (j * S, sr_key(seed, STAGE_INTER, r))
+            sends.append(quantize(acc, k_inter, G, sr=sr))
         tr.inter_send.append(sends)
 
     # Alg. 3 l.10 InterAlltoAll: worker (m, l) receives from (m'', l) the
