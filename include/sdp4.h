@@ -43,7 +43,16 @@ typedef enum {
 } sdp4_status;
 
 typedef enum { SDP4_F32 = 0, SDP4_BF16 = 1 } sdp4_dtype;
-typedef enum { SDP4_RNE = 0, SDP4_STOCHASTIC = 1 /* reserved (NEXT-2); rejected with EINVAL */ } sdp4_round;
+/* Rounding of the quantizers.  SDP4_RNE: code = RNE(x * rn(q/s)) of the exact product (R3).
+ * SDP4_STOCHASTIC (NEXT-2, R14; unbiased as the convergence theory assumes for gradients,
+ * Def. 1): y = rn(x * rn(q/s)), fl = floor(y), fr = rn(y - fl),
+ * code = clamp(fl + [U < fr], +-q) with U = (h >> 8) * 2^-24,
+ * h = mix32(lo32(i) ^ mix32(hi32(i) ^ key)), key = mix32(seed_lo ^ mix32(seed_hi ^
+ * (stage << 24) ^ rank)), stage qWD = 1 / intra = 2 / inter = 3, i = the element's global
+ * index (d: rank*S + e; gradient: its index in the full buffer; inter message: its index
+ * in the full buffer), rank = the quantizing rank; mix32(x): x ^= x >> 16;
+ * x *= 0x7feb352d; x ^= x >> 15; x *= 0x846ca68b; x ^= x >> 16.  Pass a new seed per call. */
+typedef enum { SDP4_RNE = 0, SDP4_STOCHASTIC = 1 } sdp4_round;
 
 /* Opaque communicator: world + intra (N ranks of group m) + inter (M ranks of
  * local rank l) NCCL communicators, plus profiling state.  P:292 sec. 2.3. */
@@ -139,7 +148,7 @@ size_t sdp4_tlq_workspace_offset(int groups_M, int group_size_N, size_t numel, i
  * w_main_shard: fp32[S] (this rank's main weights).  w_model_full: the
  * full replica D elements of model_dtype (bf16 or fp32); only
  * [r*S, (r+1)*S) is read.  bits in {4, 8, 32}; G power of two in [32, 2048].
- * rnd must be SDP4_RNE (seed ignored). */
+ * rnd / seed: rounding of the codes (see sdp4_round). */
 sdp4_status sdp4_qwd_quantize(sdp4_comm_t comm, const float* w_main_shard, const void* w_model_full,
                               sdp4_dtype model_dtype, size_t numel, int bits, int group,
                               sdp4_round rnd, uint64_t seed, void* workspace, size_t workspace_bytes,
@@ -187,9 +196,10 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t comm, const void* grad, sdp4_
  *   stage_final     K5: Alg. 3 l.11-13: inter_recv -> out_shard (S) */
 sdp4_status sdp4_tlq_stage_quantize(const void* grad, sdp4_dtype grad_dtype, size_t numel, int groups_M,
                                     int group_size_N, int bits_intra, int group, int hadamard_block,
-                                    void* intra_send, void* stream);
+                                    sdp4_round rnd, uint64_t seed, int rank, void* intra_send, void* stream);
 sdp4_status sdp4_tlq_stage_reduce(const void* intra_recv, size_t numel, int groups_M, int group_size_N,
-                                  int bits_intra, int bits_inter, int group, void* inter_send, void* stream);
+                                  int bits_intra, int bits_inter, int group, sdp4_round rnd, uint64_t seed,
+                                  int rank, void* inter_send, void* stream);
 sdp4_status sdp4_tlq_stage_final(const void* inter_recv, size_t numel, int groups_M, int group_size_N,
                                  int bits_inter, int group, int hadamard_block, int average, float* out_shard,
                                  void* stream);

@@ -376,6 +376,21 @@ int sm_count_current() {
 
 size_t esize(sdp4_dtype d) { return d == SDP4_BF16 ? 2 : 4; }
 
+// Stochastic rounding key (R14): key = mix32(seed_lo ^ mix32(seed_hi ^ (stage << 24) ^ rank)).
+uint32_t mix32_host(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+enum { kStageQwd = 1, kStageIntra = 2, kStageInter = 3 };
+uint32_t sr_key(uint64_t seed, int stage, int rank) {
+  return mix32_host((uint32_t)seed ^ mix32_host((uint32_t)(seed >> 32) ^ ((uint32_t)stage << 24) ^ (uint32_t)rank));
+}
+bool valid_round(sdp4_round r) { return r == SDP4_RNE || r == SDP4_STOCHASTIC; }
+
 }  // namespace
 
 extern "C" {
@@ -534,10 +549,9 @@ size_t sdp4_tlq_workspace_offset(int M, int N, size_t numel, int bi, int be, int
 sdp4_status sdp4_qwd_quantize(sdp4_comm_t c, const float* w_main_shard, const void* w_model_full,
                               sdp4_dtype model_dtype, size_t numel, int bits, int group, sdp4_round rnd,
                               uint64_t seed, void* workspace, size_t workspace_bytes, void* stream) {
-  (void)seed;
   g_err.clear();
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
-  if (rnd != SDP4_RNE) return fail(SDP4_EINVAL, "only SDP4_RNE rounding is implemented");
+  if (!valid_round(rnd)) return fail(SDP4_EINVAL, "bad rounding mode %d", (int)rnd);
   if (!valid_bits(bits)) return fail(SDP4_EINVAL, "bits %d not in {4, 8, 32}", bits);
   if (model_dtype != SDP4_F32 && model_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad model dtype");
   sdp4_status s = check_sizes(c->world, numel, group);
@@ -566,8 +580,11 @@ sdp4_status sdp4_qwd_quantize(sdp4_comm_t c, const float* w_main_shard, const vo
     std::vector<int> all(c->world);
     for (int q = 0; q < c->world; ++q) all[q] = q;
     const void* shard = static_cast<const uint8_t*>(w_model_full) + (size_t)c->rank * S * es;
+    const int sr = rnd == SDP4_STOCHASTIC;
+    const uint32_t key = sr_key(seed, kStageQwd, c->rank);
     s = launch(c, "K1_qwd_quantize", st, [&] {
-      return sdp4::launch_qwd_quantize(w_main_shard, shard, model_dtype, S, bits, group, d, c->sm_count, st);
+      return sdp4::launch_qwd_quantize(w_main_shard, shard, model_dtype, S, bits, group, d, sr, key,
+                                       (uint64_t)c->rank * S, c->sm_count, st);
     });
     if (s != SDP4_OK) return s;
     return signal_peers(c, st, c->sym_qwd, 0, all, ep);
@@ -581,7 +598,9 @@ sdp4_status sdp4_qwd_quantize(sdp4_comm_t c, const float* w_main_shard, const vo
     d.remote = 0;
     d.p[0] = region + (size_t)c->rank * W;
     s = launch(c, "K1_qwd_quantize", st, [&] {
-      return sdp4::launch_qwd_quantize(w_main_shard + ch.off, shard, model_dtype, ch.len, bits, group, d, sms, st);
+      return sdp4::launch_qwd_quantize(w_main_shard + ch.off, shard, model_dtype, ch.len, bits, group, d,
+                                       rnd == SDP4_STOCHASTIC, sr_key(seed, kStageQwd, c->rank),
+                                       (uint64_t)c->rank * S + ch.off, sms, st);
     });
     if (s != SDP4_OK) return s;
     region += (size_t)c->world * W;
@@ -653,10 +672,9 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
                                        int bits_intra, int bits_inter, int group, int hadamard_block, int average,
                                        sdp4_round rnd, uint64_t seed, float* out_shard, void* workspace,
                                        size_t workspace_bytes, void* stream) {
-  (void)seed;
   g_err.clear();
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
-  if (rnd != SDP4_RNE) return fail(SDP4_EINVAL, "only SDP4_RNE rounding is implemented");
+  if (!valid_round(rnd)) return fail(SDP4_EINVAL, "bad rounding mode %d", (int)rnd);
   if (grad_dtype != SDP4_F32 && grad_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad grad dtype");
   const int b = hadamard_block;
   sdp4_status s = check_tlq_args(c->world, numel, bits_intra, bits_inter, group, b);
@@ -678,6 +696,8 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaStream_t cs = P > 1 ? c->side : st;  // communication stream
   const float cb = hadamard_cb(b), kappa = final_kappa(b, P, average);
+  const int sr = rnd == SDP4_STOCHASTIC;
+  const uint32_t key8 = sr_key(seed, kStageIntra, c->rank), key4 = sr_key(seed, kStageInter, c->rank);
   if (c->transport == kTransportP2P) {
     // Alg. 3 with both all-to-alls fused into the producing kernels (P2P push).
     const size_t w8 = unit_bytes(S, bits_intra, group), w4 = unit_bytes(S, bits_inter, group);
@@ -694,7 +714,7 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     const uint32_t remote = ((1u << N) - 1u) & ~(1u << l);
     s = launch(c, "K3_tlq_had_quant", st, [&] {
       return sdp4::launch_tlq_had_quant(grad, S, grad_dtype, S, M, N, group, b, cb, bits_intra, blocks, remote, w8,
-                                        c->sm_count, st);
+                                        sr, key8, 0, c->sm_count, st);
     });
     if (s != SDP4_OK) return s;
     if ((s = signal_peers(c, st, c->sym_tlq, 1, group_ranks, ep)) != SDP4_OK) return s;
@@ -707,7 +727,8 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
       d4.p[mp] = sym_region(c->sym_tlq, mp * N + l, ep) + intra_bytes + (size_t)m * w4;
     uint8_t* my = sym_region(c->sym_tlq, c->rank, ep);
     s = launch(c, "K4_tlq_dq_reduce_q", st, [&] {
-      return sdp4::launch_tlq_dq_reduce_q(my, w8, bits_intra, N, M, S, group, d4, bits_inter, c->sm_count, st);
+      return sdp4::launch_tlq_dq_reduce_q(my, w8, bits_intra, N, M, S, group, d4, bits_inter, sr, key4, l, S, 0,
+                                          c->sm_count, st);
     });
     if (s != SDP4_OK) return s;
     if ((s = signal_peers(c, st, c->sym_tlq, 2, node_ranks, ep)) != SDP4_OK) return s;
@@ -733,7 +754,7 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     for (int lp = 0; lp < N && lp < sdp4::kMaxN; ++lp) blocks[lp] = ws + reg[k].send8 + (size_t)lp * M * w8;
     sdp4_status r = launch(c, "K3_tlq_had_quant", st, [&] {
       return sdp4::launch_tlq_had_quant(static_cast<const uint8_t*>(grad) + ch.off * es, S, grad_dtype, ch.len, M, N,
-                                        group, b, cb, bits_intra, blocks, 0u, w8, sms, st);
+                                        group, b, cb, bits_intra, blocks, 0u, w8, sr, key8, ch.off, sms, st);
     });
     if (r != SDP4_OK || N == 1) return r;
     c->link(st, cs);
@@ -751,8 +772,8 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     d4.remote = 0;
     for (int mp = 0; mp < M && mp < sdp4::kMaxDests; ++mp) d4.p[mp] = ws + reg[k].send4 + (size_t)mp * w4;
     sdp4_status r = launch(c, "K4_tlq_dq_reduce_q", st, [&] {
-      return sdp4::launch_tlq_dq_reduce_q(ws + reg[k].recv8, w8, bits_intra, N, M, ch.len, group, d4, bits_inter, sms,
-                                          st);
+      return sdp4::launch_tlq_dq_reduce_q(ws + reg[k].recv8, w8, bits_intra, N, M, ch.len, group, d4, bits_inter, sr,
+                                          key4, c->l, S, ch.off, sms, st);
     });
     if (r != SDP4_OK || M == 1) return r;
     c->link(st, cs);
@@ -781,9 +802,11 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
 }
 
 sdp4_status sdp4_tlq_stage_quantize(const void* grad, sdp4_dtype grad_dtype, size_t numel, int M, int N,
-                                    int bits_intra, int group, int hadamard_block, void* intra_send, void* stream) {
+                                    int bits_intra, int group, int hadamard_block, sdp4_round rnd, uint64_t seed,
+                                    int rank, void* intra_send, void* stream) {
   g_err.clear();
   if (M < 1 || N < 1) return fail(SDP4_EINVAL, "bad topology %d x %d", M, N);
+  if (!valid_round(rnd) || rank < 0 || rank >= M * N) return fail(SDP4_EINVAL, "bad rounding mode or rank");
   if (grad_dtype != SDP4_F32 && grad_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad grad dtype");
   sdp4_status s = check_tlq_args(M * N, numel, bits_intra, 4, group, hadamard_block);
   if (s != SDP4_OK) return s;
@@ -797,14 +820,17 @@ sdp4_status sdp4_tlq_stage_quantize(const void* grad, sdp4_dtype grad_dtype, siz
   for (int lp = 0; lp < N; ++lp) blocks[lp] = static_cast<uint8_t*>(intra_send) + (size_t)lp * M * w8;
   cudaError_t e = sdp4::launch_tlq_had_quant(grad, S, grad_dtype, S, M, N, group, hadamard_block,
                                              hadamard_cb(hadamard_block), bits_intra, blocks, 0u, w8,
+                                             rnd == SDP4_STOCHASTIC, sr_key(seed, kStageIntra, rank), 0,
                                              sm_count_current(), st);
   return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "K3 launch failed: %s", cudaGetErrorString(e));
 }
 
 sdp4_status sdp4_tlq_stage_reduce(const void* intra_recv, size_t numel, int M, int N, int bits_intra,
-                                  int bits_inter, int group, void* inter_send, void* stream) {
+                                  int bits_inter, int group, sdp4_round rnd, uint64_t seed, int rank,
+                                  void* inter_send, void* stream) {
   g_err.clear();
   if (M < 1 || N < 1) return fail(SDP4_EINVAL, "bad topology %d x %d", M, N);
+  if (!valid_round(rnd) || rank < 0 || rank >= M * N) return fail(SDP4_EINVAL, "bad rounding mode or rank");
   sdp4_status s = check_tlq_args(M * N, numel, bits_intra, bits_inter, group, 0);
   if (s != SDP4_OK) return s;
   if ((s = check_ptr(intra_recv, "intra_recv")) != SDP4_OK) return s;
@@ -818,7 +844,8 @@ sdp4_status sdp4_tlq_stage_reduce(const void* intra_recv, size_t numel, int M, i
   for (int mp = 0; mp < M; ++mp) d4.p[mp] = static_cast<uint8_t*>(inter_send) + (size_t)mp * unit_bytes(S, bits_inter, group);
   cudaError_t e = sdp4::launch_tlq_dq_reduce_q(static_cast<const uint8_t*>(intra_recv),
                                                unit_bytes(S, bits_intra, group), bits_intra, N, M, S, group, d4,
-                                               bits_inter, sm_count_current(), st);
+                                               bits_inter, rnd == SDP4_STOCHASTIC, sr_key(seed, kStageInter, rank),
+                                               rank % N, S, 0, sm_count_current(), st);
   return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "K4 launch failed: %s", cudaGetErrorString(e));
 }
 

@@ -63,6 +63,33 @@ __device__ __forceinline__ float stored_scale(float s, float c) {
 // RNE(x * inv) of the exact product (R3: one rounding), as magic-number bits:
 // fma(x, inv, 1.5*2^23) rounds the exact x*inv + 1.5*2^23 once, to an integer.
 __device__ __forceinline__ uint32_t rq(float x, float inv) { return __float_as_uint(__fmaf_rn(x, inv, kMagic)); }
+
+// Stochastic rounding (NEXT-2, R14): counter-based uniform U_i = (h >> 8) * 2^-24 with
+// h = mix32(lo32(i) ^ mix32(hi32(i) ^ key)); y = rn(x*inv), fl = floor(y), fr = rn(y - fl),
+// code = clamp(fl + [U < fr], +-q) -- unbiased (Def. 1).
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+__device__ __forceinline__ float sr_u(uint64_t i, uint32_t key) {
+  const uint32_t h = mix32((uint32_t)i ^ mix32((uint32_t)(i >> 32) ^ key));
+  return __uint2float_rn(h >> 8) * 0x1p-24f;  // exact: 24-bit integer times 2^-24
+}
+__device__ __forceinline__ uint32_t rq_sr(float x, float inv, float u, float q) {
+  const float y = __fmul_rn(x, inv);
+  const float fl = floorf(y);
+  const float fr = __fsub_rn(y, fl);
+  const float c = fminf(fmaxf(__fadd_rn(fl, u < fr ? 1.f : 0.f), -q), q);
+  return __float_as_uint(__fadd_rn(c, kMagic));  // c is a small integer: exact magic bits
+}
+struct SR {
+  int on;        // 0: round to nearest even (R3)
+  uint32_t key;  // per (seed, stage, rank)
+};
 __device__ __forceinline__ uint32_t pack8x4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
@@ -375,9 +402,9 @@ __device__ __forceinline__ void dequant_row(const uint8_t* tile, int t, float ds
 // row-major for a 1-D bulk store to a peer; else the TMA-swizzled layout for a tensor store);
 // the group's first row writes the scale rn(s * c) (R6) to scales_tile.  lg = log2 G:
 // G >= 64 -> a group spans G/64 rows (lanes); G == 32 -> two groups per row (one per half).
-template <int BITS, int R, bool LINEAR>
+template <int BITS, int R, bool LINEAR, bool STOCH>
 __device__ __forceinline__ void quant_row(const float2* p, int t, int lg, float c, bool act, uint8_t* out_tile,
-                                          float* scales_tile) {
+                                          float* scales_tile, const SR& sr, uint64_t i0) {
   constexpr float q = float((1 << (BITS - 1)) - 1);
   float a0 = 0.f, a1 = 0.f;
 #pragma unroll
@@ -400,11 +427,19 @@ __device__ __forceinline__ void quant_row(const float2* p, int t, int lg, float 
   }
   const float2 inv = make_float2(p0.inv, p1.inv);
   uint32_t rx[32], ry[32];
+  if constexpr (STOCH) {  // element i of the row has global index i0 + i (stochastic rounding, R14)
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const float2 y = f2rq(p[i], inv);
-    rx[i] = __float_as_uint(y.x);
-    ry[i] = __float_as_uint(y.y);
+    for (int i = 0; i < 32; ++i) {
+      rx[i] = rq_sr(p[i].x, inv.x, sr_u(i0 + i, sr.key), q);
+      ry[i] = rq_sr(p[i].y, inv.y, sr_u(i0 + 32 + i, sr.key), q);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float2 y = f2rq(p[i], inv);
+      rx[i] = __float_as_uint(y.x);
+      ry[i] = __float_as_uint(y.y);
+    }
   }
   if constexpr (BITS == 8) {
 #pragma unroll
@@ -459,7 +494,8 @@ constexpr int kVecCtas = 8;
 template <typename TM, int BITS>
 __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __restrict__ w_main,
                                                                    const TM* __restrict__ w_model, size_t S,
-                                                                   int lg, const Dests dst) {
+                                                                   int lg, const Dests dst, const SR sr,
+                                                                   uint64_t idx0) {
   constexpr int TILE = kVecThreads * 8;
   __shared__ float red[kVecThreads / 32];
   constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
@@ -508,8 +544,13 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
       const QP p = qparam(a, q);
       if (act) {
         uint32_t r[8];
+        if (sr.on) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) r[i] = rq(d[i], p.inv);
+          for (int i = 0; i < 8; ++i) r[i] = rq_sr(d[i], p.inv, sr_u(idx0 + e0 + i, sr.key), q);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) r[i] = rq(d[i], p.inv);
+        }
         // every destination unit (all-gather push, Alg. 2 l.4): warp-contiguous stores
         if constexpr (BITS == 4) {
           uint32_t w = pack4x8(r);
@@ -655,10 +696,11 @@ struct K3Out {
   uint32_t remote;         // bit l': block l' lives in a peer's memory (P2P push)
 };
 
-template <int IN_R, int BITS, int B>
+template <int IN_R, int BITS, int B, bool STOCH>
 __global__ void __launch_bounds__(kTileRows, 1)
     k3_tlq_had_quant(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ K3Out out, size_t S, int M,
-                     int N, int lg, float cb, size_t unit_bytes, uint32_t tps, uint32_t ntiles) {
+                     int N, int lg, float cb, size_t unit_bytes, uint32_t tps, uint32_t ntiles, const SR sr,
+                     size_t sr_stride, size_t sr_off) {
   constexpr int OUT_R = kRowElems * BITS / 8;
   using C = K3Cfg<IN_R, OUT_R>;
   constexpr int STAGES = C::STAGES;
@@ -740,11 +782,14 @@ __global__ void __launch_bounds__(kTileRows, 1)
         *reinterpret_cast<float4*>(ot + (remote ? t * 256 + 16 * c : tile_off<256>(t, c))) =
             c < 8 ? make_float4(q[0].x, q[1].x, q[2].x, q[3].x) : make_float4(q[0].y, q[1].y, q[2].y, q[3].y);
       }
-    } else if (remote) {  // peer block: linear tile, codes + scales bulk-stored over NVLink
-      quant_row<BITS, OUT_R, true>(p, t, lg, cb, act, ot, osc);
-    } else {              // local block: swizzled tile for the TMA tensor store, scales direct
-      float* gsc = reinterpret_cast<float*>(unit + S * BITS / 8) + (((size_t)ts * kTileElems) >> lg);
-      quant_row<BITS, OUT_R, false>(p, t, lg, cb, act, ot, gsc);
+    } else {
+      const uint64_t i0 = (uint64_t)j * sr_stride + sr_off + ((uint64_t)ts * kTileRows + t) * kRowElems;
+      if (remote) {  // peer block: linear tile, codes + scales bulk-stored over NVLink
+        quant_row<BITS, OUT_R, true, STOCH>(p, t, lg, cb, act, ot, osc, sr, i0);
+      } else {       // local block: swizzled tile for the TMA tensor store, scales direct
+        float* gsc = reinterpret_cast<float*>(unit + S * BITS / 8) + (((size_t)ts * kTileElems) >> lg);
+        quant_row<BITS, OUT_R, false, STOCH>(p, t, lg, cb, act, ot, gsc, sr, i0);
+      }
     }
     fence_proxy_async();
     __syncthreads();
@@ -802,10 +847,11 @@ struct ItemCursor {
   }
 };
 
-template <int BIN, int BOUT>
+template <int BIN, int BOUT, bool STOCH>
 __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
                                                           int N, int M, size_t S, int lg, const Dests dst,
-                                                          uint32_t tpu, uint32_t ntiles, float z) {
+                                                          uint32_t tpu, uint32_t ntiles, float z, const SR sr,
+                                                          int l_self, size_t sr_stride, size_t sr_off) {
   using C = K4Cfg<BIN, BOUT>;
   constexpr int STAGES = C::STAGES, CPT = C::CPT, EPC = C::EPC;
   constexpr float qin = float((1 << (BIN == 32 ? 1 : BIN - 1)) - 1);
@@ -982,14 +1028,23 @@ __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const 
           const bool h = (vbase(v) >> 5) != 0;
           const float iv = h ? p1.inv : p0.inv;
           uint32_t r[16];
+          const int e = 64 * t + vbase(v);
+          if constexpr (STOCH) {  // global index of the shard element (mp*N + l)*S_full + off + e0 + e (R14)
+            const uint64_t i0 = (uint64_t)(mp * N + l_self) * sr_stride + sr_off + e0 + e;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float2 y = f2rq(acc[8 * v + q], make_float2(iv, iv));
-            r[2 * q] = __float_as_uint(y.x);
-            r[2 * q + 1] = __float_as_uint(y.y);
+            for (int q = 0; q < 8; ++q) {
+              r[2 * q] = rq_sr(acc[8 * v + q].x, iv, sr_u(i0 + 2 * q, sr.key), qout);
+              r[2 * q + 1] = rq_sr(acc[8 * v + q].y, iv, sr_u(i0 + 2 * q + 1, sr.key), qout);
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float2 y = f2rq(acc[8 * v + q], make_float2(iv, iv));
+              r[2 * q] = __float_as_uint(y.x);
+              r[2 * q + 1] = __float_as_uint(y.y);
+            }
           }
           const bool okv = h ? p1.ok : p0.ok;
-          const int e = 64 * t + vbase(v);
           if constexpr (BOUT == 4) {
             uint2 w = make_uint2(pack4x8(r), pack4x8(r + 8));
             if (!okv) w = make_uint2(0u, 0u);
@@ -1202,15 +1257,28 @@ cudaError_t make_row_map(CUtensorMap* map, const void* base, int R, uint64_t row
     default: return cudaErrorInvalidValue;                      \
   }
 
+template <int IN_R, int BITS, int B, bool STOCH>
+cudaError_t k3_launch_t(const CUtensorMap& in_map, const K3Out& out, size_t S, int M, int N, int G, float cb,
+                        size_t unit_bytes, uint32_t tps, uint32_t ntiles, int grid, const SR& sr, size_t sr_stride,
+                        size_t sr_off, cudaStream_t st) {
+  constexpr int SMEM = K3Cfg<IN_R, kRowElems * BITS / 8>::SMEM;
+  cudaError_t e = set_smem(k3_tlq_had_quant<IN_R, BITS, B, STOCH>, SMEM);
+  if (e != cudaSuccess) return e;
+  k3_tlq_had_quant<IN_R, BITS, B, STOCH><<<grid, kTileRows, SMEM, st>>>(in_map, out, S, M, N, __builtin_ctz(G), cb,
+                                                                         unit_bytes, tps, ntiles, sr, sr_stride, sr_off);
+  return cudaGetLastError();
+}
 template <int IN_R, int BITS, int B>
 cudaError_t k3_launch(const CUtensorMap& in_map, const K3Out& out, size_t S, int M, int N, int G, float cb,
-                      size_t unit_bytes, uint32_t tps, uint32_t ntiles, int grid, cudaStream_t st) {
-  constexpr int SMEM = K3Cfg<IN_R, kRowElems * BITS / 8>::SMEM;
-  cudaError_t e = set_smem(k3_tlq_had_quant<IN_R, BITS, B>, SMEM);
-  if (e != cudaSuccess) return e;
-  k3_tlq_had_quant<IN_R, BITS, B><<<grid, kTileRows, SMEM, st>>>(in_map, out, S, M, N, __builtin_ctz(G), cb,
-                                                                  unit_bytes, tps, ntiles);
-  return cudaGetLastError();
+                      size_t unit_bytes, uint32_t tps, uint32_t ntiles, int grid, const SR& sr, size_t sr_stride,
+                      size_t sr_off, cudaStream_t st) {
+  if constexpr (BITS != 32) {
+    if (sr.on)
+      return k3_launch_t<IN_R, BITS, B, true>(in_map, out, S, M, N, G, cb, unit_bytes, tps, ntiles, grid, sr, sr_stride,
+                                              sr_off, st);
+  }
+  return k3_launch_t<IN_R, BITS, B, false>(in_map, out, S, M, N, G, cb, unit_bytes, tps, ntiles, grid, sr, sr_stride,
+                                           sr_off, st);
 }
 
 template <int IN_R, int B>
@@ -1224,29 +1292,39 @@ cudaError_t k5_launch(const CUtensorMap& in_map, const CUtensorMap& out_map, con
   return cudaGetLastError();
 }
 
-template <int BIN, int BOUT>
-cudaError_t k4_launch(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
-                      int sms, cudaStream_t st) {
+template <int BIN, int BOUT, bool STOCH>
+cudaError_t k4_launch_t(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
+                        const SR& sr, int l_self, size_t sr_stride, size_t sr_off, int sms, cudaStream_t st) {
   constexpr int SMEM = K4Cfg<BIN, BOUT>::SMEM;
-  cudaError_t e = set_smem(k4_tlq_dq_reduce_q<BIN, BOUT>, SMEM);
+  cudaError_t e = set_smem(k4_tlq_dq_reduce_q<BIN, BOUT, STOCH>, SMEM);
   if (e != cudaSuccess) return e;
   const uint32_t tpu = (uint32_t)((S + kK4Tile - 1) / kK4Tile);
   const uint32_t ntiles = tpu * (uint32_t)M;
   const int grid = grid_for(ntiles, sms * kK4Ctas);
-  k4_tlq_dq_reduce_q<BIN, BOUT><<<grid, kK4Threads, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G), dst, tpu,
-                                                         ntiles, -0.0f);
+  k4_tlq_dq_reduce_q<BIN, BOUT, STOCH><<<grid, kK4Threads, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G),
+                                                                dst, tpu, ntiles, -0.0f, sr, l_self, sr_stride, sr_off);
   return cudaGetLastError();
+}
+template <int BIN, int BOUT>
+cudaError_t k4_launch(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
+                      const SR& sr, int l_self, size_t sr_stride, size_t sr_off, int sms, cudaStream_t st) {
+  if constexpr (BOUT != 32) {
+    if (sr.on) return k4_launch_t<BIN, BOUT, true>(recv, in_unit_bytes, N, M, S, G, dst, sr, l_self, sr_stride, sr_off, sms, st);
+  }
+  return k4_launch_t<BIN, BOUT, false>(recv, in_unit_bytes, N, M, S, G, dst, sr, l_self, sr_stride, sr_off, sms, st);
 }
 
 }  // namespace
 
 // ------------------------------- launchers -------------------------------------------
 cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, int model_dtype,
-                                size_t S, int bits, int G, const Dests& dst, int sms,
-                                cudaStream_t st) {
+                                size_t S, int bits, int G, const Dests& dst, int sr_on, uint32_t sr_key,
+                                uint64_t idx0, int sms, cudaStream_t st) {
+  const SR sr{sr_on, sr_key};
   const int grid = grid_for((S + kVecThreads * 8 - 1) / (kVecThreads * 8), sms * kVecCtas);
 #define K1(TM, B) \
-  k1_qwd_quantize<TM, B><<<grid, kVecThreads, 0, st>>>(w_main, static_cast<const TM*>(w_model_shard), S, __builtin_ctz(G), dst)
+  k1_qwd_quantize<TM, B><<<grid, kVecThreads, 0, st>>>(w_main, static_cast<const TM*>(w_model_shard), S, __builtin_ctz(G), dst, \
+                                                       sr, idx0)
   if (model_dtype == kBF16) {
     if (bits == 4) K1(uint16_t, 4); else if (bits == 8) K1(uint16_t, 8); else K1(uint16_t, 32);
   } else {
@@ -1273,7 +1351,9 @@ cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride,
 
 cudaError_t launch_tlq_had_quant(const void* grad, size_t grad_stride, int grad_dtype, size_t S, int M, int N,
                                  int G, int b, float cb, int bits, uint8_t* const* blocks, uint32_t remote_mask,
-                                 size_t unit_bytes, int sms, cudaStream_t st) {
+                                 size_t unit_bytes, int sr_on, uint32_t sr_key, size_t sr_off, int sms,
+                                 cudaStream_t st) {
+  const SR sr{sr_on, sr_key};
   if (N > kMaxN) return cudaErrorInvalidValue;
   const uint64_t rows = S / kRowElems;
   const uint32_t tps = (uint32_t)((rows + kTileRows - 1) / kTileRows);
@@ -1295,7 +1375,7 @@ cudaError_t launch_tlq_had_quant(const void* grad, size_t grad_stride, int grad_
     }
   }
 #define K3(IR, BT) SDP4_B_SWITCH(b, return (k3_launch<IR, BT, BB>(in_map, out, S, M, N, G, cb, unit_bytes, tps, ntiles, \
-                                                                  grid, st)))
+                                                                  grid, sr, grad_stride, sr_off, st)))
   if (in_r == 128) {
     if (bits == 4) { K3(128, 4); } else if (bits == 8) { K3(128, 8); } else { K3(128, 32); }
   } else {
@@ -1306,10 +1386,13 @@ cudaError_t launch_tlq_had_quant(const void* grad, size_t grad_stride, int grad_
 }
 
 cudaError_t launch_tlq_dq_reduce_q(const uint8_t* intra_recv, size_t in_unit_bytes, int bits_in,
-                                   int N, int M, size_t S, int G, const Dests& dst, int bits_out, int sms,
+                                   int N, int M, size_t S, int G, const Dests& dst, int bits_out, int sr_on,
+                                   uint32_t sr_key, int l_self, size_t sr_stride, size_t sr_off, int sms,
                                    cudaStream_t st) {
   if (M > kMaxDests) return cudaErrorInvalidValue;
-#define K4(BI, BO) return k4_launch<BI, BO>(intra_recv, in_unit_bytes, N, M, S, G, dst, sms, st)
+  const SR sr{sr_on, sr_key};
+#define K4(BI, BO) return k4_launch<BI, BO>(intra_recv, in_unit_bytes, N, M, S, G, dst, sr, l_self, sr_stride, sr_off, \
+                                            sms, st)
 #define K4O(BI) \
   if (bits_out == 4) { K4(BI, 4); } else if (bits_out == 8) { K4(BI, 8); } else { K4(BI, 32); }
   if (bits_in == 4) { K4O(4); } else if (bits_in == 8) { K4O(8); } else { K4O(32); }

@@ -29,8 +29,10 @@ struct Dests {
 
 // K1: Alg. 2 l.2-3 -- d = w_main - w_model (this shard), k-bit group quantization
 // into the wire unit at every destination dst.p[0..n) (n = 1: local; n = P: all-gather push).
+// sr_on: stochastic rounding (R14) with key sr_key; element e has global index idx0 + e.
 cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, int model_dtype,
-                                size_t S, int bits, int G, const Dests& dst, int sms, cudaStream_t st);
+                                size_t S, int bits, int G, const Dests& dst, int sr_on, uint32_t sr_key,
+                                uint64_t idx0, int sms, cudaStream_t st);
 
 // K2: Alg. 2 l.5 -- for every shard j < P: w_model[j*stride ..+S] += dequant(unit units.p[j])
 // (local or peer memory), in place.
@@ -41,15 +43,20 @@ cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride,
 // of S elements of each of the P shards (shard j at grad + j*grad_stride elements); shard
 // m'N + l' goes to unit m' of blocks[l'] (M units of unit_bytes; blocks[l'] is the local send
 // block or the receive block of local rank l' itself; remote_mask bit l' = peer memory).
+// Stochastic rounding: element e of shard j has global index j*grad_stride + sr_off + e.
 cudaError_t launch_tlq_had_quant(const void* grad, size_t grad_stride, int grad_dtype, size_t S, int M, int N,
                                  int G, int b, float cb, int bits, uint8_t* const* blocks, uint32_t remote_mask,
-                                 size_t unit_bytes, int sms, cudaStream_t st);
+                                 size_t unit_bytes, int sr_on, uint32_t sr_key, size_t sr_off, int sms,
+                                 cudaStream_t st);
 
 // K4: Alg. 3 l.5,7,9 -- dequantize N received units per sub-block m', fp32 reduce in
 // source order, requantize at bits_out into unit dst.p[m'] (local send unit or the
 // receive slot of node m' itself).
+// Stochastic rounding: element e of unit m' (shard m'*N + l_self) has global index
+// (m'*N + l_self)*sr_stride + sr_off + e.
 cudaError_t launch_tlq_dq_reduce_q(const uint8_t* intra_recv, size_t in_unit_bytes, int bits_in,
-                                   int N, int M, size_t S, int G, const Dests& dst, int bits_out, int sms,
+                                   int N, int M, size_t S, int G, const Dests& dst, int bits_out, int sr_on,
+                                   uint32_t sr_key, int l_self, size_t sr_stride, size_t sr_off, int sms,
                                    cudaStream_t st);
 
 // K5: Alg. 3 l.11-13 -- dequantize M received units, fp32 reduce in source order,

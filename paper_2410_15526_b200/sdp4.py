@@ -48,8 +48,8 @@ SIGNATURES = {
     "sdp4_qwd_allgather_apply": (_ci, [_vp, _vp, _c_size, _c_size, _ci, _ci, _vp, _ci, _vp]),
     "sdp4_tlq_hs_reduce_scatter": (_ci, [_vp, _vp, _ci, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _u64, _vp, _vp,
                                          _c_size, _vp]),
-    "sdp4_tlq_stage_quantize": (_ci, [_vp, _ci, _c_size, _ci, _ci, _ci, _ci, _ci, _vp, _vp]),
-    "sdp4_tlq_stage_reduce": (_ci, [_vp, _c_size, _ci, _ci, _ci, _ci, _ci, _vp, _vp]),
+    "sdp4_tlq_stage_quantize": (_ci, [_vp, _ci, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _u64, _ci, _vp, _vp]),
+    "sdp4_tlq_stage_reduce": (_ci, [_vp, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _u64, _ci, _vp, _vp]),
     "sdp4_tlq_stage_final": (_ci, [_vp, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _vp, _vp]),
     "sdp4_launch_count": (_u64, [_vp, _ci]),
     "sdp4_profile_enable": (_ci, [_vp, _ci]),
@@ -119,17 +119,21 @@ def tlq_workspace_offset(M, N, numel, bits_intra, bits_inter, group, region) -> 
 
 
 def tlq_stage_quantize(grad: torch.Tensor, intra_send: torch.Tensor, M: int, N: int, bits_intra: int = 8,
-                       group: int = 128, hadamard_block: int = 64, stream=None):
-    """K3 alone (Alg. 3 l.2-3) on one rank's gradient, no communication."""
+                       group: int = 128, hadamard_block: int = 64, seed=None, rank: int = 0, stream=None):
+    """K3 alone (Alg. 3 l.2-3) on rank `rank`'s gradient, no communication.  seed: stochastic
+    rounding (R14) with that seed; None: round to nearest even."""
     _check(lib().sdp4_tlq_stage_quantize(_ptr(grad), _DT[grad.dtype], grad.numel(), M, N, bits_intra, group,
-                                         hadamard_block, _ptr(intra_send), _stream(stream)))
+                                         hadamard_block, RNE if seed is None else STOCHASTIC, seed or 0, rank,
+                                         _ptr(intra_send), _stream(stream)))
 
 
 def tlq_stage_reduce(intra_recv: torch.Tensor, inter_send: torch.Tensor, numel: int, M: int, N: int,
-                     bits_intra: int = 8, bits_inter: int = 4, group: int = 128, stream=None):
-    """K4 alone (Alg. 3 l.5, 7, 9) for one rank, no communication."""
+                     bits_intra: int = 8, bits_inter: int = 4, group: int = 128, seed=None, rank: int = 0,
+                     stream=None):
+    """K4 alone (Alg. 3 l.5, 7, 9) for rank `rank`, no communication."""
     _check(lib().sdp4_tlq_stage_reduce(_ptr(intra_recv), numel, M, N, bits_intra, bits_inter, group,
-                                       _ptr(inter_send), _stream(stream)))
+                                       RNE if seed is None else STOCHASTIC, seed or 0, rank, _ptr(inter_send),
+                                       _stream(stream)))
 
 
 def tlq_stage_final(inter_recv: torch.Tensor, out_shard: torch.Tensor, numel: int, M: int, N: int,
@@ -218,12 +222,13 @@ class Comm:
 
     # -- qWD (Alg. 2 l.2-5) ----------------------------------------------------------
     def qwd_quantize(self, w_main_shard: torch.Tensor, w_model: torch.Tensor, workspace: torch.Tensor,
-                     bits: int = 4, group: int = 128, stream=None):
+                     bits: int = 4, group: int = 128, seed=None, stream=None):
+        """seed: stochastic rounding (R14) with this seed; None: round to nearest even."""
         if w_main_shard.dtype != torch.float32:
             raise TypeError("w_main_shard must be fp32 (P:211)")
         _check(lib().sdp4_qwd_quantize(self._h, _ptr(w_main_shard), _ptr(w_model), _DT[w_model.dtype],
-                                       w_model.numel(), bits, group, RNE, 0, _ptr(workspace), workspace.numel(),
-                                       _stream(stream)))
+                                       w_model.numel(), bits, group, RNE if seed is None else STOCHASTIC,
+                                       seed or 0, _ptr(workspace), workspace.numel(), _stream(stream)))
 
     def qwd_allgather_apply(self, workspace: torch.Tensor, w_model: torch.Tensor, bits: int = 4,
                             group: int = 128, stream=None):
@@ -233,11 +238,13 @@ class Comm:
     # -- TLq-HS (Alg. 3) -------------------------------------------------------------
     def tlq_hs_reduce_scatter(self, grad: torch.Tensor, out_shard: torch.Tensor, workspace: torch.Tensor,
                               bits_intra: int = 8, bits_inter: int = 4, group: int = 128,
-                              hadamard_block: int = 64, average: bool = True, stream=None):
+                              hadamard_block: int = 64, average: bool = True, seed=None, stream=None):
+        """seed: stochastic rounding (R14) of both quantizers with this seed; None: nearest even."""
         if out_shard.dtype != torch.float32:
             raise TypeError("out_shard must be fp32")
         _check(lib().sdp4_tlq_hs_reduce_scatter(self._h, _ptr(grad), _DT[grad.dtype], grad.numel(), bits_intra,
-                                                bits_inter, group, hadamard_block, int(bool(average)), RNE, 0,
+                                                bits_inter, group, hadamard_block, int(bool(average)),
+                                                RNE if seed is None else STOCHASTIC, seed or 0,
                                                 _ptr(out_shard), _ptr(workspace), workspace.numel(),
                                                 _stream(stream)))
 

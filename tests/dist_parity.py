@@ -52,15 +52,16 @@ def main():
         sys.exit(0 if ok else 1)
     runs = []
     for tr in a.transports.split(","):
-        runs += [(tr, ch) for ch in ([int(x) for x in a.chunks.split(",")] if tr == "nccl" else [0])]
-    for tr, chunks in runs:
+        runs += [(tr, ch, None) for ch in ([int(x) for x in a.chunks.split(",")] if tr == "nccl" else [0])]
+        runs.append((tr, 3 if tr == "nccl" else 0, 2 ** 34 + 2410))     # stochastic rounding (R14)
+    for tr, chunks, seed in runs:
         comm.set_transport(tr)
         comm.set_chunks(chunks)
         for S in (16384 * 2 + 64 * 5 * max(1, G // 64), 16384 * 12 + 640):
             S -= S % max(G, 64)
-            ok_c, m_c = run_checks(comm, rank, P, M, N, G, b, S)
+            ok_c, m_c = run_checks(comm, rank, P, M, N, G, b, S, seed)
             ok &= ok_c
-            msgs += [f"{tr} chunks={chunks} S={S} ({comm.chunks(P * S, G)} used): {m}" for m in m_c]
+            msgs += [f"{tr} chunks={chunks} seed={seed} S={S} ({comm.chunks(P * S, G)} used): {m}" for m in m_c]
     comm.close()
     print(f"rank {rank}/{world} ({M}x{N}) {'PASS' if ok else 'FAIL'} runs={runs} {'; '.join(msgs)}", flush=True)
     dist.barrier()
@@ -121,7 +122,7 @@ def run_full(comm, rank, P, M, N, G=128, b=64, win=16384, nwin=6):
     return ok, msgs
 
 
-def run_checks(comm, rank, P, M, N, G, b, S):
+def run_checks(comm, rank, P, M, N, G, b, S, seed=None):
     D = P * S
     ok = True
     msgs = []
@@ -131,10 +132,10 @@ def run_checks(comm, rank, P, M, N, G, b, S):
     mains = [synth.main_weights(w_model[r * S:(r + 1) * S], seed=synth.seed_for(r, 2)) for r in range(P)]
     ws = torch.zeros(comm.qwd_workspace_bytes(D, 4, G), dtype=torch.uint8, device="cuda")
     wm = w_model.cuda()
-    comm.qwd_quantize(mains[rank].cuda(), wm, ws, 4, G)
+    comm.qwd_quantize(mains[rank].cuda(), wm, ws, 4, G, seed=seed)
     comm.qwd_allgather_apply(ws, wm, 4, G)
     torch.cuda.synchronize()
-    _, want = oracle.qwd_step([m.numpy() for m in mains], synth.bf16_bits(w_model), 4, G, model_bf16=True)
+    _, want = oracle.qwd_step([m.numpy() for m in mains], synth.bf16_bits(w_model), 4, G, model_bf16=True, seed=seed)
     got = synth.bf16_bits(wm.cpu())
     if not np.array_equal(got, want):
         ok = False
@@ -152,9 +153,10 @@ def run_checks(comm, rank, P, M, N, G, b, S):
         grads = [synth.gradient(D, seed=synth.seed_for(r, 3), dtype=dtype) for r in range(P)]
         tws = torch.zeros(comm.tlq_workspace_bytes(D, 8, 4, G), dtype=torch.uint8, device="cuda")
         out = torch.empty(S, dtype=torch.float32, device="cuda")
-        comm.tlq_hs_reduce_scatter(grads[rank].cuda(), out, tws, 8, 4, G, b, True)
+        comm.tlq_hs_reduce_scatter(grads[rank].cuda(), out, tws, 8, 4, G, b, True, seed=seed)
         torch.cuda.synchronize()
-        tr = oracle.tlq_hs_reduce_scatter([g.float().numpy() for g in grads], oracle.Topology(M, N), G, b, 8, 4, True)
+        tr = oracle.tlq_hs_reduce_scatter([g.float().numpy() for g in grads], oracle.Topology(M, N), G, b, 8, 4, True,
+                                          seed=seed)
         o = out.cpu().numpy()
         w = tr.out[rank]
         same = (o.view(np.uint32) == w.view(np.uint32)) | (np.isnan(o) & np.isnan(w))

@@ -65,8 +65,8 @@ def test_validation_errors_before_any_launch():
     assert st == sdp4.EINVAL and b"grad" in L.sdp4_last_error()
     st = L.sdp4_tlq_hs_reduce_scatter(c._h, None, 0, 4096, 5, 4, 128, 64, 1, 0, 0, None, None, 0, None)
     assert st == sdp4.EINVAL
-    st = L.sdp4_qwd_quantize(c._h, None, None, 1, 4096, 4, 128, 1, 0, None, 0, None)
-    assert st == sdp4.EINVAL                      # stochastic rounding not implemented
+    st = L.sdp4_qwd_quantize(c._h, None, None, 1, 4096, 4, 128, 7, 0, None, 0, None)
+    assert st == sdp4.EINVAL and b"rounding" in L.sdp4_last_error()   # unknown rounding mode
     bad = ctypes.c_void_p()
     assert L.sdp4_comm_init(ctypes.byref(bad), None, 0, 8, 3, 3, 0) == sdp4.EINVAL
     assert L.sdp4_comm_set_chunks(c._h, 17) == sdp4.EINVAL

@@ -16,7 +16,7 @@ from tests.test_gpu_parity import assert_unit_equal, f32_equal
 pytestmark = pytest.mark.gpu
 
 
-def emulate(grads, M, N, bi, be, G, b, average=True):
+def emulate(grads, M, N, bi, be, G, b, average=True, seed=None):
     P = M * N
     D = grads[0].numel()
     S = D // P
@@ -25,14 +25,14 @@ def emulate(grads, M, N, bi, be, G, b, average=True):
     intra_send = []
     for r in range(P):
         buf = torch.zeros(N * M * w8, dtype=torch.uint8, device=dev)
-        tlq_stage_quantize(grads[r].to(dev), buf, M, N, bi, G, b)
+        tlq_stage_quantize(grads[r].to(dev), buf, M, N, bi, G, b, seed=seed, rank=r)
         intra_send.append(buf)
     inter_send = []
     for r in range(P):
         m, l = divmod(r, N)
         recv = torch.cat([intra_send[m * N + lpp][l * M * w8:(l + 1) * M * w8] for lpp in range(N)])
         buf = torch.zeros(M * w4, dtype=torch.uint8, device=dev)
-        tlq_stage_reduce(recv, buf, D, M, N, bi, be, G)
+        tlq_stage_reduce(recv, buf, D, M, N, bi, be, G, seed=seed, rank=r)
         inter_send.append(buf)
     outs = []
     for r in range(P):
@@ -46,31 +46,34 @@ def emulate(grads, M, N, bi, be, G, b, average=True):
             [x.cpu().numpy() for x in outs], w8, w4, S)
 
 
-CASES = [  # (M, N, bits_intra, bits_inter, G, b, dtype)
-    (2, 4, 8, 4, 128, 64, torch.bfloat16),
-    (4, 2, 8, 4, 128, 64, torch.bfloat16),
-    (2, 4, 8, 4, 128, 32, torch.float32),
-    (1, 8, 8, 4, 128, 64, torch.bfloat16),
-    (8, 1, 8, 4, 128, 64, torch.bfloat16),
-    (2, 2, 4, 4, 128, 0, torch.float32),      # ULq
-    (3, 2, 8, 4, 64, 16, torch.float32),      # P = 6: kappa = rn(c_b / 6)
-    (2, 4, 8, 4, 256, 256, torch.bfloat16),   # cross-lane Hadamard stages
-    (2, 2, 8, 4, 32, 32, torch.bfloat16),     # two groups per row
-    (2, 2, 32, 32, 128, 64, torch.float32),   # identity codec (R12)
-    (4, 2, 8, 8, 2048, 128, torch.bfloat16),  # large groups (cross-warp K4 group max)
+CASES = [  # (M, N, bits_intra, bits_inter, G, b, dtype, seed)
+    (2, 4, 8, 4, 128, 64, torch.bfloat16, None),
+    (4, 2, 8, 4, 128, 64, torch.bfloat16, None),
+    (2, 4, 8, 4, 128, 32, torch.float32, None),
+    (1, 8, 8, 4, 128, 64, torch.bfloat16, None),
+    (8, 1, 8, 4, 128, 64, torch.bfloat16, None),
+    (2, 2, 4, 4, 128, 0, torch.float32, None),      # ULq
+    (3, 2, 8, 4, 64, 16, torch.float32, None),      # P = 6: kappa = rn(c_b / 6)
+    (2, 4, 8, 4, 256, 256, torch.bfloat16, None),   # cross-lane Hadamard stages
+    (2, 2, 8, 4, 32, 32, torch.bfloat16, None),     # two groups per row
+    (2, 2, 32, 32, 128, 64, torch.float32, None),   # identity codec (R12)
+    (4, 2, 8, 8, 2048, 128, torch.bfloat16, None),  # large groups (cross-warp K4 group max)
+    (2, 4, 8, 4, 128, 64, torch.bfloat16, 2410),    # stochastic rounding (R14): per-rank keys
+    (4, 2, 4, 4, 32, 0, torch.float32, 2 ** 36 + 1),
 ]
 
 
-@pytest.mark.parametrize("M,N,bi,be,G,b,dtype", CASES)
-def test_tlq_multirank_emulated(M, N, bi, be, G, b, dtype):
+@pytest.mark.parametrize("M,N,bi,be,G,b,dtype,seed", CASES)
+def test_tlq_multirank_emulated(M, N, bi, be, G, b, dtype, seed):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     P = M * N
     align = P * max(G, 64)
     D = ((16384 * P * 2 + 64 * 37 * P) // align + 1) * align     # > 2 tiles per shard + ragged tail
     grads = [synth.gradient(D, seed=synth.seed_for(r, 3), dtype=dtype) for r in range(P)]
-    intra, inter, outs, w8, w4, S = emulate(grads, M, N, bi, be, G, b)
-    tr = oracle.tlq_hs_reduce_scatter([g.float().numpy() for g in grads], oracle.Topology(M, N), G, b, bi, be, True)
+    intra, inter, outs, w8, w4, S = emulate(grads, M, N, bi, be, G, b, seed=seed)
+    tr = oracle.tlq_hs_reduce_scatter([g.float().numpy() for g in grads], oracle.Topology(M, N), G, b, bi, be, True,
+                                      seed=seed)
     for r in range(P):
         for lp in range(N):
             for mp in range(M):

@@ -53,11 +53,11 @@ def bf16_equal(a_bits, b_bits):
 
 
 # --------------------------------------------------------------------------------- qWD
-def run_qwd(comm, w_main, w_model, bits, G):
+def run_qwd(comm, w_main, w_model, bits, G, seed=None):
     D = w_model.numel()
     ws = torch.zeros(comm.qwd_workspace_bytes(D, bits, G), dtype=torch.uint8, device="cuda")
     wm = w_model.cuda()
-    comm.qwd_quantize(w_main.cuda(), wm, ws, bits, G)
+    comm.qwd_quantize(w_main.cuda(), wm, ws, bits, G, seed=seed)
     torch.cuda.synchronize()
     unit = ws.cpu().numpy().copy()
     comm.qwd_allgather_apply(ws, wm, bits, G)
@@ -65,10 +65,10 @@ def run_qwd(comm, w_main, w_model, bits, G):
     return unit, wm.cpu()
 
 
-def oracle_qwd(w_main, w_model, bits, G):
+def oracle_qwd(w_main, w_model, bits, G, seed=None):
     bf = w_model.dtype == torch.bfloat16
     wm = synth.bf16_bits(w_model) if bf else w_model.numpy()
-    units, new = oracle.qwd_step([w_main.numpy()], wm, bits, G, model_bf16=bf)
+    units, new = oracle.qwd_step([w_main.numpy()], wm, bits, G, model_bf16=bf, seed=seed)
     return units[0], new
 
 
@@ -101,12 +101,12 @@ def test_qwd_edge_cases(comm, G):
 
 
 # ------------------------------------------------------------------------------ TLq-HS
-def run_tlq(comm, grad, bits_intra, bits_inter, G, b, average=True):
+def run_tlq(comm, grad, bits_intra, bits_inter, G, b, average=True, seed=None):
     D = grad.numel()
     nbytes = comm.tlq_workspace_bytes(D, bits_intra, bits_inter, G)
     ws = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
     out = torch.empty(D, dtype=torch.float32, device="cuda")
-    comm.tlq_hs_reduce_scatter(grad.cuda(), out, ws, bits_intra, bits_inter, G, b, average)
+    comm.tlq_hs_reduce_scatter(grad.cuda(), out, ws, bits_intra, bits_inter, G, b, average, seed=seed)
     torch.cuda.synchronize()
     from paper_2410_15526_b200 import tlq_workspace_offset
     w = ws.cpu().numpy()
@@ -114,15 +114,15 @@ def run_tlq(comm, grad, bits_intra, bits_inter, G, b, average=True):
     return w[:o_inter].copy(), w[o_inter:].copy(), out.cpu().numpy()
 
 
-def oracle_tlq(grad, bits_intra, bits_inter, G, b, average=True):
+def oracle_tlq(grad, bits_intra, bits_inter, G, b, average=True, seed=None):
     g = grad.float().numpy()
-    return oracle.tlq_hs_reduce_scatter([g], oracle.Topology(1, 1), G, b, bits_intra, bits_inter, average)
+    return oracle.tlq_hs_reduce_scatter([g], oracle.Topology(1, 1), G, b, bits_intra, bits_inter, average, seed=seed)
 
 
-def check_tlq(comm, grad, bi, be, G, b, average=True):
+def check_tlq(comm, grad, bi, be, G, b, average=True, seed=None):
     D = grad.numel()
-    intra, inter, out = run_tlq(comm, grad, bi, be, G, b, average)
-    tr = oracle_tlq(grad, bi, be, G, b, average)
+    intra, inter, out = run_tlq(comm, grad, bi, be, G, b, average, seed)
+    tr = oracle_tlq(grad, bi, be, G, b, average, seed)
     c8, s8 = tr.intra_send[0][0][0]
     assert_unit_equal(intra, c8, s8, bi, G, D, f"K3 intra unit (b={b}, G={G}, k={bi})")
     c4, s4 = tr.inter_send[0][0]
@@ -190,3 +190,26 @@ def test_errors_raise(comm):
     with pytest.raises(SDP4Error):   # host pointer rejected before any launch
         comm.tlq_hs_reduce_scatter(torch.zeros(16384), torch.empty(16384, device="cuda"),
                                    torch.empty(10**6, dtype=torch.uint8, device="cuda"))
+
+
+# --------------------------------------------------------------- stochastic rounding (R14)
+@pytest.mark.parametrize("bits,G", [(4, 128), (8, 32), (4, 2048)])
+@pytest.mark.parametrize("seed", [1, 2 ** 40 + 17])
+def test_qwd_stochastic_parity(comm, bits, G, seed):
+    D = max(G, 64) * 29
+    w_model = synth.model_weights(D, seed=11, dtype=torch.bfloat16)
+    w_main = synth.main_weights(w_model, seed=12)
+    unit, new = run_qwd(comm, w_main, w_model, bits, G, seed)
+    (codes, scales), want_new = oracle_qwd(w_main, w_model, bits, G, seed)
+    assert_unit_equal(unit, codes, scales, bits, G, D, "qWD stochastic unit")
+    assert bf16_equal(synth.bf16_bits(new), want_new)
+    unit2, _ = run_qwd(comm, w_main, w_model, bits, G, seed + 1)
+    assert not np.array_equal(unit2, unit)                  # a new seed draws new codes
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("G,b,bi,be", [(128, 64, 8, 4), (32, 32, 8, 4), (256, 0, 4, 4), (128, 128, 8, 8)])
+def test_tlq_stochastic_parity(comm, dtype, G, b, bi, be):
+    D = 16384 * 2 + max(G, 64) * 7
+    grad = synth.gradient(D, seed=31 + G, dtype=dtype)
+    check_tlq(comm, grad, bi, be, G, b, True, seed=2 ** 35 + G)

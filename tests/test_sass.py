@@ -31,7 +31,7 @@ def functions(sass):
         if m:
             name = m.group(1)
             out[name] = []
-        elif name and re.match(r"\s+/\*[0-9a-f]{4}\*/", line):
+        elif name and re.match(r"\s+/\*[0-9a-f]{4,}\*/", line):
             out[name].append(line)
     return out
 
