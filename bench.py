@@ -131,6 +131,27 @@ def kernel_bytes(name, D, S, P, M, N, a):
     return None
 
 
+NVLINK_PEAK_GBS = 770.0  # B200_PROFILING.md: measured peer copy, per direction per GPU (900 nominal)
+
+
+def kernel_nvlink_bytes(name, D, S, P, M, N, a, transport):
+    """Bytes a fused kernel moves over NVLink per launch (P2P transport; the larger of this
+    rank's egress and ingress): K2 pulls the P-1 peer units of the qWD all-gather, K3 pushes
+    the N-1 peer blocks of the intra all-to-all, K4 the M-1 peer units of the inter one."""
+    if transport != "p2p" or P == 1:
+        return 0
+
+    def wire(n, k, G):
+        return n * k / 8 + (4 * n / G if k != 32 else 0)
+    if name.startswith("K2"):
+        return (P - 1) * wire(S, a.bits_w, a.qwd_group)
+    if name.startswith("K3"):
+        return (N - 1) * M * wire(S, a.bits_intra, a.group)
+    if name.startswith("K4"):
+        return (M - 1) * wire(S, a.bits_inter, a.group)
+    return 0
+
+
 def ncu_traffic(kernel, workload):
     """dram read+write bytes per launch from the committed ncu summary, if it matches."""
     try:
@@ -285,13 +306,18 @@ def run_sdp4(a, rank, world, local_rank):
                f"bits={a.bits_w}/{a.bits_intra}/{a.bits_inter} grad={a.grad_dtype} model={a.model_dtype}"
     peak, peak_src = peaks()
     kern = {}
+    transport = comm.transport if world > 1 else "local"
     for name, (tms, cnt) in prof.items():
         if name.startswith("nccl_"):
             continue
         kb = kernel_bytes(name, D, S, P, M, N, a)
+        nb = kernel_nvlink_bytes(name, D, S, P, M, N, a, transport)
         avg = tms / max(cnt, 1)
         kern[name] = {"avg_ms": round(avg, 4), "launches": cnt, "share": None,
                       "alg_bytes": kb, "gbs": round(kb / (avg * 1e-3) / 1e9, 1) if kb and avg > 0 else None}
+        if nb:
+            kern[name]["nvlink_bytes"] = nb
+            kern[name]["nvlink_gbs"] = round(nb / (avg * 1e-3) / 1e9, 1)
     comm_ops = {n: {"ms_per_step": round(t / a.steps, 4), "calls": c} for n, (t, c) in prof.items()
                 if n.startswith("nccl_")}
     tot = sum(v["avg_ms"] * v["launches"] for v in kern.values()) or 1.0
@@ -306,6 +332,14 @@ def run_sdp4(a, rank, world, local_rank):
         roofline = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                     "frac": round(ach / peak, 4) if ach else None, "traffic": tr,
                     "alg_bytes_per_launch": kern[dom]["alg_bytes"], "peak_source": peak_src}
+        nv = kern[dom].get("nvlink_gbs")
+        if nv and nv / NVLINK_PEAK_GBS > (ach or 0) / peak:
+            # the fused kernel is bound by its NVLink traffic, not by HBM
+            roofline.update({"bound": "nvlink", "achieved": nv, "peak": NVLINK_PEAK_GBS,
+                             "frac": round(nv / NVLINK_PEAK_GBS, 4), "traffic": None,
+                             "alg_bytes_per_launch": kern[dom]["nvlink_bytes"],
+                             "hbm_frac": round(ach / peak, 4) if ach else None,
+                             "peak_source": "B200_PROFILING.md measured peer copy per direction (fallback)"})
 
     # unquantized NCCL comparators on the same buffers (sec. 2.1), N > 1 only
     comparators = None
