@@ -31,7 +31,8 @@ __all__ = [
     "F32", "TINY", "q_levels", "bf16_widen", "bf16_round", "hadamard_c",
     "group_scales", "quantize", "dequantize", "fwht_unnormalized", "hadamard_normalized",
     "pack_codes", "unpack_codes", "wire_unit_bytes", "wire_unit", "wire_unit_decode",
-    "Topology", "qwd_quantize", "qwd_allgather_apply", "qwd_step",
+    "Topology", "qwd_quantize", "qwd_allgather_apply", "qwd_step", "qw_quantize", "qw_allgather_apply", "qw_step",
+    "ring_reduce_scatter", "RingTrace",
     "TlqTrace", "tlq_hs_reduce_scatter", "naive_tlq_hs_reduce_scatter", "mix32", "sr_key", "sr_uniform",
     "STAGE_QWD", "STAGE_INTRA", "STAGE_INTER",
     "exact_reduce_scatter_f64", "comm_bits_per_param",
@@ -207,7 +208,9 @@ def hadamard_normalized(x: np.ndarray, b: int) -> np.ndarray:
 # Wire format (R4, R15): one "wire unit" per (shard, bit-width):
 #   [codes: n*k/8 bytes][scales: n/G fp32 little-endian] padded to 256 bytes.
 #   int8 codes are two's complement; int4 codes are two's-complement nibbles,
-#   element 2j in the low nibble.  k = 32: n fp32 values, no scales.
+#   element 2j in the low nibble; int2 codes (the ternary codec of
+#   Counterexample 1, weights only) are two's-complement bit pairs, element
+#   4j+i in bits 2i..2i+1 (R4).  k = 32: n fp32 values, no scales.
 # --------------------------------------------------------------------------
 def pack_codes(codes: np.ndarray, k: int) -> np.ndarray:
     c = np.asarray(codes, dtype=np.int64)
@@ -216,6 +219,10 @@ def pack_codes(codes: np.ndarray, k: int) -> np.ndarray:
     if k == 4:
         nib = (c & 0xF).astype(np.uint8).reshape(-1, 2)
         return (nib[:, 0] | (nib[:, 1] << np.uint8(4))).astype(np.uint8)
+    if k == 2:
+        two = (c & 0x3).astype(np.uint8).reshape(-1, 4)
+        return (two[:, 0] | (two[:, 1] << np.uint8(2)) | (two[:, 2] << np.uint8(4))
+                | (two[:, 3] << np.uint8(6))).astype(np.uint8)
     raise ValueError(f"pack_codes: unsupported k={k}")
 
 
@@ -228,6 +235,10 @@ def unpack_codes(packed: np.ndarray, k: int, n: int) -> np.ndarray:
         hi = (p >> 4).astype(np.int32)
         out = np.stack([lo, hi], axis=1).reshape(-1)[:n]
         return np.where(out >= 8, out - 16, out).astype(np.int32)
+    if k == 2:
+        out = np.stack([(p >> np.uint8(2 * i)) & np.uint8(3) for i in range(4)], axis=1).astype(np.int32)
+        out = out.reshape(-1)[:n]
+        return np.where(out >= 2, out - 4, out).astype(np.int32)
     raise ValueError(f"unpack_codes: unsupported k={k}")
 
 
@@ -331,6 +342,35 @@ def qwd_step(w_main_shards, w_model, k: int, G: int, model_bf16: bool, seed=None
         c, s, _ = qwd_quantize(shard, wm[p * S:(p + 1) * S], k, G, sr)
         units.append((c, s))
     return units, qwd_allgather_apply(units, wm, k, G, model_bf16)
+
+
+# --------------------------------------------------------------------------
+# qW: direct weight quantization, the comparison codec of QSDP / ZeRO++ (Alg. 1,
+# "Quantize weights", "AllGather"; sec. 3.1 P:330-336 and Counterexample 1
+# P:412-416 contrast it with qWD).  Ablation baseline, same wire unit.
+# --------------------------------------------------------------------------
+def qw_quantize(w_main_shard: np.ndarray, k: int, G: int, sr=None):
+    """Alg. 1 "Quantize weights" on worker p: codes/scales of w_main[p] itself (no difference)."""
+    return quantize(np.asarray(w_main_shard, dtype=F32), k, G, sr=sr)
+
+
+def qw_allgather_apply(units, k: int, G: int, model_bf16: bool):
+    """Alg. 1 "AllGather" + dequantize: the replica BECOMES the gathered dequantized weights
+    (w_model <- concat_j Dequantize(unit_j)), stored bf16 (RNE) or fp32 -- no accumulation,
+    which is why a biased codec can stall (Counterexample 1)."""
+    w = np.concatenate([dequantize(c, s, k, G) for (c, s) in units]).astype(F32)
+    return bf16_round(w) if model_bf16 else w
+
+
+def qw_step(w_main_shards, k: int, G: int, model_bf16: bool, seed=None):
+    """One qW iteration over all P simulated workers.  seed: stochastic rounding with the
+    qWD stage key (R14), element index = the global index p*S + j."""
+    S = len(w_main_shards[0])
+    units = []
+    for p, shard in enumerate(w_main_shards):
+        sr = None if seed is None else (p * S, sr_key(seed, STAGE_QWD, p))
+        units.append(qw_quantize(shard, k, G, sr))
+    return units, qw_allgather_apply(units, k, G, model_bf16)
 
 
 # --------------------------------------------------------------------------
@@ -463,6 +503,42 @@ def naive_tlq_hs_reduce_scatter(grads, topo: Topology, G: int, b: int,
             acc = (acc / F32(P)).astype(F32)
         outs.append(acc)
     return outs
+
+
+@dataclass
+class RingTrace:
+    """Messages of one ring reduce-scatter: send[t][r] = (codes, scales) rank r sends to rank
+    (r+1) mod P at hop t (t = 0..P-2), carrying chunk (r - t - 1) mod P; out[r]: shard r."""
+    send: list = field(default_factory=list)
+    out: list = field(default_factory=list)
+
+
+def ring_reduce_scatter(grads, k: int, G: int, average: bool = True) -> RingTrace:
+    """Ring reduce-scatter with per-hop quantization, the baseline of sec. 2.3 ("P-1
+    rounds, during which each GPU sends local data and aggregates the received data. When
+    quantization is applied, this necessitates P-1 rounds of quantization and
+    dequantization").  Ablation baseline, nearest rounding.
+
+    Chunk c (= shard c, ending on rank c) starts on rank c+1: acc = g_{c+1}[c].  Hop h =
+    1..P-1: rank (c+h) mod P sends Quantize(acc) (k bits, group G); rank (c+h+1) mod P sets
+    acc = rn(Dequantize(msg) + g_own[c]) (fp32).  Finally out_c = rn(acc * rn(1/P)) when
+    averaging (as R8).  k = 32 is the identity codec (R12)."""
+    P = len(grads)
+    D = len(grads[0])
+    S = D // P
+    g = [np.asarray(x, dtype=F32) for x in grads]
+    tr = RingTrace(send=[[None] * P for _ in range(max(P - 1, 0))], out=[None] * P)
+    for c in range(P):
+        acc = g[(c + 1) % P][c * S:(c + 1) * S].copy()
+        for h in range(1, P):
+            sender, recv = (c + h) % P, (c + h + 1) % P
+            codes, scales = quantize(acc, k, G)
+            tr.send[h - 1][sender] = (codes, scales)
+            acc = (dequantize(codes, scales, k, G) + g[recv][c * S:(c + 1) * S]).astype(F32)
+        if average:
+            acc = (acc * F32(F32(1.0) / F32(P))).astype(F32)
+        tr.out[c] = acc
+    return tr
 
 
 def exact_reduce_scatter_f64(grads, P: int, average: bool = True):
