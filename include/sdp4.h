@@ -147,7 +147,8 @@ size_t sdp4_tlq_workspace_offset(int groups_M, int group_size_N, size_t numel, i
  *           (R2, R3), written as wire unit r of `workspace` (layout above).
  * w_main_shard: fp32[S] (this rank's main weights).  w_model_full: the
  * full replica D elements of model_dtype (bf16 or fp32); only
- * [r*S, (r+1)*S) is read.  bits in {4, 8, 32}; G power of two in [32, 2048].
+ * [r*S, (r+1)*S) is read.  bits in {2, 4, 8, 32} (2 = the ternary codec of
+ * Counterexample 1, int2 packing R4); G power of two in [32, 2048].
  * rnd / seed: rounding of the codes (see sdp4_round). */
 sdp4_status sdp4_qwd_quantize(sdp4_comm_t comm, const float* w_main_shard, const void* w_model_full,
                               sdp4_dtype model_dtype, size_t numel, int bits, int group,
@@ -162,6 +163,40 @@ sdp4_status sdp4_qwd_quantize(sdp4_comm_t comm, const float* w_main_shard, const
 sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t comm, void* workspace, size_t workspace_bytes,
                                      size_t numel, int bits, int group, void* w_model_full,
                                      sdp4_dtype model_dtype, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Ablation baselines: the codecs SDP4Bit is compared against.
+ * ------------------------------------------------------------------------- */
+
+/* qW -- direct weight quantization of QSDP / ZeRO++ (Alg. 1 P:231-233 "Quantize weights",
+ * "AllGather"; contrasted with qWD in sec. 3.1 P:330-336 and Counterexample 1 P:412-416).
+ * Same workspace, wire unit, symmetric buffers and rounding as sdp4_qwd_quantize, but the
+ * codes are those of w_main[r] itself:  codes = RNE(w_main * rn(q_k/s)), s = max|w_main| per
+ * group.  No replica is read.  Errors as sdp4_qwd_quantize. */
+sdp4_status sdp4_qw_quantize(sdp4_comm_t comm, const float* w_main_shard, size_t numel, int bits, int group,
+                             sdp4_round rnd, uint64_t seed, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
+/* qW AllGather + dequantize: for all D elements  w_model <- dtype_rn(code * rn(s / q_k))
+ * (assignment, not accumulation: the replica becomes the gathered quantized weights, which
+ * is why a biased codec can stall).  w_model_full is only written. */
+sdp4_status sdp4_qw_allgather_apply(sdp4_comm_t comm, void* workspace, size_t workspace_bytes, size_t numel,
+                                    int bits, int group, void* w_model_full, sdp4_dtype model_dtype,
+                                    void* stream);
+
+/* Ring reduce-scatter with per-hop quantization (sec. 2.3: "P-1 rounds of
+ * quantization and dequantization, potentially leading to error propagation").  Chunk c
+ * (= shard c, ends on rank c) starts on rank c+1: acc = g_{c+1}[c]; at hop h = 1..P-1 rank
+ * (c+h) mod P sends Quantize(acc) (bits, group G, nearest, R3) and rank (c+h+1) mod P sets
+ * acc = rn(Dequantize(msg) + g_own[c]) in fp32; out_shard = rn(acc * rn(1/P)) if average
+ * else acc.  grad: D elements of grad_dtype; out_shard: fp32[S].  bits in {4, 8, 32}.
+ * Transport as configured: P2P pushes each hop into the next rank's library-owned slot over
+ * NVLink (one flag per hop); NCCL uses ncclSend/ncclRecv on `stream` with `workspace` as
+ * the send and receive units.  workspace_bytes >= sdp4_ring_workspace_bytes (2 units). */
+size_t sdp4_ring_workspace_bytes(int world, size_t numel, int bits, int group);
+sdp4_status sdp4_ring_reduce_scatter(sdp4_comm_t comm, const void* grad, sdp4_dtype grad_dtype, size_t numel,
+                                     int bits, int group, int average, float* out_shard, void* workspace,
+                                     size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * TLq-HS -- two-level gradient quantization with Hadamard smoother, replacing the

@@ -62,6 +62,7 @@ bool is_pow2(long long x) { return x > 0 && (x & (x - 1)) == 0; }
 size_t round_up(size_t a, size_t m) { return (a + m - 1) / m * m; }
 
 bool valid_bits(int bits) { return bits == 4 || bits == 8 || bits == 32; }
+bool valid_wbits(int bits) { return bits == 2 || valid_bits(bits); }  // weight codecs add int2 (R4)
 
 // Wire unit (R15): [codes n*k/8][fp32 scales n/G] padded to 256 bytes; k = 32: n fp32.
 size_t unit_bytes(size_t n, int bits, int group) {
@@ -131,8 +132,8 @@ enum Transport { kTransportNccl = 0, kTransportP2P = 1 };
 struct sdp4_comm {
   int rank = 0, world = 1, M = 1, N = 1, m = 0, l = 0;
   int transport = kTransportNccl;
-  SymBuf sym_qwd, sym_tlq;
-  uint32_t epoch_qwd = 0, epoch_tlq = 0;
+  SymBuf sym_qwd, sym_tlq, sym_ring;
+  uint32_t epoch_qwd = 0, epoch_tlq = 0, epoch_ring = 0;
   PFN_cuStreamWriteValue32_v11070 write_value = nullptr;
   PFN_cuStreamWaitValue32_v11070 wait_value = nullptr;
   int device = 0;
@@ -480,7 +481,7 @@ sdp4_status sdp4_comm_destroy(sdp4_comm_t c) {
   }
   for (auto e : c->pool) cudaEventDestroy(e);
   for (auto e : c->deps) cudaEventDestroy(e);
-  for (SymBuf* b : {&c->sym_qwd, &c->sym_tlq}) {
+  for (SymBuf* b : {&c->sym_qwd, &c->sym_tlq, &c->sym_ring}) {
     if (!b->local) continue;
     cudaDeviceSynchronize();
     for (int q = 0; q < c->world; ++q)
@@ -520,12 +521,12 @@ int sdp4_comm_chunks(sdp4_comm_t c, size_t numel, int group) {
 }
 
 size_t sdp4_wire_unit_bytes(size_t n, int bits, int group) {
-  if (!valid_bits(bits) || !is_pow2(group)) return 0;
+  if (!valid_wbits(bits) || !is_pow2(group)) return 0;
   return unit_bytes(n, bits, group);
 }
 
 size_t sdp4_qwd_workspace_bytes(int world, size_t numel, int bits, int group) {
-  if (world < 1 || !valid_bits(bits) || !is_pow2(group) || numel % (size_t)world) return 0;
+  if (world < 1 || !valid_wbits(bits) || !is_pow2(group) || numel % (size_t)world) return 0;
   size_t m = 0;
   for (int C = 1; C <= kMaxChunks; ++C) m = std::max(m, qwd_total(world, numel / world, bits, group, C));
   return m;
@@ -546,27 +547,34 @@ size_t sdp4_tlq_workspace_offset(int M, int N, size_t numel, int bi, int be, int
   return offs[region];
 }
 
-sdp4_status sdp4_qwd_quantize(sdp4_comm_t c, const float* w_main_shard, const void* w_model_full,
-                              sdp4_dtype model_dtype, size_t numel, int bits, int group, sdp4_round rnd,
-                              uint64_t seed, void* workspace, size_t workspace_bytes, void* stream) {
+namespace {
+// Alg. 2 l.2-3 (qWD, diff) or Alg. 1's "Quantize weights" (qW, !diff: w_model_full unused).
+sdp4_status weight_quantize(sdp4_comm_t c, bool diff, const float* w_main_shard, const void* w_model_full,
+                            sdp4_dtype model_dtype, size_t numel, int bits, int group, sdp4_round rnd, uint64_t seed,
+                            void* workspace, size_t workspace_bytes, void* stream, const char* kname) {
   g_err.clear();
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (!valid_round(rnd)) return fail(SDP4_EINVAL, "bad rounding mode %d", (int)rnd);
-  if (!valid_bits(bits)) return fail(SDP4_EINVAL, "bits %d not in {4, 8, 32}", bits);
-  if (model_dtype != SDP4_F32 && model_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad model dtype");
+  if (!valid_wbits(bits)) return fail(SDP4_EINVAL, "bits %d not in {2, 4, 8, 32}", bits);
+  if (diff && model_dtype != SDP4_F32 && model_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad model dtype");
   sdp4_status s = check_sizes(c->world, numel, group);
   if (s != SDP4_OK) return s;
   if ((s = check_ptr(w_main_shard, "w_main_shard")) != SDP4_OK) return s;
-  if ((s = check_ptr(w_model_full, "w_model_full")) != SDP4_OK) return s;
+  if (diff && (s = check_ptr(w_model_full, "w_model_full")) != SDP4_OK) return s;
   if ((s = check_ptr(workspace, "workspace")) != SDP4_OK) return s;
   const size_t need = sdp4_qwd_workspace_bytes(c->world, numel, bits, group);
   if (workspace_bytes < need) return fail(SDP4_ESTATE, "workspace %zu < %zu bytes", workspace_bytes, need);
   if ((s = async_check(c)) != SDP4_OK) return s;
   const size_t S = numel / c->world;
-  const size_t es = esize(model_dtype);
+  const size_t es = diff ? esize(model_dtype) : 0;
   const auto chunks = plan_chunks(S, c->chunks(S), group);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int sms = c->sms(chunks.size() > 1);
+  const int sr = rnd == SDP4_STOCHASTIC;
+  const uint32_t key = sr_key(seed, kStageQwd, c->rank);
+  auto shard_of = [&](size_t off) -> const void* {
+    return diff ? static_cast<const uint8_t*>(w_model_full) + ((size_t)c->rank * S + off) * es : nullptr;
+  };
   if (c->transport == kTransportP2P) {
     // Alg. 2 l.2-3: K1 writes unit `rank` into this rank's own symmetric buffer and raises
     // flag[0][rank] on every peer; the all-gather (l.4) is the pull inside each rank's K2.
@@ -579,11 +587,8 @@ sdp4_status sdp4_qwd_quantize(sdp4_comm_t c, const float* w_main_shard, const vo
     d.p[0] = sym_region(c->sym_qwd, c->rank, ep);
     std::vector<int> all(c->world);
     for (int q = 0; q < c->world; ++q) all[q] = q;
-    const void* shard = static_cast<const uint8_t*>(w_model_full) + (size_t)c->rank * S * es;
-    const int sr = rnd == SDP4_STOCHASTIC;
-    const uint32_t key = sr_key(seed, kStageQwd, c->rank);
-    s = launch(c, "K1_qwd_quantize", st, [&] {
-      return sdp4::launch_qwd_quantize(w_main_shard, shard, model_dtype, S, bits, group, d, sr, key,
+    s = launch(c, kname, st, [&] {
+      return sdp4::launch_qwd_quantize(w_main_shard, shard_of(0), model_dtype, S, bits, group, d, sr, key,
                                        (uint64_t)c->rank * S, c->sm_count, st);
     });
     if (s != SDP4_OK) return s;
@@ -592,15 +597,13 @@ sdp4_status sdp4_qwd_quantize(sdp4_comm_t c, const float* w_main_shard, const vo
   uint8_t* region = static_cast<uint8_t*>(workspace);
   for (const Chunk& ch : chunks) {  // Alg. 2 l.2-3 per chunk: unit (chunk, rank)
     const size_t W = unit_bytes(ch.len, bits, group);
-    const void* shard = static_cast<const uint8_t*>(w_model_full) + ((size_t)c->rank * S + ch.off) * es;
     sdp4::Dests d;
     d.n = 1;
     d.remote = 0;
     d.p[0] = region + (size_t)c->rank * W;
-    s = launch(c, "K1_qwd_quantize", st, [&] {
-      return sdp4::launch_qwd_quantize(w_main_shard + ch.off, shard, model_dtype, ch.len, bits, group, d,
-                                       rnd == SDP4_STOCHASTIC, sr_key(seed, kStageQwd, c->rank),
-                                       (uint64_t)c->rank * S + ch.off, sms, st);
+    s = launch(c, kname, st, [&] {
+      return sdp4::launch_qwd_quantize(w_main_shard + ch.off, shard_of(ch.off), model_dtype, ch.len, bits, group, d,
+                                       sr, key, (uint64_t)c->rank * S + ch.off, sms, st);
     });
     if (s != SDP4_OK) return s;
     region += (size_t)c->world * W;
@@ -608,11 +611,12 @@ sdp4_status sdp4_qwd_quantize(sdp4_comm_t c, const float* w_main_shard, const vo
   return SDP4_OK;
 }
 
-sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes, size_t numel, int bits,
-                                     int group, void* w_model_full, sdp4_dtype model_dtype, void* stream) {
+// Alg. 2 l.4-5 (qWD: add) or Alg. 1's "AllGather" + dequantize (qW: assign).
+sdp4_status weight_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes, size_t numel, int bits, int group,
+                         void* w_model_full, sdp4_dtype model_dtype, void* stream, bool add, const char* kname) {
   g_err.clear();
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
-  if (!valid_bits(bits)) return fail(SDP4_EINVAL, "bits %d not in {4, 8, 32}", bits);
+  if (!valid_wbits(bits)) return fail(SDP4_EINVAL, "bits %d not in {2, 4, 8, 32}", bits);
   if (model_dtype != SDP4_F32 && model_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad model dtype");
   sdp4_status s = check_sizes(c->world, numel, group);
   if (s != SDP4_OK) return s;
@@ -638,8 +642,8 @@ sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t c, void* workspace, size_t work
     u.n = P;
     u.remote = 0;
     for (int q = 0; q < P; ++q) u.p[q] = sym_region(c->sym_qwd, q, ep);
-    return launch(c, "K2_qwd_apply", st, [&] {
-      return sdp4::launch_qwd_apply(u, P, S, S, bits, group, w_model_full, model_dtype, c->sm_count, st);
+    return launch(c, kname, st, [&] {
+      return sdp4::launch_qwd_apply(u, P, S, S, bits, group, w_model_full, model_dtype, add, c->sm_count, st);
     });
   }
   if (P > 1) c->link(st, c->side);  // the units of every chunk were written on st (K1)
@@ -659,13 +663,39 @@ sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t c, void* workspace, size_t work
     u.n = P;
     u.remote = 0;
     for (int q = 0; q < P && q < sdp4::kMaxDests; ++q) u.p[q] = region + (size_t)q * W;
-    s = launch(c, "K2_qwd_apply", st, [&] {
-      return sdp4::launch_qwd_apply(u, P, ch.len, S, bits, group, wm, model_dtype, sms, st);
+    s = launch(c, kname, st, [&] {
+      return sdp4::launch_qwd_apply(u, P, ch.len, S, bits, group, wm, model_dtype, add, sms, st);
     });
     if (s != SDP4_OK) return s;
     region += (size_t)P * W;
   }
   return SDP4_OK;
+}
+}  // namespace
+
+sdp4_status sdp4_qwd_quantize(sdp4_comm_t c, const float* w_main_shard, const void* w_model_full,
+                              sdp4_dtype model_dtype, size_t numel, int bits, int group, sdp4_round rnd,
+                              uint64_t seed, void* workspace, size_t workspace_bytes, void* stream) {
+  return weight_quantize(c, true, w_main_shard, w_model_full, model_dtype, numel, bits, group, rnd, seed, workspace,
+                         workspace_bytes, stream, "K1_qwd_quantize");
+}
+
+sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes, size_t numel, int bits,
+                                     int group, void* w_model_full, sdp4_dtype model_dtype, void* stream) {
+  return weight_apply(c, workspace, workspace_bytes, numel, bits, group, w_model_full, model_dtype, stream, true,
+                      "K2_qwd_apply");
+}
+
+sdp4_status sdp4_qw_quantize(sdp4_comm_t c, const float* w_main_shard, size_t numel, int bits, int group,
+                             sdp4_round rnd, uint64_t seed, void* workspace, size_t workspace_bytes, void* stream) {
+  return weight_quantize(c, false, w_main_shard, nullptr, SDP4_F32, numel, bits, group, rnd, seed, workspace,
+                         workspace_bytes, stream, "K1_qw_quantize");
+}
+
+sdp4_status sdp4_qw_allgather_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes, size_t numel, int bits,
+                                    int group, void* w_model_full, sdp4_dtype model_dtype, void* stream) {
+  return weight_apply(c, workspace, workspace_bytes, numel, bits, group, w_model_full, model_dtype, stream, false,
+                      "K2_qw_apply");
 }
 
 sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dtype grad_dtype, size_t numel,
@@ -799,6 +829,74 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     if (i - 2 >= 0 && i - 2 < C && (s = stage_k5(i - 2)) != SDP4_OK) return s;
   }
   return SDP4_OK;
+}
+
+size_t sdp4_ring_workspace_bytes(int world, size_t numel, int bits, int group) {
+  if (world < 1 || !valid_bits(bits) || !is_pow2(group) || numel % (size_t)world) return 0;
+  return 2 * unit_bytes(numel / world, bits, group);
+}
+
+// Ring reduce-scatter with per-hop quantization (sec. 2.3) -- the ablation baseline.
+// Hop t on rank r: chunk (r - t - 1) mod P; K6 folds the received partial sum into this rank's
+// gradient chunk and quantizes it into the next rank's receive slot; the last hop writes the
+// fp32 output shard r.  P2P: slot t of hop t in the library's symmetric buffer, one flag per
+// hop raised with cuStreamWriteValue32 (value (epoch << 6) + t + 1).  NCCL: ncclSend/ncclRecv.
+sdp4_status sdp4_ring_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dtype grad_dtype, size_t numel, int bits,
+                                     int group, int average, float* out_shard, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!c) return fail(SDP4_EINVAL, "comm is NULL");
+  if (!valid_bits(bits)) return fail(SDP4_EINVAL, "bits %d not in {4, 8, 32}", bits);
+  if (grad_dtype != SDP4_F32 && grad_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad grad dtype");
+  sdp4_status s = check_sizes(c->world, numel, group);
+  if (s != SDP4_OK) return s;
+  if ((s = check_ptr(grad, "grad")) != SDP4_OK) return s;
+  if ((s = check_ptr(out_shard, "out_shard")) != SDP4_OK) return s;
+  if ((s = check_ptr(workspace, "workspace")) != SDP4_OK) return s;
+  const size_t need = sdp4_ring_workspace_bytes(c->world, numel, bits, group);
+  if (workspace_bytes < need) return fail(SDP4_ESTATE, "workspace %zu < %zu bytes", workspace_bytes, need);
+  if ((s = async_check(c)) != SDP4_OK) return s;
+  const int P = c->world, r = c->rank;
+  if (P > sdp4::kMaxDests) return fail(SDP4_EINVAL, "world %d > %d", P, sdp4::kMaxDests);
+  const size_t S = numel / P, es = esize(grad_dtype), W = unit_bytes(S, bits, group);
+  const float kappa = average ? 1.0f / (float)P : 1.0f;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int sms = c->sm_count;
+  auto chunk = [&](int j) { return static_cast<const uint8_t*>(grad) + (size_t)j * S * es; };
+  auto hop = [&](int j, const uint8_t* recv, uint8_t* dst, float* out) {
+    return launch(c, "K6_ring_hop", st, [&] {
+      return sdp4::launch_ring_hop(chunk(j), grad_dtype, recv, dst, out, kappa, S, bits, group, sms, st);
+    });
+  };
+  if (P == 1) return hop(0, nullptr, nullptr, out_shard);
+  const int next = (r + 1) % P, prev = (r + P - 1) % P;
+  if (c->transport == kTransportP2P) {
+    if ((s = sym_ensure(c, c->sym_ring, (size_t)(P - 1) * W, &c->epoch_ring)) != SDP4_OK) return s;
+    const uint32_t ep = ++c->epoch_ring;
+    auto slot = [&](int owner, int t) { return sym_region(c->sym_ring, owner, ep) + (size_t)t * W; };
+    auto val = [&](int t) { return (ep << 6) + (uint32_t)t + 1; };
+    for (int t = 0; t < P - 1; ++t) {
+      if (t > 0 && (s = wait_peers(c, st, c->sym_ring, 0, {prev}, val(t - 1))) != SDP4_OK) return s;
+      if ((s = hop((r - t - 1 + 2 * P) % P, t ? slot(r, t - 1) : nullptr, slot(next, t), nullptr)) != SDP4_OK)
+        return s;
+      if ((s = signal_peers(c, st, c->sym_ring, 0, {next}, val(t))) != SDP4_OK) return s;
+    }
+    if ((s = wait_peers(c, st, c->sym_ring, 0, {prev}, val(P - 2))) != SDP4_OK) return s;
+    return hop(r, slot(r, P - 2), nullptr, out_shard);
+  }
+  uint8_t* send = static_cast<uint8_t*>(workspace);
+  uint8_t* recv = send + W;
+  for (int t = 0; t < P - 1; ++t) {
+    if ((s = hop((r - t - 1 + 2 * P) % P, t ? recv : nullptr, send, nullptr)) != SDP4_OK) return s;
+    s = nccl_op(c, "nccl_ring_sendrecv", st, [&] {
+      ncclGroupStart();
+      ncclSend(send, W, ncclUint8, next, c->world_c, st);
+      ncclRecv(recv, W, ncclUint8, prev, c->world_c, st);
+      return ncclGroupEnd();
+    });
+    if (s != SDP4_OK) return s;
+  }
+  return hop(r, recv, nullptr, out_shard);
 }
 
 sdp4_status sdp4_tlq_stage_quantize(const void* grad, sdp4_dtype grad_dtype, size_t numel, int M, int N,

@@ -93,6 +93,18 @@ struct SR {
 __device__ __forceinline__ uint32_t pack8x4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
+// int2 (ternary weight codec, R4): element 4j+i in bits 2i..2i+1 of byte j.
+__device__ __forceinline__ uint32_t pack2x8(const uint32_t* r) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w |= (r[i] & 3u) << (2 * i);
+  return w;
+}
+__device__ __forceinline__ void dec2x16(uint32_t w, float* f) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) f[i] = float((int)(((w >> (2 * i)) & 3u) ^ 2u) - 2);
+}
+
 __device__ __forceinline__ uint32_t pack4x8(const uint32_t* r) {
   uint32_t p01 = (r[0] & 0xFu) | (r[1] << 4);
   uint32_t p23 = (r[2] & 0xFu) | (r[3] << 4);
@@ -487,11 +499,12 @@ struct TileIter {
 // K1  qWD quantize (Alg. 2 l.2-3): d = rn(w_main - widen(w_model)),
 // per G-group s = max|d|, codes = RNE(d * rn(q/s)) (R3: fused, exact product).  8 elements per
 // thread, a group is G/8 consecutive threads.  Output: one wire unit [codes][scales].
+// DIFF = false is the qW ablation codec (Alg. 1, QSDP / ZeRO++): d = w_main itself.
 // =====================================================================================
 constexpr int kVecThreads = 256;  // K1 / K2: 256-thread CTAs, kVecCtas per SM (persistent)
 constexpr int kVecCtas = 8;
 
-template <typename TM, int BITS>
+template <typename TM, int BITS, bool DIFF>
 __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __restrict__ w_main,
                                                                    const TM* __restrict__ w_model, size_t S,
                                                                    int lg, const Dests dst, const SR sr,
@@ -511,7 +524,10 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
       const float4 a0 = *reinterpret_cast<const float4*>(w_main + e0);
       const float4 a1 = *reinterpret_cast<const float4*>(w_main + e0 + 4);
       float m[8];
-      if constexpr (sizeof(TM) == 2) {
+      if constexpr (!DIFF) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m[i] = 0.f;
+      } else if constexpr (sizeof(TM) == 2) {
         const uint4 u = *reinterpret_cast<const uint4*>(w_model + e0);
         m[0] = bf16_lo(u.x); m[1] = bf16_hi(u.x); m[2] = bf16_lo(u.y); m[3] = bf16_hi(u.y);
         m[4] = bf16_lo(u.z); m[5] = bf16_hi(u.z); m[6] = bf16_lo(u.w); m[7] = bf16_hi(u.w);
@@ -521,10 +537,15 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
         m[0] = b0.x; m[1] = b0.y; m[2] = b0.z; m[3] = b0.w;
         m[4] = b1.x; m[5] = b1.y; m[6] = b1.z; m[7] = b1.w;
       }
-      d[0] = __fsub_rn(a0.x, m[0]); d[1] = __fsub_rn(a0.y, m[1]);
-      d[2] = __fsub_rn(a0.z, m[2]); d[3] = __fsub_rn(a0.w, m[3]);
-      d[4] = __fsub_rn(a1.x, m[4]); d[5] = __fsub_rn(a1.y, m[5]);
-      d[6] = __fsub_rn(a1.z, m[6]); d[7] = __fsub_rn(a1.w, m[7]);
+      if constexpr (DIFF) {
+        d[0] = __fsub_rn(a0.x, m[0]); d[1] = __fsub_rn(a0.y, m[1]);
+        d[2] = __fsub_rn(a0.z, m[2]); d[3] = __fsub_rn(a0.w, m[3]);
+        d[4] = __fsub_rn(a1.x, m[4]); d[5] = __fsub_rn(a1.y, m[5]);
+        d[6] = __fsub_rn(a1.z, m[6]); d[7] = __fsub_rn(a1.w, m[7]);
+      } else {
+        d[0] = a0.x; d[1] = a0.y; d[2] = a0.z; d[3] = a0.w;
+        d[4] = a1.x; d[5] = a1.y; d[6] = a1.z; d[7] = a1.w;
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) d[i] = 0.f;
@@ -552,7 +573,11 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
           for (int i = 0; i < 8; ++i) r[i] = rq(d[i], p.inv);
         }
         // every destination unit (all-gather push, Alg. 2 l.4): warp-contiguous stores
-        if constexpr (BITS == 4) {
+        if constexpr (BITS == 2) {
+          uint32_t w = pack2x8(r);
+          if (!p.ok) w = 0u;
+          for (int k = 0; k < dst.n; ++k) *reinterpret_cast<uint16_t*>(dst.p[k] + e0 / 4) = (uint16_t)w;
+        } else if constexpr (BITS == 4) {
           uint32_t w = pack4x8(r);
           if (!p.ok) w = 0u;
           for (int k = 0; k < dst.n; ++k) *reinterpret_cast<uint32_t*>(dst.p[k] + e0 / 2) = w;
@@ -576,14 +601,15 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
 // the gathered local copy (NCCL transport) or, with the P2P transport, rank j's own buffer
 // over NVLink -- the all-gather (Alg. 2 l.4) fused into the consumer as a pull, so the
 // NVLink ingress overlaps the HBM-bound replica update.  Each thread updates two 16-element
-// vectors per tile, all loads issued up front.
+// vectors per tile, all loads issued up front.  ADD = false is the qW ablation codec
+// (Alg. 1): the replica becomes the dequantized weights, w_model = dtype_rn(x^).
 // =====================================================================================
 template <int BITS>
 struct K2Vec {
   static constexpr int CB = BITS == 32 ? 64 : 16 * BITS / 8;  // code bytes per 16 elements
 };
 
-template <typename TM, int BITS>
+template <typename TM, int BITS, bool ADD>
 __device__ __forceinline__ void k2_load(const uint8_t* unit, const float* scales, const TM* wm, size_t e, int lg,
                                         uint4* cw, float& sc, uint4* mw) {
   if constexpr (BITS == 32) {
@@ -592,12 +618,17 @@ __device__ __forceinline__ void k2_load(const uint8_t* unit, const float* scales
   } else if constexpr (BITS == 8) {
     cw[0] = *reinterpret_cast<const uint4*>(unit + e);
     sc = scales[e >> lg];
-  } else {
+  } else if constexpr (BITS == 4) {
     const uint2 w = *reinterpret_cast<const uint2*>(unit + e / 2);
     cw[0] = make_uint4(w.x, w.y, 0u, 0u);
     sc = scales[e >> lg];
+  } else {
+    cw[0] = make_uint4(*reinterpret_cast<const uint32_t*>(unit + e / 4), 0u, 0u, 0u);
+    sc = scales[e >> lg];
   }
-  if constexpr (sizeof(TM) == 2) {
+  if constexpr (!ADD) {
+    return;
+  } else if constexpr (sizeof(TM) == 2) {
     mw[0] = *reinterpret_cast<const uint4*>(wm + e);
     mw[1] = *reinterpret_cast<const uint4*>(wm + e + 8);
   } else {
@@ -606,7 +637,7 @@ __device__ __forceinline__ void k2_load(const uint8_t* unit, const float* scales
   }
 }
 
-template <typename TM, int BITS>
+template <typename TM, int BITS, bool ADD>
 __device__ __forceinline__ void k2_apply(const uint4* cw, float sc, uint4* mw, TM* wm, size_t e, float z) {
   constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
   float x[16];
@@ -619,7 +650,9 @@ __device__ __forceinline__ void k2_apply(const uint4* cw, float sc, uint4* mw, T
   } else {
     const float ds = __fdiv_rn(sc, q);
     float f[16];
-    if constexpr (BITS == 4) {
+    if constexpr (BITS == 2) {
+      dec2x16(cw[0].x, f);
+    } else if constexpr (BITS == 4) {
       dec4x8(cw[0].x, f);
       dec4x8(cw[0].y, f + 8);
     } else {
@@ -628,7 +661,20 @@ __device__ __forceinline__ void k2_apply(const uint4* cw, float sc, uint4* mw, T
 #pragma unroll
     for (int i = 0; i < 16; ++i) x[i] = mulz(f[i], ds, z);  // the product is added next: fusion barrier
   }
-  if constexpr (sizeof(TM) == 2) {
+  if constexpr (!ADD) {
+    if constexpr (sizeof(TM) == 2) {
+      uint4 o[2];
+      uint32_t* w = &o[0].x;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = pack_bf16x2(x[2 * i], x[2 * i + 1]);
+      reinterpret_cast<uint4*>(wm + e)[0] = o[0];
+      reinterpret_cast<uint4*>(wm + e + 8)[0] = o[1];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        reinterpret_cast<float4*>(wm + e + 4 * i)[0] = make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
+    }
+  } else if constexpr (sizeof(TM) == 2) {
     uint32_t* w = &mw[0].x;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -648,7 +694,7 @@ __device__ __forceinline__ void k2_apply(const uint4* cw, float sc, uint4* mw, T
   }
 }
 
-template <typename TM, int BITS>
+template <typename TM, int BITS, bool ADD>
 __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply(const Dests units, size_t S, size_t stride, int P,
                                                                int lg, TM* __restrict__ w_model, float z) {
   constexpr int TILE = kVecThreads * 32;
@@ -662,10 +708,107 @@ __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply(const Dests units, s
     uint4 ca[4], cb[4], ma[4], mb[4];
     float sa = 0.f, sb = 0.f;
     const bool aa = ea < S, ab = eb < S;
-    if (aa) k2_load<TM, BITS>(unit, scales, wm, ea, lg, ca, sa, ma);
-    if (ab) k2_load<TM, BITS>(unit, scales, wm, eb, lg, cb, sb, mb);
-    if (aa) k2_apply<TM, BITS>(ca, sa, ma, wm, ea, z);
-    if (ab) k2_apply<TM, BITS>(cb, sb, mb, wm, eb, z);
+    if (aa) k2_load<TM, BITS, ADD>(unit, scales, wm, ea, lg, ca, sa, ma);
+    if (ab) k2_load<TM, BITS, ADD>(unit, scales, wm, eb, lg, cb, sb, mb);
+    if (aa) k2_apply<TM, BITS, ADD>(ca, sa, ma, wm, ea, z);
+    if (ab) k2_apply<TM, BITS, ADD>(cb, sb, mb, wm, eb, z);
+  }
+}
+
+// =====================================================================================
+// K6  one hop of the ring reduce-scatter with per-hop quantization (sec. 2.3) -- the
+// ablation baseline TLq-HS is measured against.  acc = rn(dequant(recv) + g) (RECV) or g;
+// then either quantize acc into the next rank's wire unit (local or peer memory; K1's
+// vector layout, so a warp stores 128 contiguous code bytes) or, on the last hop,
+// out = rn(acc * kappa).
+// =====================================================================================
+template <typename TG, int BITS, bool RECV, bool LAST>
+__global__ void __launch_bounds__(kVecThreads) k6_ring_hop(const TG* __restrict__ g, const uint8_t* __restrict__ recv,
+                                                               uint8_t* __restrict__ dst, float* __restrict__ out,
+                                                               float kappa, size_t S, int lg, float z) {
+  constexpr int TILE = kVecThreads * 8;
+  __shared__ float red[kVecThreads / 32];
+  constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
+  const int tpg = (1 << lg) >> 3;
+  const size_t ntiles = (S + TILE - 1) / TILE;
+  const size_t sc_off = S * (BITS == 32 ? 4 : BITS) / 8;
+  const int t = threadIdx.x;
+  for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const size_t e0 = tile * TILE + t * 8;
+    const bool act = e0 < S;
+    float a[8];
+    if (act) {
+      if constexpr (sizeof(TG) == 2) {
+        const uint4 u = *reinterpret_cast<const uint4*>(g + e0);
+        a[0] = bf16_lo(u.x); a[1] = bf16_hi(u.x); a[2] = bf16_lo(u.y); a[3] = bf16_hi(u.y);
+        a[4] = bf16_lo(u.z); a[5] = bf16_hi(u.z); a[6] = bf16_lo(u.w); a[7] = bf16_hi(u.w);
+      } else {
+        const float4 b0 = *reinterpret_cast<const float4*>(g + e0);
+        const float4 b1 = *reinterpret_cast<const float4*>(g + e0 + 4);
+        a[0] = b0.x; a[1] = b0.y; a[2] = b0.z; a[3] = b0.w;
+        a[4] = b1.x; a[5] = b1.y; a[6] = b1.z; a[7] = b1.w;
+      }
+      if constexpr (RECV) {
+        float x[8];
+        if constexpr (BITS == 32) {
+          const float4 r0 = *reinterpret_cast<const float4*>(recv + e0 * 4);
+          const float4 r1 = *reinterpret_cast<const float4*>(recv + e0 * 4 + 16);
+          x[0] = r0.x; x[1] = r0.y; x[2] = r0.z; x[3] = r0.w;
+          x[4] = r1.x; x[5] = r1.y; x[6] = r1.z; x[7] = r1.w;
+        } else {
+          const float ds = __fdiv_rn(reinterpret_cast<const float*>(recv + sc_off)[e0 >> lg], q);
+          float f[8];
+          if constexpr (BITS == 4) {
+            dec4x8(*reinterpret_cast<const uint32_t*>(recv + e0 / 2), f);
+          } else {
+            const uint2 w = *reinterpret_cast<const uint2*>(recv + e0);
+            dec8x4(w.x, f);
+            dec8x4(w.y, f + 4);
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] = mulz(f[i], ds, z);  // added next: fusion barrier
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = __fadd_rn(x[i], a[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = 0.f;
+    }
+    if constexpr (LAST) {
+      if (act) {
+        float4* o = reinterpret_cast<float4*>(out + e0);
+        o[0] = make_float4(__fmul_rn(a[0], kappa), __fmul_rn(a[1], kappa), __fmul_rn(a[2], kappa),
+                           __fmul_rn(a[3], kappa));
+        o[1] = make_float4(__fmul_rn(a[4], kappa), __fmul_rn(a[5], kappa), __fmul_rn(a[6], kappa),
+                           __fmul_rn(a[7], kappa));
+      }
+    } else if constexpr (BITS == 32) {
+      if (act) {
+        float4* o = reinterpret_cast<float4*>(dst + e0 * 4);
+        o[0] = make_float4(a[0], a[1], a[2], a[3]);
+        o[1] = make_float4(a[4], a[5], a[6], a[7]);
+      }
+    } else {
+      float m = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m = max_nan(m, fabsf(a[i]));
+      m = group_max(m, tpg, red);
+      const QP p = qparam(m, q);
+      if (act) {
+        uint32_t r[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] = rq(a[i], p.inv);
+        if constexpr (BITS == 4) {
+          *reinterpret_cast<uint32_t*>(dst + e0 / 2) = p.ok ? pack4x8(r) : 0u;
+        } else {
+          *reinterpret_cast<uint2*>(dst + e0) = p.ok ? make_uint2(pack8x4(r[0], r[1], r[2], r[3]),
+                                                                  pack8x4(r[4], r[5], r[6], r[7]))
+                                                     : make_uint2(0u, 0u);
+        }
+        if ((t & (tpg - 1)) == 0) reinterpret_cast<float*>(dst + sc_off)[e0 >> lg] = stored_scale(m, 1.f);
+      }
+    }
   }
 }
 
@@ -1322,30 +1465,63 @@ cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, 
                                 uint64_t idx0, int sms, cudaStream_t st) {
   const SR sr{sr_on, sr_key};
   const int grid = grid_for((S + kVecThreads * 8 - 1) / (kVecThreads * 8), sms * kVecCtas);
-#define K1(TM, B) \
-  k1_qwd_quantize<TM, B><<<grid, kVecThreads, 0, st>>>(w_main, static_cast<const TM*>(w_model_shard), S, __builtin_ctz(G), dst, \
-                                                       sr, idx0)
-  if (model_dtype == kBF16) {
-    if (bits == 4) K1(uint16_t, 4); else if (bits == 8) K1(uint16_t, 8); else K1(uint16_t, 32);
+#define K1(TM, B, DF) \
+  k1_qwd_quantize<TM, B, DF><<<grid, kVecThreads, 0, st>>>(w_main, static_cast<const TM*>(w_model_shard), S, \
+                                                           __builtin_ctz(G), dst, sr, idx0)
+#define K1B(TM, DF) \
+  if (bits == 2) K1(TM, 2, DF); else if (bits == 4) K1(TM, 4, DF); else if (bits == 8) K1(TM, 8, DF); else K1(TM, 32, DF)
+  if (!w_model_shard) {
+    K1B(float, false);
+  } else if (model_dtype == kBF16) {
+    K1B(uint16_t, true);
   } else {
-    if (bits == 4) K1(float, 4); else if (bits == 8) K1(float, 8); else K1(float, 32);
+    K1B(float, true);
   }
+#undef K1B
 #undef K1
   return cudaGetLastError();
 }
 
 cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride, int bits, int G, void* w_model,
-                             int model_dtype, int sms, cudaStream_t st) {
+                             int model_dtype, bool add, int sms, cudaStream_t st) {
   const int grid = grid_for((S + kVecThreads * 32 - 1) / (kVecThreads * 32) * P, sms * kVecCtas);
-#define K2(TM, B)                                                                                  \
-  k2_qwd_apply<TM, B><<<grid, kVecThreads, 0, st>>>(units, S, stride, P, __builtin_ctz(G), \
-                                                    static_cast<TM*>(w_model), -0.0f)
+#define K2(TM, B, AD)                                                                              \
+  k2_qwd_apply<TM, B, AD><<<grid, kVecThreads, 0, st>>>(units, S, stride, P, __builtin_ctz(G), \
+                                                        static_cast<TM*>(w_model), -0.0f)
+#define K2B(TM, AD) \
+  if (bits == 2) K2(TM, 2, AD); else if (bits == 4) K2(TM, 4, AD); else if (bits == 8) K2(TM, 8, AD); else K2(TM, 32, AD)
   if (model_dtype == kBF16) {
-    if (bits == 4) K2(uint16_t, 4); else if (bits == 8) K2(uint16_t, 8); else K2(uint16_t, 32);
+    if (add) { K2B(uint16_t, true); } else { K2B(uint16_t, false); }
   } else {
-    if (bits == 4) K2(float, 4); else if (bits == 8) K2(float, 8); else K2(float, 32);
+    if (add) { K2B(float, true); } else { K2B(float, false); }
   }
+#undef K2B
 #undef K2
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ring_hop(const void* grad_chunk, int grad_dtype, const uint8_t* recv, uint8_t* dst, float* out,
+                            float kappa, size_t S, int bits, int G, int sms, cudaStream_t st) {
+  const int grid = grid_for((S + kVecThreads * 8 - 1) / (kVecThreads * 8), sms * kVecCtas);
+#define K6(TG, B, RV, LS)                                                                                 \
+  k6_ring_hop<TG, B, RV, LS><<<grid, kVecThreads, 0, st>>>(static_cast<const TG*>(grad_chunk), recv, dst, out, \
+                                                           kappa, S, __builtin_ctz(G), -0.0f)
+#define K6B(TG, RV, LS) \
+  if (bits == 4) K6(TG, 4, RV, LS); else if (bits == 8) K6(TG, 8, RV, LS); else K6(TG, 32, RV, LS)
+#define K6T(TG)                                                         \
+  if (recv) {                                                           \
+    if (dst) { K6B(TG, true, false); } else { K6B(TG, true, true); }    \
+  } else {                                                              \
+    if (dst) { K6B(TG, false, false); } else { K6B(TG, false, true); }  \
+  }
+  if (grad_dtype == kBF16) {
+    K6T(uint16_t)
+  } else {
+    K6T(float)
+  }
+#undef K6T
+#undef K6B
+#undef K6
   return cudaGetLastError();
 }
 

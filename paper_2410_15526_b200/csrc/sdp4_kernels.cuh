@@ -29,15 +29,23 @@ struct Dests {
 
 // K1: Alg. 2 l.2-3 -- d = w_main - w_model (this shard), k-bit group quantization
 // into the wire unit at every destination dst.p[0..n) (n = 1: local; n = P: all-gather push).
+// w_model_shard = nullptr: the qW codec (Alg. 1), d = w_main.  bits in {2, 4, 8, 32}.
 // sr_on: stochastic rounding (R14) with key sr_key; element e has global index idx0 + e.
 cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, int model_dtype,
                                 size_t S, int bits, int G, const Dests& dst, int sr_on, uint32_t sr_key,
                                 uint64_t idx0, int sms, cudaStream_t st);
 
 // K2: Alg. 2 l.5 -- for every shard j < P: w_model[j*stride ..+S] += dequant(unit units.p[j])
-// (local or peer memory), in place.
+// (local or peer memory), in place.  add = false (qW): w_model[...] = dequant(unit), no read.
 cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride, int bits, int G, void* w_model,
-                             int model_dtype, int sms, cudaStream_t st);
+                             int model_dtype, bool add, int sms, cudaStream_t st);
+
+// K6: one hop of the ring reduce-scatter with per-hop quantization (sec. 2.3, ablation):
+// acc = (recv ? rn(dequant(recv) + g) : g) over S elements of one chunk (grad dtype);
+// dst != nullptr: quantize acc (bits, G) into the wire unit at dst (local or peer memory);
+// else out = rn(acc * kappa).
+cudaError_t launch_ring_hop(const void* grad_chunk, int grad_dtype, const uint8_t* recv, uint8_t* dst, float* out,
+                            float kappa, size_t S, int bits, int G, int sms, cudaStream_t st);
 
 // K3: Alg. 3 l.2-3 -- blockwise Hadamard (b, in {0,2,..,256}) + bits_intra quantization
 // of S elements of each of the P shards (shard j at grad + j*grad_stride elements); shard

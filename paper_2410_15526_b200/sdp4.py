@@ -46,6 +46,10 @@ SIGNATURES = {
     "sdp4_tlq_workspace_offset": (_c_size, [_ci, _ci, _c_size, _ci, _ci, _ci, _ci]),
     "sdp4_qwd_quantize": (_ci, [_vp, _vp, _vp, _ci, _c_size, _ci, _ci, _ci, _u64, _vp, _c_size, _vp]),
     "sdp4_qwd_allgather_apply": (_ci, [_vp, _vp, _c_size, _c_size, _ci, _ci, _vp, _ci, _vp]),
+    "sdp4_qw_quantize": (_ci, [_vp, _vp, _c_size, _ci, _ci, _ci, _u64, _vp, _c_size, _vp]),
+    "sdp4_qw_allgather_apply": (_ci, [_vp, _vp, _c_size, _c_size, _ci, _ci, _vp, _ci, _vp]),
+    "sdp4_ring_workspace_bytes": (_c_size, [_ci, _c_size, _ci, _ci]),
+    "sdp4_ring_reduce_scatter": (_ci, [_vp, _vp, _ci, _c_size, _ci, _ci, _ci, _vp, _vp, _c_size, _vp]),
     "sdp4_tlq_hs_reduce_scatter": (_ci, [_vp, _vp, _ci, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _u64, _vp, _vp,
                                          _c_size, _vp]),
     "sdp4_tlq_stage_quantize": (_ci, [_vp, _ci, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _u64, _ci, _vp, _vp]),
@@ -108,6 +112,10 @@ def wire_unit_bytes(n: int, bits: int, group: int) -> int:
 
 def qwd_workspace_bytes(world: int, numel: int, bits: int, group: int) -> int:
     return lib().sdp4_qwd_workspace_bytes(world, numel, bits, group)
+
+
+def ring_workspace_bytes(world: int, numel: int, bits: int, group: int) -> int:
+    return lib().sdp4_ring_workspace_bytes(world, numel, bits, group)
 
 
 def tlq_workspace_bytes(M: int, N: int, numel: int, bits_intra: int, bits_inter: int, group: int) -> int:
@@ -234,6 +242,34 @@ class Comm:
                             group: int = 128, stream=None):
         _check(lib().sdp4_qwd_allgather_apply(self._h, _ptr(workspace), workspace.numel(), w_model.numel(), bits,
                                               group, _ptr(w_model), _DT[w_model.dtype], _stream(stream)))
+
+    # -- ablation baselines ---------------------------------------------
+    def qw_quantize(self, w_main_shard: torch.Tensor, numel: int, workspace: torch.Tensor, bits: int = 4,
+                    group: int = 128, seed=None, stream=None):
+        """qW (Alg. 1, QSDP / ZeRO++): quantize the main-weight shard itself."""
+        if w_main_shard.dtype != torch.float32:
+            raise TypeError("w_main_shard must be fp32 (P:211)")
+        _check(lib().sdp4_qw_quantize(self._h, _ptr(w_main_shard), numel, bits, group,
+                                      RNE if seed is None else STOCHASTIC, seed or 0, _ptr(workspace),
+                                      workspace.numel(), _stream(stream)))
+
+    def qw_allgather_apply(self, workspace: torch.Tensor, w_model: torch.Tensor, bits: int = 4, group: int = 128,
+                           stream=None):
+        """qW all-gather + dequantize: the replica becomes the gathered quantized weights."""
+        _check(lib().sdp4_qw_allgather_apply(self._h, _ptr(workspace), workspace.numel(), w_model.numel(), bits,
+                                             group, _ptr(w_model), _DT[w_model.dtype], _stream(stream)))
+
+    def ring_workspace_bytes(self, numel: int, bits: int = 4, group: int = 128) -> int:
+        return ring_workspace_bytes(self.world, numel, bits, group)
+
+    def ring_reduce_scatter(self, grad: torch.Tensor, out_shard: torch.Tensor, workspace: torch.Tensor,
+                            bits: int = 4, group: int = 128, average: bool = True, stream=None):
+        """Ring reduce-scatter with per-hop quantization (sec. 2.3), ablation baseline."""
+        if out_shard.dtype != torch.float32:
+            raise TypeError("out_shard must be fp32")
+        _check(lib().sdp4_ring_reduce_scatter(self._h, _ptr(grad), _DT[grad.dtype], grad.numel(), bits, group,
+                                              int(bool(average)), _ptr(out_shard), _ptr(workspace),
+                                              workspace.numel(), _stream(stream)))
 
     # -- TLq-HS (Alg. 3) -------------------------------------------------------------
     def tlq_hs_reduce_scatter(self, grad: torch.Tensor, out_shard: torch.Tensor, workspace: torch.Tensor,

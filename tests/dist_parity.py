@@ -6,7 +6,8 @@ Every rank draws all P ranks' synthetic inputs (seeded, CPU), runs
   qWD:    sdp4_qwd_quantize + sdp4_qwd_allgather_apply  (ncclAllGather)
   TLq-HS: sdp4_tlq_hs_reduce_scatter                     (2 x ncclAlltoAll, intra/inter split)
 through the C ABI, and checks against the oracle (bit-exact codes/outputs), plus the
-replica identity of w_model across ranks.  Prints one PASS/FAIL line per rank.
+replica identity of w_model across ranks, and the ablation baselines (qW all-gather,
+ring reduce-scatter with per-hop quantization).  Prints one PASS/FAIL line per rank.
 """
 import argparse
 import os
@@ -163,6 +164,29 @@ def run_checks(comm, rank, P, M, N, G, b, S, seed=None):
         if not same.all():
             ok = False
             msgs.append(f"TLq-HS {dtype} out shard: {int((~same).sum())} of {S} elements differ")
+    # ---- ablation baselines (NEXT-3): qW all-gather (Alg. 1) and the per-hop-quantized
+    # ring reduce-scatter, same transports
+    if seed is None:
+        ws = torch.zeros(comm.qwd_workspace_bytes(D, 4, G), dtype=torch.uint8, device="cuda")
+        wq = torch.empty(D, dtype=torch.bfloat16, device="cuda")
+        comm.qw_quantize(mains[rank].cuda(), D, ws, 4, G)
+        comm.qw_allgather_apply(ws, wq, 4, G)
+        torch.cuda.synchronize()
+        _, want = oracle.qw_step([m.numpy() for m in mains], 4, G, model_bf16=True)
+        if not np.array_equal(synth.bf16_bits(wq.cpu()), want):
+            ok = False
+            msgs.append("qW replica differs from oracle")
+        grads = [synth.gradient(D, seed=synth.seed_for(r, 4), dtype=torch.bfloat16) for r in range(P)]
+        for bits in (4, 32):
+            rws = torch.zeros(comm.ring_workspace_bytes(D, bits, G), dtype=torch.uint8, device="cuda")
+            out = torch.empty(S, dtype=torch.float32, device="cuda")
+            comm.ring_reduce_scatter(grads[rank].cuda(), out, rws, bits, G, True)
+            comm.ring_reduce_scatter(grads[rank].cuda(), out, rws, bits, G, True)   # slot reuse across calls
+            torch.cuda.synchronize()
+            w = oracle.ring_reduce_scatter([g.float().numpy() for g in grads], bits, G, True).out[rank]
+            if not np.array_equal(out.cpu().numpy().view(np.uint32), w.view(np.uint32)):
+                ok = False
+                msgs.append(f"ring k={bits} out shard differs from oracle")
     return ok, msgs
 
 

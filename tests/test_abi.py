@@ -67,6 +67,12 @@ def test_validation_errors_before_any_launch():
     assert st == sdp4.EINVAL
     st = L.sdp4_qwd_quantize(c._h, None, None, 1, 4096, 4, 128, 7, 0, None, 0, None)
     assert st == sdp4.EINVAL and b"rounding" in L.sdp4_last_error()   # unknown rounding mode
+    st = L.sdp4_qw_quantize(c._h, None, 4096, 3, 128, 0, 0, None, 0, None)
+    assert st == sdp4.EINVAL and b"bits" in L.sdp4_last_error()
+    st = L.sdp4_ring_reduce_scatter(c._h, None, 0, 4096, 2, 128, 1, None, None, 0, None)
+    assert st == sdp4.EINVAL and b"bits" in L.sdp4_last_error()        # int2 is a weight codec only
+    assert L.sdp4_ring_workspace_bytes(4, 4096, 4, 128) == 2 * oracle.wire_unit_bytes(1024, 4, 128)
+    assert L.sdp4_wire_unit_bytes(4096, 2, 64) == oracle.wire_unit_bytes(4096, 2, 64)
     bad = ctypes.c_void_p()
     assert L.sdp4_comm_init(ctypes.byref(bad), None, 0, 8, 3, 3, 0) == sdp4.EINVAL
     assert L.sdp4_comm_set_chunks(c._h, 17) == sdp4.EINVAL
