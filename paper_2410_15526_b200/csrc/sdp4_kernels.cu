@@ -817,9 +817,10 @@ struct K3Cfg {
   static constexpr int IN_TILE = kTileRows * IN_R;
   static constexpr int OUT_TILE = kTileRows * OUT_R + kTileElems / 32 * 4;  // codes + scales (G >= 32)
   static constexpr int BUDGET = 200 * 1024;
-  static constexpr int S0 = (BUDGET - 2 * OUT_TILE) / IN_TILE;
+  static constexpr int OUTB = 4;  // output tiles in flight (bulk / TMA stores not yet read out of smem)
+  static constexpr int S0 = (BUDGET - OUTB * OUT_TILE) / IN_TILE;
   static constexpr int STAGES = S0 > 4 ? 4 : (S0 < 1 ? 1 : S0);
-  static constexpr int SMEM = STAGES * IN_TILE + 2 * OUT_TILE + 64 + 1024;
+  static constexpr int SMEM = STAGES * IN_TILE + OUTB * OUT_TILE + 64 + 1024;
 };
 
 // =====================================================================================
@@ -851,7 +852,7 @@ __global__ void __launch_bounds__(kTileRows, 1)
   uint8_t* smem = align1024(smem_raw);
   uint8_t* in_buf = smem;
   uint8_t* out_buf = smem + STAGES * C::IN_TILE;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(out_buf + 2 * C::OUT_TILE);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(out_buf + C::OUTB * C::OUT_TILE);
   const int t = threadIdx.x;
   const uint32_t rows_per_shard = (uint32_t)(S / kRowElems);
 
@@ -904,14 +905,14 @@ __global__ void __launch_bounds__(kTileRows, 1)
         }
       }
     }
-    if (t == 0) bulk_wait_read<1>();  // the store issued two tiles ago has left out_buf[i & 1]
+    if (t == 0) bulk_wait_read<C::OUTB - 1>();  // the store of tile i - OUTB has left out_buf[i % OUTB]
     __syncthreads();                  // stage s fully consumed -> refill it
     if (t == 0) issue(i + STAGES);
 
     fwht_pairs<B>(p);
 
     const uint32_t lp = j % N, mp = j / N;  // shard j = m'N + l' goes to local rank l', unit m' (R9)
-    uint8_t* ot = out_buf + (i & 1) * C::OUT_TILE;
+    uint8_t* ot = out_buf + (i % C::OUTB) * C::OUT_TILE;
     float* osc = reinterpret_cast<float*>(ot + kTileRows * OUT_R);
     uint8_t* unit = out.blk[lp] + mp * unit_bytes;
     const bool remote = (out.remote >> lp) & 1u;  // CTA-uniform
@@ -970,9 +971,10 @@ struct K4Cfg {
   static constexpr int SC_BYTES = BIN == 32 ? 0 : kK4Tile / 32 * 4;
   static constexpr int STAGE = CODE_BYTES + SC_BYTES;
   static constexpr int OUT_TILE = kK4Tile * BOUT / 8 + kK4Tile / 32 * 4;  // staged output: codes + scales
-  static constexpr int S0 = (72 * 1024 - 2 * OUT_TILE) / STAGE;  // ~72 KB per CTA: kK4Ctas per SM
+  static constexpr int OUTB = 4;  // staged remote output tiles in flight
+  static constexpr int S0 = (72 * 1024 - OUTB * OUT_TILE) / STAGE;  // ~72 KB per CTA: kK4Ctas per SM
   static constexpr int STAGES = S0 > 8 ? 8 : (S0 < 1 ? 1 : S0);
-  static constexpr int SMEM = STAGES * STAGE + 2 * OUT_TILE + 64 + 128;
+  static constexpr int SMEM = STAGES * STAGE + OUTB * OUT_TILE + 64 + 128;
   static constexpr int CPT = 64 * BIN / 8 / 16;   // 16-byte chunks per thread
   static constexpr int EPC = 64 / CPT;            // elements per chunk
 };
@@ -1003,7 +1005,7 @@ __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   uint8_t* out_buf = smem + STAGES * C::STAGE;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(out_buf + 2 * C::OUT_TILE);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(out_buf + C::OUTB * C::OUT_TILE);
   const int t = threadIdx.x;
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
@@ -1113,11 +1115,11 @@ __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const 
     // peer destination: stage the tile in smem and bulk-store it (contiguous NVLink writes)
     const bool remote = (dst.remote >> mp) & 1u;  // CTA-uniform
     uint8_t* gout = dst.p[mp];
-    uint8_t* ot = remote ? out_buf + (i & 1) * C::OUT_TILE : gout + e0 * BOUT / 8;
+    uint8_t* ot = remote ? out_buf + (i % C::OUTB) * C::OUT_TILE : gout + e0 * BOUT / 8;
     float* osc = remote ? reinterpret_cast<float*>(ot + kK4Tile * BOUT / 8)
                         : reinterpret_cast<float*>(gout + S * BOUT / 8) + (e0 >> lg);
     if (remote) {
-      if (t == 0) bulk_wait_read<1>();  // the stores issued two tiles ago have left out_buf[i & 1]
+      if (t == 0) bulk_wait_read<C::OUTB - 1>();  // the stores of tile i - OUTB have left out_buf[i % OUTB]
       __syncthreads();
     }
     auto vbase = [&](int v) {  // element offset (within the thread's 64) of slot-order vector v
