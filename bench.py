@@ -54,6 +54,8 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-comparators", action="store_true")
+    p.add_argument("--intra-pull", type=str, default=None,
+                   help="P2P: num/den of the intra all-to-all pulled by K4 (default: the library's 1/2)")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle timing")
     return p.parse_args()
 
@@ -246,6 +248,8 @@ def run_sdp4(a, rank, world, local_rank):
     comm = Comm.from_process_group(a.groups, dev, a.nccl_ctas, a.chunks) if world > 1 else Comm()
     if world > 1 and a.transport != "auto":
         comm.set_transport(a.transport)
+    if a.intra_pull:
+        comm.set_intra_pull(*[int(x) for x in a.intra_pull.split("/")])
     lr = synth.GPT_LR.get(a.model, 2e-4)
     # synthetic inputs: w_model identical on all ranks, w_main shard r, grad per rank
     w_model = synth.model_weights(D, seed=synth.seed_for(0, 1), device=dev, dtype=mdt)
@@ -341,6 +345,23 @@ def run_sdp4(a, rank, world, local_rank):
                              "hbm_frac": round(ach / peak, 4) if ach else None,
                              "peak_source": "B200_PROFILING.md measured peer copy per direction (fallback)"})
 
+    # each collective alone (K steps each): effective pre-quantization GB/s and, with the P2P
+    # transport, the NVLink bytes this rank moves against the 900 GB/s per-direction NVLink 5
+    # figure the north star names (the fused kernels are the collectives: no NCCL kernel runs)
+    t_qwd = timed(lambda: (comm.qwd_quantize(w_main, w_model, ws_q, a.bits_w, a.qwd_group),
+                           comm.qwd_allgather_apply(ws_q, w_model, a.bits_w, a.qwd_group)), a.steps)
+    t_tlq = timed(lambda: comm.tlq_hs_reduce_scatter(grad, out, ws_t, a.bits_intra, a.bits_inter, a.group,
+                                                     a.hadamard, True), a.steps)
+    nv_q = kernel_nvlink_bytes("K2", D, S, P, M, N, a, transport)
+    nv_t = kernel_nvlink_bytes("K3", D, S, P, M, N, a, transport) + kernel_nvlink_bytes("K4", D, S, P, M, N, a,
+                                                                                          transport)
+    collectives = {}
+    for name, t, pre, nv in (("qwd_all_gather", t_qwd, D * 4, nv_q), ("tlq_hs_reduce_scatter", t_tlq, D * g_bytes, nv_t)):
+        collectives[name] = {"ms": round(t, 4), "pre_quant_GBps": round(P * pre / (t * 1e-3) / 1e9, 1),
+                             "nvlink_bytes_per_rank": int(nv),
+                             "nvlink_GBps": round(nv / (t * 1e-3) / 1e9, 1) if nv else None,
+                             "nvlink_frac_of_900": round(nv / (t * 1e-3) / 900e9, 4) if nv else None}
+
     # unquantized NCCL comparators on the same buffers (sec. 2.1), N > 1 only
     comparators = None
     if world > 1 and not a.no_comparators:
@@ -352,10 +373,18 @@ def run_sdp4(a, rank, world, local_rank):
         t_ag = timed(lambda: dist.all_gather_into_tensor(big, d_shard), max(3, a.steps // 2))
         t_rs = timed(lambda: dist.reduce_scatter_tensor(rs_out, grad, op=dist.ReduceOp.AVG), max(3, a.steps // 2))
         del big
+        # ablation baselines through libsdp4 (NEXT-3): 4-bit ring reduce-scatter with per-hop
+        # quantization and the qW direct-weight all-gather (Alg. 1)
+        ws_r = torch.empty(comm.ring_workspace_bytes(D, a.bits_inter, a.group), dtype=torch.uint8, device=dev)
+        t_ring = timed(lambda: comm.ring_reduce_scatter(grad, out, ws_r, a.bits_inter, a.group, True),
+                       max(3, a.steps // 2))
+        del ws_r
         comparators = {"nccl_all_gather_fp32_ms": round(t_ag, 3), "nccl_reduce_scatter_grad_ms": round(t_rs, 3),
                        "unquantized_ms_per_step": round(t_ag + t_rs, 3),
                        "unquantized_GBps": round(P * pre_bytes_rank / ((t_ag + t_rs) * 1e-3) / 1e9, 2),
-                       "speedup_vs_unquantized": round((t_ag + t_rs) / ms, 3)}
+                       "speedup_vs_unquantized": round((t_ag + t_rs) / ms, 3),
+                       "speedup_all_gather": round(t_ag / t_qwd, 3), "speedup_reduce_scatter": round(t_rs / t_tlq, 3),
+                       f"ring_q{a.bits_inter}_reduce_scatter_ms": round(t_ring, 3)}
 
     # end to end through the public API with host buffers (pinned), copies inside the region
     e2e = None
@@ -390,6 +419,7 @@ def run_sdp4(a, rank, world, local_rank):
                 "config": {"workload": workload, "D": D, "D_unpadded": D0, "M": M, "N": N, "G": a.group,
                            "pipeline_chunks": comm.chunks(D, a.group),
                            "transport": comm.transport if world > 1 else "local",
+                           "intra_pull": a.intra_pull or "1/2",
                            "G_w": a.qwd_group, "hadamard_block": a.hadamard,
                            "bits": {"qwd": a.bits_w, "intra": a.bits_intra, "inter": a.bits_inter},
                            "grad_dtype": a.grad_dtype, "model_dtype": a.model_dtype,
@@ -398,7 +428,7 @@ def run_sdp4(a, rank, world, local_rank):
                            "storage": "bf16/fp32 storage, fp32 arithmetic, int8/int4 wire codes"},
                 "clocks": clk.summary(), "gpu_launches": int(launches), "kernels": kern, "comm_ops": comm_ops,
                 "ms_per_step_profiled": round(ms_prof, 4), "roofline": roofline,
-                "e2e": e2e, "comparators": comparators, "cpu_baseline": cpu}
+                "collectives": collectives, "e2e": e2e, "comparators": comparators, "cpu_baseline": cpu}
         emit(line)
     comm.close()
 

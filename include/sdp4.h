@@ -105,6 +105,15 @@ int sdp4_comm_chunks(sdp4_comm_t comm, size_t numel, int group);
 sdp4_status sdp4_comm_set_transport(sdp4_comm_t comm, int transport);
 int sdp4_comm_transport(sdp4_comm_t comm);
 
+/* Host.  P2P transport only: how the intra all-to-all (Alg. 3 l.4) moves over NVLink.  Of
+ * the K3 tiles (16384 elements of a shard) bound for another local rank, those with
+ * tile_index % den < num are PULLED -- K3 stores them into this rank's own outbox and K4 on
+ * the destination bulk-loads them over NVLink -- and the rest are PUSHED by K3 into the
+ * destination's receive block.  Splitting the bytes between the two kernels overlaps them
+ * with both kernels' HBM streams.  num = 0: push only.  Default 1/2.  Results do not depend
+ * on the split (R16).  EINVAL unless 0 <= num <= den, 1 <= den <= 64. */
+sdp4_status sdp4_comm_set_intra_pull(sdp4_comm_t comm, int num, int den);
+
 /* Host, collective.  Destroys the NCCL communicators and frees the comm. */
 sdp4_status sdp4_comm_destroy(sdp4_comm_t comm);
 

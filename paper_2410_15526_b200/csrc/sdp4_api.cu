@@ -140,6 +140,7 @@ struct sdp4_comm {
   int sm_count = 148;
   int nccl_ctas = kDefaultNcclCtas;
   int chunks_cfg = 0;  // 0 = auto
+  int pull_num = 1, pull_den = 2;  // P2P intra all-to-all: share of peer tiles pulled by K4 (IntraPull)
   ncclComm_t world_c = nullptr, intra = nullptr, inter = nullptr;
   cudaStream_t side = nullptr;
   uint64_t launches = 0;
@@ -503,6 +504,14 @@ sdp4_status sdp4_comm_set_chunks(sdp4_comm_t c, int chunks) {
   return SDP4_OK;
 }
 
+sdp4_status sdp4_comm_set_intra_pull(sdp4_comm_t c, int num, int den) {
+  if (!c) return fail(SDP4_EINVAL, "comm is NULL");
+  if (den < 1 || den > 64 || num < 0 || num > den) return fail(SDP4_EINVAL, "intra pull %d/%d not in [0, 1]", num, den);
+  c->pull_num = num;
+  c->pull_den = den;
+  return SDP4_OK;
+}
+
 sdp4_status sdp4_comm_set_transport(sdp4_comm_t c, int transport) {
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (transport != kTransportNccl && transport != kTransportP2P) return fail(SDP4_EINVAL, "bad transport %d", transport);
@@ -729,10 +738,14 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
   const int sr = rnd == SDP4_STOCHASTIC;
   const uint32_t key8 = sr_key(seed, kStageIntra, c->rank), key4 = sr_key(seed, kStageInter, c->rank);
   if (c->transport == kTransportP2P) {
-    // Alg. 3 with both all-to-alls fused into the producing kernels (P2P push).
+    // Alg. 3 with both all-to-alls fused into the producing kernels: the intra one (l.4) split
+    // between K3 pushes and K4 pulls (IntraPull), the inter one (l.10) pushed by K4.
+    // Symmetric region: [intra receive: N blocks][inter receive: M units][outbox: N blocks].
     const size_t w8 = unit_bytes(S, bits_intra, group), w4 = unit_bytes(S, bits_inter, group);
     const size_t intra_bytes = (size_t)N * M * w8, inter_bytes = (size_t)M * w4;
-    if ((s = sym_ensure(c, c->sym_tlq, intra_bytes + inter_bytes, &c->epoch_tlq)) != SDP4_OK) return s;
+    const bool pulling = N > 1 && c->pull_num > 0;
+    const size_t outbox_off = intra_bytes + inter_bytes;
+    if ((s = sym_ensure(c, c->sym_tlq, outbox_off + (pulling ? intra_bytes : 0), &c->epoch_tlq)) != SDP4_OK) return s;
     const uint32_t ep = ++c->epoch_tlq;
     const int m = c->m, l = c->l;
     std::vector<int> group_ranks(N), node_ranks(M);
@@ -742,9 +755,18 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     uint8_t* blocks[sdp4::kMaxN];
     for (int lp = 0; lp < N; ++lp) blocks[lp] = sym_region(c->sym_tlq, m * N + lp, ep) + (size_t)l * M * w8;
     const uint32_t remote = ((1u << N) - 1u) & ~(1u << l);
+    sdp4::IntraPull pull;
+    memset(&pull, 0, sizeof(pull));
+    pull.mask = pulling ? remote : 0u;
+    pull.num = pulling ? c->pull_num : 0;
+    pull.den = c->pull_den;
+    for (int lp = 0; lp < N; ++lp) {
+      pull.outbox[lp] = sym_region(c->sym_tlq, c->rank, ep) + outbox_off + (size_t)lp * M * w8;  // mine, for l'
+      pull.src[lp] = sym_region(c->sym_tlq, m * N + lp, ep) + outbox_off + (size_t)l * M * w8;   // l''s, for me
+    }
     s = launch(c, "K3_tlq_had_quant", st, [&] {
       return sdp4::launch_tlq_had_quant(grad, S, grad_dtype, S, M, N, group, b, cb, bits_intra, blocks, remote, w8,
-                                        sr, key8, 0, c->sm_count, st);
+                                        sr, key8, 0, c->sm_count, st, &pull);
     });
     if (s != SDP4_OK) return s;
     if ((s = signal_peers(c, st, c->sym_tlq, 1, group_ranks, ep)) != SDP4_OK) return s;
@@ -758,7 +780,7 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     uint8_t* my = sym_region(c->sym_tlq, c->rank, ep);
     s = launch(c, "K4_tlq_dq_reduce_q", st, [&] {
       return sdp4::launch_tlq_dq_reduce_q(my, w8, bits_intra, N, M, S, group, d4, bits_inter, sr, key4, l, S, 0,
-                                          c->sm_count, st);
+                                          c->sm_count, st, &pull);
     });
     if (s != SDP4_OK) return s;
     if ((s = signal_peers(c, st, c->sym_tlq, 2, node_ranks, ep)) != SDP4_OK) return s;

@@ -835,9 +835,13 @@ struct K3Cfg {
 // Output of K3: per destination local rank l', the block this rank sends to l' (peer
 // receive buffer or local send buffer); unit m' at blk + m' * unit_bytes.
 struct K3Out {
-  CUtensorMap map[kMaxN];  // valid for local blocks: M units of that block
+  CUtensorMap map[kMaxN];   // valid for local blocks: M units of that block
+  CUtensorMap omap[kMaxN];  // outbox blocks (pulled tiles, IntraPull), local memory
   uint8_t* blk[kMaxN];
-  uint32_t remote;         // bit l': block l' lives in a peer's memory (P2P push)
+  uint8_t* oblk[kMaxN];
+  uint32_t remote;          // bit l': block l' lives in a peer's memory (P2P push)
+  uint32_t pmask;           // bit l': some tiles for l' are pulled (IntraPull)
+  uint32_t pnum, pden;
 };
 
 template <int IN_R, int BITS, int B, bool STOCH>
@@ -914,8 +918,9 @@ __global__ void __launch_bounds__(kTileRows, 1)
     const uint32_t lp = j % N, mp = j / N;  // shard j = m'N + l' goes to local rank l', unit m' (R9)
     uint8_t* ot = out_buf + (i % C::OUTB) * C::OUT_TILE;
     float* osc = reinterpret_cast<float*>(ot + kTileRows * OUT_R);
-    uint8_t* unit = out.blk[lp] + mp * unit_bytes;
-    const bool remote = (out.remote >> lp) & 1u;  // CTA-uniform
+    const bool pull = ((out.pmask >> lp) & 1u) && ts % out.pden < out.pnum;  // kept in the outbox
+    uint8_t* unit = (pull ? out.oblk[lp] : out.blk[lp]) + mp * unit_bytes;
+    const bool remote = !pull && ((out.remote >> lp) & 1u);  // CTA-uniform
     if constexpr (BITS == 32) {  // identity codec (R12): rn(u * c_b)
       const float2 cc = make_float2(cb, cb);
 #pragma unroll
@@ -944,7 +949,7 @@ __global__ void __launch_bounds__(kTileRows, 1)
                  reinterpret_cast<float*>(unit + S * BITS / 8) + (((size_t)ts * kTileElems) >> lg));
       if (t == 0) bulk_commit();
     } else if (t == 0) {
-      tma_store_tile<OUT_R>(&out.map[lp], ot, (int)(ts * kTileRows), (int)mp);
+      tma_store_tile<OUT_R>(pull ? &out.omap[lp] : &out.map[lp], ot, (int)(ts * kTileRows), (int)mp);
       bulk_commit();
     }
   }
@@ -992,11 +997,17 @@ struct ItemCursor {
   }
 };
 
+struct K4Pull {  // IntraPull, K4 side: tiles of source l with ts % den < num come from src[l]
+  const uint8_t* src[kMaxN];
+  uint32_t mask, num, den;
+};
+
 template <int BIN, int BOUT, bool STOCH>
 __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
                                                           int N, int M, size_t S, int lg, const Dests dst,
                                                           uint32_t tpu, uint32_t ntiles, float z, const SR sr,
-                                                          int l_self, size_t sr_stride, size_t sr_off) {
+                                                          int l_self, size_t sr_stride, size_t sr_off,
+                                                          const K4Pull pull) {
   using C = K4Cfg<BIN, BOUT>;
   constexpr int STAGES = C::STAGES, CPT = C::CPT, EPC = C::EPC;
   constexpr float qin = float((1 << (BIN == 32 ? 1 : BIN - 1)) - 1);
@@ -1019,7 +1030,10 @@ __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const 
       const int s = pk % STAGES;
       const size_t e0 = (size_t)pc.it.ts * kK4Tile;
       const uint32_t n = (uint32_t)min((size_t)kK4Tile, S - e0);
-      const uint8_t* unit = recv + ((size_t)pc.l * M + pc.it.unit) * in_unit_bytes;
+      // K3 tile (kTileElems) holding these elements: pulled from the source's outbox or pushed
+      const bool pulled = ((pull.mask >> pc.l) & 1u) && (uint32_t)(e0 / kTileElems) % pull.den < pull.num;
+      const uint8_t* unit = pulled ? pull.src[pc.l] + (size_t)pc.it.unit * in_unit_bytes
+                                   : recv + ((size_t)pc.l * M + pc.it.unit) * in_unit_bytes;
       const uint32_t cb = n * BIN / 8;
       uint32_t sb = 0;
       if constexpr (BIN != 32) sb = (((n >> lg) * 4) + 15) & ~15u;
@@ -1439,7 +1453,8 @@ cudaError_t k5_launch(const CUtensorMap& in_map, const CUtensorMap& out_map, con
 
 template <int BIN, int BOUT, bool STOCH>
 cudaError_t k4_launch_t(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
-                        const SR& sr, int l_self, size_t sr_stride, size_t sr_off, int sms, cudaStream_t st) {
+                        const SR& sr, int l_self, size_t sr_stride, size_t sr_off, int sms, cudaStream_t st,
+                        const K4Pull& pull) {
   constexpr int SMEM = K4Cfg<BIN, BOUT>::SMEM;
   cudaError_t e = set_smem(k4_tlq_dq_reduce_q<BIN, BOUT, STOCH>, SMEM);
   if (e != cudaSuccess) return e;
@@ -1447,16 +1462,21 @@ cudaError_t k4_launch_t(const uint8_t* recv, size_t in_unit_bytes, int N, int M,
   const uint32_t ntiles = tpu * (uint32_t)M;
   const int grid = grid_for(ntiles, sms * kK4Ctas);
   k4_tlq_dq_reduce_q<BIN, BOUT, STOCH><<<grid, kK4Threads, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G),
-                                                                dst, tpu, ntiles, -0.0f, sr, l_self, sr_stride, sr_off);
+                                                                dst, tpu, ntiles, -0.0f, sr, l_self, sr_stride, sr_off,
+                                                                pull);
   return cudaGetLastError();
 }
 template <int BIN, int BOUT>
 cudaError_t k4_launch(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
-                      const SR& sr, int l_self, size_t sr_stride, size_t sr_off, int sms, cudaStream_t st) {
+                      const SR& sr, int l_self, size_t sr_stride, size_t sr_off, int sms, cudaStream_t st,
+                      const K4Pull& pull) {
   if constexpr (BOUT != 32) {
-    if (sr.on) return k4_launch_t<BIN, BOUT, true>(recv, in_unit_bytes, N, M, S, G, dst, sr, l_self, sr_stride, sr_off, sms, st);
+    if (sr.on)
+      return k4_launch_t<BIN, BOUT, true>(recv, in_unit_bytes, N, M, S, G, dst, sr, l_self, sr_stride, sr_off, sms, st,
+                                          pull);
   }
-  return k4_launch_t<BIN, BOUT, false>(recv, in_unit_bytes, N, M, S, G, dst, sr, l_self, sr_stride, sr_off, sms, st);
+  return k4_launch_t<BIN, BOUT, false>(recv, in_unit_bytes, N, M, S, G, dst, sr, l_self, sr_stride, sr_off, sms, st,
+                                       pull);
 }
 
 }  // namespace
@@ -1530,7 +1550,7 @@ cudaError_t launch_ring_hop(const void* grad_chunk, int grad_dtype, const uint8_
 cudaError_t launch_tlq_had_quant(const void* grad, size_t grad_stride, int grad_dtype, size_t S, int M, int N,
                                  int G, int b, float cb, int bits, uint8_t* const* blocks, uint32_t remote_mask,
                                  size_t unit_bytes, int sr_on, uint32_t sr_key, size_t sr_off, int sms,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, const IntraPull* pull) {
   const SR sr{sr_on, sr_key};
   if (N > kMaxN) return cudaErrorInvalidValue;
   const uint64_t rows = S / kRowElems;
@@ -1545,10 +1565,18 @@ cudaError_t launch_tlq_had_quant(const void* grad, size_t grad_stride, int grad_
   cudaError_t e = make_row_map(&in_map, grad, in_r, rows, (uint64_t)M * N, (uint64_t)grad_stride * (in_r / kRowElems));
   if (e != cudaSuccess) return e;
   out.remote = remote_mask;
+  out.pmask = pull && pull->num > 0 ? pull->mask : 0u;
+  out.pnum = pull ? (uint32_t)pull->num : 0u;
+  out.pden = pull && pull->den > 0 ? (uint32_t)pull->den : 1u;
   for (int lp = 0; lp < N; ++lp) {
     out.blk[lp] = blocks[lp];
     if (!((remote_mask >> lp) & 1u)) {
       e = make_row_map(&out.map[lp], blocks[lp], out_r, rows, (uint64_t)M, unit_bytes);
+      if (e != cudaSuccess) return e;
+    }
+    if ((out.pmask >> lp) & 1u) {
+      out.oblk[lp] = pull->outbox[lp];
+      e = make_row_map(&out.omap[lp], pull->outbox[lp], out_r, rows, (uint64_t)M, unit_bytes);
       if (e != cudaSuccess) return e;
     }
   }
@@ -1566,11 +1594,20 @@ cudaError_t launch_tlq_had_quant(const void* grad, size_t grad_stride, int grad_
 cudaError_t launch_tlq_dq_reduce_q(const uint8_t* intra_recv, size_t in_unit_bytes, int bits_in,
                                    int N, int M, size_t S, int G, const Dests& dst, int bits_out, int sr_on,
                                    uint32_t sr_key, int l_self, size_t sr_stride, size_t sr_off, int sms,
-                                   cudaStream_t st) {
-  if (M > kMaxDests) return cudaErrorInvalidValue;
+                                   cudaStream_t st, const IntraPull* pull) {
+  if (M > kMaxDests || N > kMaxN) return cudaErrorInvalidValue;
   const SR sr{sr_on, sr_key};
+  K4Pull kp;
+  memset(&kp, 0, sizeof(kp));
+  kp.den = 1;
+  if (pull && pull->num > 0) {
+    kp.mask = pull->mask;
+    kp.num = (uint32_t)pull->num;
+    kp.den = (uint32_t)pull->den;
+    for (int l = 0; l < N; ++l) kp.src[l] = pull->src[l];
+  }
 #define K4(BI, BO) return k4_launch<BI, BO>(intra_recv, in_unit_bytes, N, M, S, G, dst, sr, l_self, sr_stride, sr_off, \
-                                            sms, st)
+                                            sms, st, kp)
 #define K4O(BI) \
   if (bits_out == 4) { K4(BI, 4); } else if (bits_out == 8) { K4(BI, 8); } else { K4(BI, 32); }
   if (bits_in == 4) { K4O(4); } else if (bits_in == 8) { K4O(8); } else { K4O(32); }

@@ -47,6 +47,19 @@ cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride,
 cudaError_t launch_ring_hop(const void* grad_chunk, int grad_dtype, const uint8_t* recv, uint8_t* dst, float* out,
                             float kappa, size_t S, int bits, int G, int sms, cudaStream_t st);
 
+// Split of the P2P intra all-to-all (Alg. 3 l.4) between push and pull: K3 tile ts (16384
+// elements) of a shard bound for local rank l' with bit l' of `mask` set is PULLED iff
+// ts % den < num -- K3 stores it into its own outbox block l' (local memory) and K4 on rank l'
+// bulk-loads it from there over NVLink; every other peer tile is pushed by K3 into the
+// receive block of rank l'.  Spreading the NVLink bytes over K3 and K4 overlaps them with
+// both kernels' HBM streams.
+struct IntraPull {
+  uint8_t* outbox[kMaxN];     // K3: this rank's outbox block for destination l' (M units)
+  const uint8_t* src[kMaxN];  // K4: the outbox block of source l'' for this rank (peer memory)
+  uint32_t mask;              // K3: destinations with pulled tiles; K4: sources with pulled tiles
+  int num, den;
+};
+
 // K3: Alg. 3 l.2-3 -- blockwise Hadamard (b, in {0,2,..,256}) + bits_intra quantization
 // of S elements of each of the P shards (shard j at grad + j*grad_stride elements); shard
 // m'N + l' goes to unit m' of blocks[l'] (M units of unit_bytes; blocks[l'] is the local send
@@ -55,7 +68,7 @@ cudaError_t launch_ring_hop(const void* grad_chunk, int grad_dtype, const uint8_
 cudaError_t launch_tlq_had_quant(const void* grad, size_t grad_stride, int grad_dtype, size_t S, int M, int N,
                                  int G, int b, float cb, int bits, uint8_t* const* blocks, uint32_t remote_mask,
                                  size_t unit_bytes, int sr_on, uint32_t sr_key, size_t sr_off, int sms,
-                                 cudaStream_t st);
+                                 cudaStream_t st, const IntraPull* pull = nullptr);
 
 // K4: Alg. 3 l.5,7,9 -- dequantize N received units per sub-block m', fp32 reduce in
 // source order, requantize at bits_out into unit dst.p[m'] (local send unit or the
@@ -65,7 +78,7 @@ cudaError_t launch_tlq_had_quant(const void* grad, size_t grad_stride, int grad_
 cudaError_t launch_tlq_dq_reduce_q(const uint8_t* intra_recv, size_t in_unit_bytes, int bits_in,
                                    int N, int M, size_t S, int G, const Dests& dst, int bits_out, int sr_on,
                                    uint32_t sr_key, int l_self, size_t sr_stride, size_t sr_off, int sms,
-                                   cudaStream_t st);
+                                   cudaStream_t st, const IntraPull* pull = nullptr);
 
 // K5: Alg. 3 l.11-13 -- dequantize M received units, fp32 reduce in source order,
 // inverse blockwise Hadamard, scale by kappa, write the fp32 shard.

@@ -40,6 +40,7 @@ SIGNATURES = {
     "sdp4_comm_chunks": (_ci, [_vp, _c_size, _ci]),
     "sdp4_comm_set_transport": (_ci, [_vp, _ci]),
     "sdp4_comm_transport": (_ci, [_vp]),
+    "sdp4_comm_set_intra_pull": (_ci, [_vp, _ci, _ci]),
     "sdp4_wire_unit_bytes": (_c_size, [_c_size, _ci, _ci]),
     "sdp4_qwd_workspace_bytes": (_c_size, [_ci, _c_size, _ci, _ci]),
     "sdp4_tlq_workspace_bytes": (_c_size, [_ci, _ci, _c_size, _ci, _ci, _ci]),
@@ -179,6 +180,11 @@ class Comm:
     def set_transport(self, transport):
         """'nccl' or 'p2p' (fused NVLink push); see sdp4_comm_set_transport."""
         _check(lib().sdp4_comm_set_transport(self._h, self.TRANSPORTS.get(transport, transport)))
+
+    def set_intra_pull(self, num: int, den: int):
+        """P2P: share num/den of the peer tiles of the intra all-to-all pulled by K4 (the rest
+        pushed by K3); see sdp4_comm_set_intra_pull."""
+        _check(lib().sdp4_comm_set_intra_pull(self._h, num, den))
 
     @property
     def transport(self) -> str:

@@ -55,9 +55,13 @@ def main():
     for tr in a.transports.split(","):
         runs += [(tr, ch, None) for ch in ([int(x) for x in a.chunks.split(",")] if tr == "nccl" else [0])]
         runs.append((tr, 3 if tr == "nccl" else 0, 2 ** 34 + 2410))     # stochastic rounding (R14)
+    if "p2p" in a.transports:   # intra all-to-all split between K3 pushes and K4 pulls
+        runs += [("p2p", -1, None), ("p2p", -3, 2410)]
     for tr, chunks, seed in runs:
         comm.set_transport(tr)
-        comm.set_chunks(chunks)
+        comm.set_chunks(max(chunks, 0))
+        if tr == "p2p":      # chunks -1: push only; -3: pull 2 of 3 tiles; else the default 1/2
+            comm.set_intra_pull(*{-1: (0, 1), -3: (2, 3)}.get(chunks, (1, 2)))
         for S in (16384 * 2 + 64 * 5 * max(1, G // 64), 16384 * 12 + 640):
             S -= S % max(G, 64)
             ok_c, m_c = run_checks(comm, rank, P, M, N, G, b, S, seed)
