@@ -38,6 +38,12 @@ __device__ __forceinline__ float max_nan(float a, float b) {
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
   return r;
 }
+// 3-input form (sm_100 FMNMX3): max|.| of two more elements per instruction
+__device__ __forceinline__ float max3_abs_nan(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(fabsf(b)), "f"(fabsf(c)));
+  return r;
+}
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -420,9 +426,9 @@ __device__ __forceinline__ void quant_row(const float2* p, int t, int lg, float 
   constexpr float q = float((1 << (BITS - 1)) - 1);
   float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    a0 = max_nan(a0, fabsf(p[i].x));
-    a1 = max_nan(a1, fabsf(p[i].y));
+  for (int i = 0; i < 32; i += 2) {
+    a0 = max3_abs_nan(a0, p[i].x, p[i + 1].x);
+    a1 = max3_abs_nan(a1, p[i].y, p[i + 1].y);
   }
   QP p0, p1;
   if (lg >= 6) {
@@ -560,7 +566,7 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
     } else {
       float a = 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a = max_nan(a, fabsf(d[i]));
+      for (int i = 0; i < 8; i += 2) a = max3_abs_nan(a, d[i], d[i + 1]);
       a = group_max(a, tpg, red);
       const QP p = qparam(a, q);
       if (act) {
@@ -792,7 +798,7 @@ __global__ void __launch_bounds__(kVecThreads) k6_ring_hop(const TG* __restrict_
     } else {
       float m = 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) m = max_nan(m, fabsf(a[i]));
+      for (int i = 0; i < 8; i += 2) m = max3_abs_nan(m, a[i], a[i + 1]);
       m = group_max(m, tpg, red);
       const QP p = qparam(m, q);
       if (act) {
@@ -817,10 +823,11 @@ struct K3Cfg {
   static constexpr int IN_TILE = kTileRows * IN_R;
   static constexpr int OUT_TILE = kTileRows * OUT_R + kTileElems / 32 * 4;  // codes + scales (G >= 32)
   static constexpr int BUDGET = 200 * 1024;
-  static constexpr int OUTB = 4;  // output tiles in flight (bulk / TMA stores not yet read out of smem)
+  static constexpr int OUTB = OUT_TILE <= 20 * 1024 ? 4 : 2;  // output tiles in flight (stores not yet read out)
   static constexpr int S0 = (BUDGET - OUTB * OUT_TILE) / IN_TILE;
   static constexpr int STAGES = S0 > 4 ? 4 : (S0 < 1 ? 1 : S0);
   static constexpr int SMEM = STAGES * IN_TILE + OUTB * OUT_TILE + 64 + 1024;
+  static_assert(SMEM <= 227 * 1024, "K3 tile configuration exceeds the per-CTA shared memory");
 };
 
 // =====================================================================================
@@ -976,10 +983,11 @@ struct K4Cfg {
   static constexpr int SC_BYTES = BIN == 32 ? 0 : kK4Tile / 32 * 4;
   static constexpr int STAGE = CODE_BYTES + SC_BYTES;
   static constexpr int OUT_TILE = kK4Tile * BOUT / 8 + kK4Tile / 32 * 4;  // staged output: codes + scales
-  static constexpr int OUTB = 4;  // staged remote output tiles in flight
+  static constexpr int OUTB = OUT_TILE <= 8 * 1024 ? 4 : 2;  // staged remote output tiles in flight
   static constexpr int S0 = (72 * 1024 - OUTB * OUT_TILE) / STAGE;  // ~72 KB per CTA: kK4Ctas per SM
   static constexpr int STAGES = S0 > 8 ? 8 : (S0 < 1 ? 1 : S0);
   static constexpr int SMEM = STAGES * STAGE + OUTB * OUT_TILE + 64 + 128;
+  static_assert(SMEM <= 227 * 1024, "K4 tile configuration exceeds the per-CTA shared memory");
   static constexpr int CPT = 64 * BIN / 8 / 16;   // 16-byte chunks per thread
   static constexpr int EPC = 64 / CPT;            // elements per chunk
 };
@@ -1157,7 +1165,7 @@ __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const 
       for (int v = 0; v < 4; ++v) {
         float a = 0.f;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) a = max_nan(a, max_nan(fabsf(acc[8 * v + q].x), fabsf(acc[8 * v + q].y)));
+        for (int q = 0; q < 8; ++q) a = max3_abs_nan(a, acc[8 * v + q].x, acc[8 * v + q].y);
         am[v] = a;
       }
       QP p0, p1;
@@ -1253,6 +1261,7 @@ struct K5Cfg {
   static constexpr int S0 = (100 * 1024 - 2 * OUT_TILE) / STAGE;
   static constexpr int STAGES = S0 > 6 ? 6 : (S0 < 1 ? 1 : S0);
   static constexpr int SMEM = STAGES * STAGE + 2 * OUT_TILE + 64 + 1024;
+  static_assert(SMEM <= 227 * 1024, "K5 tile configuration exceeds the per-CTA shared memory");
 };
 
 template <int IN_R, int B>
