@@ -974,7 +974,7 @@ __global__ void __launch_bounds__(kTileRows, 1)
 // unit m' (P2P transport: the receive slot of node m' itself -- the inter all-to-all).
 // =====================================================================================
 constexpr int kK4Threads = 128;
-constexpr int kK4Ctas = 3;
+constexpr int kK4Ctas = 4;
 constexpr int kK4Tile = kK4Threads * 64;
 
 template <int BIN, int BOUT>
@@ -984,7 +984,7 @@ struct K4Cfg {
   static constexpr int STAGE = CODE_BYTES + SC_BYTES;
   static constexpr int OUT_TILE = kK4Tile * BOUT / 8 + kK4Tile / 32 * 4;  // staged output: codes + scales
   static constexpr int OUTB = OUT_TILE <= 8 * 1024 ? 4 : 2;  // staged remote output tiles in flight
-  static constexpr int S0 = (72 * 1024 - OUTB * OUT_TILE) / STAGE;  // ~72 KB per CTA: kK4Ctas per SM
+  static constexpr int S0 = (54 * 1024 - OUTB * OUT_TILE) / STAGE;  // ~54 KB per CTA: kK4Ctas per SM
   static constexpr int STAGES = S0 > 8 ? 8 : (S0 < 1 ? 1 : S0);
   static constexpr int SMEM = STAGES * STAGE + OUTB * OUT_TILE + 64 + 128;
   static_assert(SMEM <= 227 * 1024, "K4 tile configuration exceeds the per-CTA shared memory");
