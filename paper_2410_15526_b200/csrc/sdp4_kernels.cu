@@ -388,31 +388,83 @@ __device__ __forceinline__ void dec4x8_2(uint32_t w, float* f) {
   }
 }
 
+// K5's row layout: 32 f32x2 registers p[j] = {v[2j], v[2j+1]} (adjacent elements), so the
+// decoded pairs come straight out of one FADD2 each and four consecutive elements are one
+// 16-byte store -- no re-pairing moves.
+//
 // Decode the 64 codes of row t of a row tile (R = 64*BIN/8 bytes) and dequantize:
-// x[i] = {code_i * ds0, code_{i+32} * ds1} (ds0 for elements 0..31, ds1 for 32..63).
+// x[j] = {code_2j, code_2j+1} * ds (ds0 for elements 0..31, ds1 for 32..63).
 template <int BIN, int R, int ROWS>
-__device__ __forceinline__ void dequant_row(const uint8_t* tile, int t, float ds0, float ds1, float z, float2* x) {
-  float f[64];
+__device__ __forceinline__ void dequant_row_adj(const uint8_t* tile, int t, float ds0, float ds1, float z,
+                                                float2* x) {
 #pragma unroll
   for (int c = 0; c < R / 16; ++c) {
     const uint4 u = *reinterpret_cast<const uint4*>(tile + tile_off<R, ROWS>(t, c));
-    if constexpr (BIN == 4) {
-      dec4x8_2(u.x, f + 32 * c); dec4x8_2(u.y, f + 32 * c + 8); dec4x8_2(u.z, f + 32 * c + 16);
-      dec4x8_2(u.w, f + 32 * c + 24);
-    } else if constexpr (BIN == 8) {
-      dec8x4_2(u.x, f + 16 * c); dec8x4_2(u.y, f + 16 * c + 4); dec8x4_2(u.z, f + 16 * c + 8);
-      dec8x4_2(u.w, f + 16 * c + 12);
-    } else {
-      f[4 * c] = __uint_as_float(u.x); f[4 * c + 1] = __uint_as_float(u.y);
-      f[4 * c + 2] = __uint_as_float(u.z); f[4 * c + 3] = __uint_as_float(u.w);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    if constexpr (BIN == 32) {  // chunk c: elements 4c..4c+3
+      x[2 * c] = make_float2(__uint_as_float(w[0]), __uint_as_float(w[1]));
+      x[2 * c + 1] = make_float2(__uint_as_float(w[2]), __uint_as_float(w[3]));
+    } else if constexpr (BIN == 8) {  // chunk c: elements 16c..16c+15 (word q: 16c + 4q + k)
+      const float d = c < 2 ? ds0 : ds1;
+      const float2 dd = make_float2(d, d), m = make_float2(-kDec8, -kDec8);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t xw = w[q] ^ 0x80808080u;
+        const float2 v0 = f2add(make_float2(__uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7540)),
+                                            __uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7541))), m);
+        const float2 v1 = f2add(make_float2(__uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7542)),
+                                            __uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7543))), m);
+        x[8 * c + 2 * q] = f2mulz(v0, dd, z);
+        x[8 * c + 2 * q + 1] = f2mulz(v1, dd, z);
+      }
+    } else {  // BIN == 4: chunk c: elements 32c..32c+31 (word q: 32c + 8q + 2k + {0, 1})
+      const float d = c == 0 ? ds0 : ds1;
+      const float2 dd = make_float2(d, d), m = make_float2(-kDec4, -kDec4);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t xw = w[q] ^ 0x88888888u;
+        const uint32_t lo = xw & 0x0F0F0F0Fu, hi = (xw >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 v = f2add(make_float2(__uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7540 + k)),
+                                             __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7540 + k))), m);
+          x[16 * c + 4 * q + k] = f2mulz(v, dd, z);
+        }
+      }
     }
   }
-  if constexpr (BIN == 32) {
+}
+
+// Unnormalized Sylvester butterfly (R6) on the adjacent-pair layout: stage h = 1 inside each
+// pair, h = 2..32 between pairs j and j + h/2, h = 64, 128 across lanes (row t ^ h/64).
+template <int B>
+__device__ __forceinline__ void fwht_adj(float2* p) {
+  if constexpr (B >= 2) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = make_float2(f[i], f[i + 32]);
-  } else {
+    for (int j = 0; j < 32; ++j) {
+      const float a = p[j].x, c = p[j].y;
+      p[j] = make_float2(__fadd_rn(a, c), __fsub_rn(a, c));
+    }
+  }
 #pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = f2mulz(make_float2(f[i], f[i + 32]), make_float2(ds0, ds1), z);
+  for (int h2 = 1; h2 < 32 && 2 * h2 < B; h2 <<= 1) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if ((j & h2) == 0) {
+        const float2 a = p[j], c = p[j + h2];
+        p[j] = f2add(a, c);
+        p[j + h2] = f2sub(a, c);
+      }
+    }
+  }
+#pragma unroll
+  for (int hx = 1; 64 * hx < B; hx <<= 1) {
+    const bool upper = (threadIdx.x & hx) != 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, p[i].x, hx), __shfl_xor_sync(0xffffffffu, p[i].y, hx));
+      p[i] = upper ? f2sub(o, p[i]) : f2add(p[i], o);
+    }
   }
 }
 
@@ -1326,7 +1378,7 @@ __global__ void __launch_bounds__(kK5Rows, kK5Ctas)
         }
       }
       float2 x[32];
-      dequant_row<BIN, IN_R, kK5Rows>(st, t, ds0, ds1, z, x);
+      dequant_row_adj<BIN, IN_R, kK5Rows>(st, t, ds0, ds1, z, x);
       // R8 order; the first add 0 + x_0 is exact for quantized inputs (x_0 != -0).
       if (m == 0 && BIN != 32) {
 #pragma unroll
@@ -1343,17 +1395,15 @@ __global__ void __launch_bounds__(kK5Rows, kK5Ctas)
       __syncthreads();
       if (t == 0) issue(k + STAGES);
     }
-    fwht_pairs<B>(acc);
+    fwht_adj<B>(acc);
     const float2 kk = make_float2(kappa, kappa);
 #pragma unroll
     for (int q = 0; q < 32; ++q) acc[q] = f2mul(acc[q], kk);
     uint8_t* ot = out_buf + (i & 1) * C::OUT_TILE;
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const float2* q = acc + 4 * (c & 7);
+    for (int c = 0; c < 16; ++c)  // chunk c = elements 4c..4c+3 = pairs 2c, 2c+1
       *reinterpret_cast<float4*>(ot + tile_off<256, kK5Rows>(t, c)) =
-          c < 8 ? make_float4(q[0].x, q[1].x, q[2].x, q[3].x) : make_float4(q[0].y, q[1].y, q[2].y, q[3].y);
-    }
+          make_float4(acc[2 * c].x, acc[2 * c].y, acc[2 * c + 1].x, acc[2 * c + 1].y);
     fence_proxy_async();
     __syncthreads();
     if (t == 0) {
