@@ -386,26 +386,64 @@ def run_sdp4(a, rank, world, local_rank):
                        "speedup_all_gather": round(t_ag / t_qwd, 3), "speedup_reduce_scatter": round(t_rs / t_tlq, 3),
                        f"ring_q{a.bits_inter}_reduce_scatter_ms": round(t_ring, 3)}
 
-    # end to end through the public API with host buffers (pinned), copies inside the region
+    # end to end through the public API with host buffers (pinned), copies inside the region.
+    # Pipelined like a data loader: step i+1's inputs are copied host->device on one stream
+    # while step i computes and its output shard is read back on another (double-buffered
+    # device inputs/outputs), so PCIe runs both directions at once.  Every step's copies are
+    # inside the timed region.
     e2e = None
     if not a.no_e2e:
         h_grad = grad.cpu().pin_memory()
         h_main = w_main.cpu().pin_memory()
         h_out = torch.empty(S, dtype=torch.float32).pin_memory()
+        del grad
+        torch.cuda.empty_cache()
+        comp = torch.cuda.current_stream()
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        gd = [torch.empty_like(h_grad, device=dev) for _ in range(2)]
+        wmn = [torch.empty_like(h_main, device=dev) for _ in range(2)]
+        outs = [torch.empty(S, dtype=torch.float32, device=dev) for _ in range(2)]
+        ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in_ready", "in_free", "out_ready", "out_free")}
+        for k in ("in_free", "out_free"):
+            for e in ev[k]:
+                e.record(comp)
+        it = [0]
 
         def e2e_step():
-            gd = h_grad.to(dev, non_blocking=True)
-            wmn = h_main.to(dev, non_blocking=True)
-            comm.qwd_quantize(wmn, w_model, ws_q, a.bits_w, a.qwd_group)
+            sl = it[0] % 2
+            it[0] += 1
+            with torch.cuda.stream(s_in):
+                s_in.wait_event(ev["in_free"][sl])
+                gd[sl].copy_(h_grad, non_blocking=True)
+                wmn[sl].copy_(h_main, non_blocking=True)
+                ev["in_ready"][sl].record(s_in)
+            comp.wait_event(ev["in_ready"][sl])
+            comp.wait_event(ev["out_free"][sl])
+            comm.qwd_quantize(wmn[sl], w_model, ws_q, a.bits_w, a.qwd_group)
             comm.qwd_allgather_apply(ws_q, w_model, a.bits_w, a.qwd_group)
-            comm.tlq_hs_reduce_scatter(gd, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
-            h_out.copy_(out, non_blocking=True)
-        e2e_step()
-        ms_e2e = timed(e2e_step, max(2, min(a.steps, 5)))
+            comm.tlq_hs_reduce_scatter(gd[sl], outs[sl], ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
+            ev["in_free"][sl].record(comp)
+            ev["out_ready"][sl].record(comp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev["out_ready"][sl])
+                h_out.copy_(outs[sl], non_blocking=True)
+                ev["out_free"][sl].record(s_out)
+
+        def e2e_run(n):
+            for _ in range(n):
+                e2e_step()
+            comp.wait_stream(s_out)    # the region ends when the last readback has landed
+            comp.wait_stream(s_in)
+
+        e2e_run(2)
+        steps_e2e = max(3, min(a.steps, 6))
+        ms_e2e = timed(lambda: e2e_run(steps_e2e), 1) / steps_e2e
         e2e = {"value": round(P * pre_bytes_rank / (ms_e2e * 1e-3) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": int(h_grad.numel() * h_grad.element_size() + h_main.numel() * 4),
-               "d2h_bytes_per_step": int(h_out.numel() * 4), "ms_per_step": round(ms_e2e, 3)}
-        del h_grad, h_main, h_out
+               "d2h_bytes_per_step": int(h_out.numel() * 4), "ms_per_step": round(ms_e2e, 3),
+               "steps": steps_e2e,
+               "schedule": "double-buffered: H2D of step i+1 and D2H of step i overlap step i's kernels"}
+        del h_grad, h_main, h_out, gd, wmn, outs
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
