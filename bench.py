@@ -256,9 +256,12 @@ def run_sdp4(a, rank, world, local_rank):
     w_main = synth.main_weights(w_model[rank * S:(rank + 1) * S], seed=synth.seed_for(rank, 2), lr=lr)
     grad = synth.gradient(D, seed=synth.seed_for(rank, 3), device=dev, dtype=gdt)
     out = torch.empty(S, dtype=torch.float32, device=dev)
-    ws_q = torch.empty(comm.qwd_workspace_bytes(D, a.bits_w, a.qwd_group), dtype=torch.uint8, device=dev)
-    ws_t = torch.empty(comm.tlq_workspace_bytes(D, a.bits_intra, a.bits_inter, a.group), dtype=torch.uint8,
-                       device=dev)
+    if comm.transport == "p2p":   # exchanges through libsdp4's own symmetric buffers
+        ws_q = ws_t = None
+    else:
+        ws_q = torch.empty(comm.qwd_workspace_bytes(D, a.bits_w, a.qwd_group), dtype=torch.uint8, device=dev)
+        ws_t = torch.empty(comm.tlq_workspace_bytes(D, a.bits_intra, a.bits_inter, a.group), dtype=torch.uint8,
+                           device=dev)
 
     def step():
         comm.qwd_quantize(w_main, w_model, ws_q, a.bits_w, a.qwd_group)
@@ -375,7 +378,8 @@ def run_sdp4(a, rank, world, local_rank):
         del big
         # ablation baselines through libsdp4 (NEXT-3): 4-bit ring reduce-scatter with per-hop
         # quantization and the qW direct-weight all-gather (Alg. 1)
-        ws_r = torch.empty(comm.ring_workspace_bytes(D, a.bits_inter, a.group), dtype=torch.uint8, device=dev)
+        ws_r = None if comm.transport == "p2p" else torch.empty(comm.ring_workspace_bytes(D, a.bits_inter, a.group),
+                                                                 dtype=torch.uint8, device=dev)
         t_ring = timed(lambda: comm.ring_reduce_scatter(grad, out, ws_r, a.bits_inter, a.group, True),
                        max(3, a.steps // 2))
         del ws_r

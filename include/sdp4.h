@@ -98,7 +98,7 @@ int sdp4_comm_chunks(sdp4_comm_t comm, size_t numel, int group);
  *     receive buffers of the ranks that own them; the qWD all-gather is a pull inside K2
  *     (unit j read from rank j's buffer while the replica update streams HBM).  Those receive buffers are library-
  *     owned, symmetric, double-buffered by call parity and allocated collectively on first
- *     use (the caller's workspace is then unused); completion is signalled per source with
+ *     use (the caller's workspace is then unused and may be NULL / 0 bytes); completion is signalled per source with
  *     epoch flags (cuStreamWriteValue32 / cuStreamWaitValue32).  P2P never chunks.
  * Results are bit-identical across transports (R16).  sdp4_comm_transport returns the
  * current one. */

@@ -342,6 +342,16 @@ sdp4_status check_ptr(const void* p, const char* what) {
   return SDP4_OK;
 }
 
+// The caller's workspace is only used by the NCCL transport (and at world 1); with the P2P
+// transport the exchanges go through library-owned symmetric buffers, so it may be NULL.
+sdp4_status check_workspace(const sdp4_comm* c, const void* ws, size_t bytes, size_t need) {
+  if (c->transport == kTransportP2P && c->world > 1) return SDP4_OK;
+  sdp4_status s = check_ptr(ws, "workspace");
+  if (s != SDP4_OK) return s;
+  if (bytes < need) return fail(SDP4_ESTATE, "workspace %zu < %zu bytes", bytes, need);
+  return SDP4_OK;
+}
+
 // R1: numel % (P * lcm(G, 64)) == 0, G power of two in [32, 2048].
 sdp4_status check_sizes(int P, size_t numel, int group) {
   if (!is_pow2(group) || group < 32 || group > 2048)
@@ -570,9 +580,8 @@ sdp4_status weight_quantize(sdp4_comm_t c, bool diff, const float* w_main_shard,
   if (s != SDP4_OK) return s;
   if ((s = check_ptr(w_main_shard, "w_main_shard")) != SDP4_OK) return s;
   if (diff && (s = check_ptr(w_model_full, "w_model_full")) != SDP4_OK) return s;
-  if ((s = check_ptr(workspace, "workspace")) != SDP4_OK) return s;
   const size_t need = sdp4_qwd_workspace_bytes(c->world, numel, bits, group);
-  if (workspace_bytes < need) return fail(SDP4_ESTATE, "workspace %zu < %zu bytes", workspace_bytes, need);
+  if ((s = check_workspace(c, workspace, workspace_bytes, need)) != SDP4_OK) return s;
   if ((s = async_check(c)) != SDP4_OK) return s;
   const size_t S = numel / c->world;
   const size_t es = diff ? esize(model_dtype) : 0;
@@ -629,10 +638,9 @@ sdp4_status weight_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes,
   if (model_dtype != SDP4_F32 && model_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad model dtype");
   sdp4_status s = check_sizes(c->world, numel, group);
   if (s != SDP4_OK) return s;
-  if ((s = check_ptr(workspace, "workspace")) != SDP4_OK) return s;
   if ((s = check_ptr(w_model_full, "w_model_full")) != SDP4_OK) return s;
   const size_t need = sdp4_qwd_workspace_bytes(c->world, numel, bits, group);
-  if (workspace_bytes < need) return fail(SDP4_ESTATE, "workspace %zu < %zu bytes", workspace_bytes, need);
+  if ((s = check_workspace(c, workspace, workspace_bytes, need)) != SDP4_OK) return s;
   if ((s = async_check(c)) != SDP4_OK) return s;
   const size_t S = numel / c->world;
   const size_t es = esize(model_dtype);
@@ -720,10 +728,9 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
   if (s != SDP4_OK) return s;
   if ((s = check_ptr(grad, "grad")) != SDP4_OK) return s;
   if ((s = check_ptr(out_shard, "out_shard")) != SDP4_OK) return s;
-  if ((s = check_ptr(workspace, "workspace")) != SDP4_OK) return s;
   const int M = c->M, N = c->N, P = c->world;
   const size_t need = sdp4_tlq_workspace_bytes(M, N, numel, bits_intra, bits_inter, group);
-  if (workspace_bytes < need) return fail(SDP4_ESTATE, "workspace %zu < %zu bytes", workspace_bytes, need);
+  if ((s = check_workspace(c, workspace, workspace_bytes, need)) != SDP4_OK) return s;
   if ((s = async_check(c)) != SDP4_OK) return s;
 
   const size_t S = numel / P;
@@ -874,9 +881,8 @@ sdp4_status sdp4_ring_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dtype
   if (s != SDP4_OK) return s;
   if ((s = check_ptr(grad, "grad")) != SDP4_OK) return s;
   if ((s = check_ptr(out_shard, "out_shard")) != SDP4_OK) return s;
-  if ((s = check_ptr(workspace, "workspace")) != SDP4_OK) return s;
   const size_t need = sdp4_ring_workspace_bytes(c->world, numel, bits, group);
-  if (workspace_bytes < need) return fail(SDP4_ESTATE, "workspace %zu < %zu bytes", workspace_bytes, need);
+  if ((s = check_workspace(c, workspace, workspace_bytes, need)) != SDP4_OK) return s;
   if ((s = async_check(c)) != SDP4_OK) return s;
   const int P = c->world, r = c->rank;
   if (P > sdp4::kMaxDests) return fail(SDP4_EINVAL, "world %d > %d", P, sdp4::kMaxDests);

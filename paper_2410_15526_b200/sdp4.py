@@ -101,6 +101,10 @@ def _ptr(t: Optional[torch.Tensor]):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _nbytes(t: Optional[torch.Tensor]) -> int:
+    return 0 if t is None else t.numel() * t.element_size()
+
+
 def _stream(stream) -> ctypes.c_void_p:
     if stream is None:
         stream = torch.cuda.current_stream()
@@ -242,11 +246,11 @@ class Comm:
             raise TypeError("w_main_shard must be fp32 (P:211)")
         _check(lib().sdp4_qwd_quantize(self._h, _ptr(w_main_shard), _ptr(w_model), _DT[w_model.dtype],
                                        w_model.numel(), bits, group, RNE if seed is None else STOCHASTIC,
-                                       seed or 0, _ptr(workspace), workspace.numel(), _stream(stream)))
+                                       seed or 0, _ptr(workspace), _nbytes(workspace), _stream(stream)))
 
     def qwd_allgather_apply(self, workspace: torch.Tensor, w_model: torch.Tensor, bits: int = 4,
                             group: int = 128, stream=None):
-        _check(lib().sdp4_qwd_allgather_apply(self._h, _ptr(workspace), workspace.numel(), w_model.numel(), bits,
+        _check(lib().sdp4_qwd_allgather_apply(self._h, _ptr(workspace), _nbytes(workspace), w_model.numel(), bits,
                                               group, _ptr(w_model), _DT[w_model.dtype], _stream(stream)))
 
     # -- ablation baselines ---------------------------------------------
@@ -257,12 +261,12 @@ class Comm:
             raise TypeError("w_main_shard must be fp32 (P:211)")
         _check(lib().sdp4_qw_quantize(self._h, _ptr(w_main_shard), numel, bits, group,
                                       RNE if seed is None else STOCHASTIC, seed or 0, _ptr(workspace),
-                                      workspace.numel(), _stream(stream)))
+                                      _nbytes(workspace), _stream(stream)))
 
     def qw_allgather_apply(self, workspace: torch.Tensor, w_model: torch.Tensor, bits: int = 4, group: int = 128,
                            stream=None):
         """qW all-gather + dequantize: the replica becomes the gathered quantized weights."""
-        _check(lib().sdp4_qw_allgather_apply(self._h, _ptr(workspace), workspace.numel(), w_model.numel(), bits,
+        _check(lib().sdp4_qw_allgather_apply(self._h, _ptr(workspace), _nbytes(workspace), w_model.numel(), bits,
                                              group, _ptr(w_model), _DT[w_model.dtype], _stream(stream)))
 
     def ring_workspace_bytes(self, numel: int, bits: int = 4, group: int = 128) -> int:
@@ -275,7 +279,7 @@ class Comm:
             raise TypeError("out_shard must be fp32")
         _check(lib().sdp4_ring_reduce_scatter(self._h, _ptr(grad), _DT[grad.dtype], grad.numel(), bits, group,
                                               int(bool(average)), _ptr(out_shard), _ptr(workspace),
-                                              workspace.numel(), _stream(stream)))
+                                              _nbytes(workspace), _stream(stream)))
 
     # -- TLq-HS (Alg. 3) -------------------------------------------------------------
     def tlq_hs_reduce_scatter(self, grad: torch.Tensor, out_shard: torch.Tensor, workspace: torch.Tensor,
@@ -287,7 +291,7 @@ class Comm:
         _check(lib().sdp4_tlq_hs_reduce_scatter(self._h, _ptr(grad), _DT[grad.dtype], grad.numel(), bits_intra,
                                                 bits_inter, group, hadamard_block, int(bool(average)),
                                                 RNE if seed is None else STOCHASTIC, seed or 0,
-                                                _ptr(out_shard), _ptr(workspace), workspace.numel(),
+                                                _ptr(out_shard), _ptr(workspace), _nbytes(workspace),
                                                 _stream(stream)))
 
     # -- instrumentation -------------------------------------------------------------

@@ -58,27 +58,52 @@ def _gen(seed: int, device) -> torch.Generator:
     return g
 
 
+_BIG = 1 << 31   # above this, buffers are generated in 2^30-element pieces (piece seeds seed+k)
+
+
+def _pieces(n: int, seed: int, dtype, device, fn) -> torch.Tensor:
+    """Generate n elements as fn(count, seed) in pieces so that no full-size fp32 temporary
+    exists (GPT-13B buffers); small buffers (n <= 2^31) are a single piece, unchanged."""
+    if n <= _BIG:
+        return fn(n, seed).to(dtype)
+    out = torch.empty(n, dtype=dtype, device=device)
+    step = 1 << 30
+    for k, o in enumerate(range(0, n, step)):
+        out[o:o + step] = fn(min(step, n - o), seed * 1000003 + k)
+    return out
+
+
 def gradient(n: int, seed: int, device="cpu", dtype=torch.float32, std: float = 1e-3,
              spike_prob: float = 0.01, spike_scale: float = 50.0) -> torch.Tensor:
     """Spiky gradient: N(0, std^2), each element x spike_scale w.p. spike_prob."""
-    g = _gen(seed, device)
-    x = torch.randn(n, generator=g, device=device, dtype=torch.float32) * std
-    if spike_prob > 0:
-        mask = torch.rand(n, generator=g, device=device) < spike_prob
-        x = torch.where(mask, x * spike_scale, x)
-    return x.to(dtype)
+    def fn(m, sd):
+        g = _gen(sd, device)
+        x = torch.randn(m, generator=g, device=device, dtype=torch.float32) * std
+        if spike_prob > 0:
+            mask = torch.rand(m, generator=g, device=device) < spike_prob
+            x = torch.where(mask, x * spike_scale, x)
+        return x
+    return _pieces(n, seed, dtype, device, fn)
 
 
 def model_weights(n: int, seed: int, device="cpu", dtype=torch.bfloat16, std: float = 0.02) -> torch.Tensor:
-    g = _gen(seed, device)
-    return (torch.randn(n, generator=g, device=device, dtype=torch.float32) * std).to(dtype)
+    def fn(m, sd):
+        return torch.randn(m, generator=_gen(sd, device), device=device, dtype=torch.float32) * std
+    return _pieces(n, seed, dtype, device, fn)
 
 
 def main_weights(w_model_shard: torch.Tensor, seed: int, lr: float = 2e-4) -> torch.Tensor:
     """fp32 main weights one optimizer step away from the stored model weights."""
-    g = _gen(seed, w_model_shard.device)
-    u = torch.rand(w_model_shard.numel(), generator=g, device=w_model_shard.device) * 2.0 - 1.0
-    return w_model_shard.to(torch.float32) + lr * u
+    n, dev = w_model_shard.numel(), w_model_shard.device
+    if n <= _BIG:
+        u = torch.rand(n, generator=_gen(seed, dev), device=dev) * 2.0 - 1.0
+        return w_model_shard.to(torch.float32) + lr * u
+    out = w_model_shard.to(torch.float32)
+    step = 1 << 30
+    for k, o in enumerate(range(0, n, step)):
+        m = min(step, n - o)
+        out[o:o + m] += lr * (torch.rand(m, generator=_gen(seed * 1000003 + k, dev), device=dev) * 2.0 - 1.0)
+    return out
 
 
 def uniform_ints(n: int, seed: int, lo: int = -8, hi: int = 8, device="cpu") -> torch.Tensor:

@@ -135,7 +135,8 @@ def run_checks(comm, rank, P, M, N, G, b, S, seed=None):
     # ---- qWD (Alg. 2 l.2-5)
     w_model = synth.model_weights(D, seed=1)
     mains = [synth.main_weights(w_model[r * S:(r + 1) * S], seed=synth.seed_for(r, 2)) for r in range(P)]
-    ws = torch.zeros(comm.qwd_workspace_bytes(D, 4, G), dtype=torch.uint8, device="cuda")
+    p2p = comm.transport == "p2p"      # P2P exchanges through libsdp4's buffers: no workspace
+    ws = None if p2p else torch.zeros(comm.qwd_workspace_bytes(D, 4, G), dtype=torch.uint8, device="cuda")
     wm = w_model.cuda()
     comm.qwd_quantize(mains[rank].cuda(), wm, ws, 4, G, seed=seed)
     comm.qwd_allgather_apply(ws, wm, 4, G)
@@ -156,7 +157,7 @@ def run_checks(comm, rank, P, M, N, G, b, S, seed=None):
     # ---- TLq-HS (Alg. 3)
     for dtype in (torch.bfloat16, torch.float32):
         grads = [synth.gradient(D, seed=synth.seed_for(r, 3), dtype=dtype) for r in range(P)]
-        tws = torch.zeros(comm.tlq_workspace_bytes(D, 8, 4, G), dtype=torch.uint8, device="cuda")
+        tws = None if p2p else torch.zeros(comm.tlq_workspace_bytes(D, 8, 4, G), dtype=torch.uint8, device="cuda")
         out = torch.empty(S, dtype=torch.float32, device="cuda")
         comm.tlq_hs_reduce_scatter(grads[rank].cuda(), out, tws, 8, 4, G, b, True, seed=seed)
         torch.cuda.synchronize()
