@@ -147,10 +147,13 @@ def kernel_nvlink_bytes(name, D, S, P, M, N, a, transport):
         return n * k / 8 + (4 * n / G if k != 32 else 0)
     if name.startswith("K2"):
         return (P - 1) * wire(S, a.bits_w, a.qwd_group)
-    if name.startswith("K3"):
-        return (N - 1) * M * wire(S, a.bits_intra, a.group)
-    if name.startswith("K4"):
-        return (M - 1) * wire(S, a.bits_inter, a.group)
+    num, den = [int(x) for x in (a.intra_pull or "1/2").split("/")]
+    f = num / den if N > 1 else 0.0                      # share of intra tiles K4 pulls
+    intra = (N - 1) * M * wire(S, a.bits_intra, a.group)
+    if name.startswith("K3"):                            # pushed intra tiles (egress)
+        return (1 - f) * intra
+    if name.startswith("K4"):                            # max(pulled intra ingress, inter egress)
+        return max(f * intra, (M - 1) * wire(S, a.bits_inter, a.group))
     return 0
 
 
@@ -356,8 +359,11 @@ def run_sdp4(a, rank, world, local_rank):
     t_tlq = timed(lambda: comm.tlq_hs_reduce_scatter(grad, out, ws_t, a.bits_intra, a.bits_inter, a.group,
                                                      a.hadamard, True), a.steps)
     nv_q = kernel_nvlink_bytes("K2", D, S, P, M, N, a, transport)
-    nv_t = kernel_nvlink_bytes("K3", D, S, P, M, N, a, transport) + kernel_nvlink_bytes("K4", D, S, P, M, N, a,
-                                                                                          transport)
+    def wire_b(n, k, G):
+        return n * k / 8 + (4 * n / G if k != 32 else 0)
+    # per-direction NVLink bytes of one TLq-HS call: intra (N-1) blocks + inter (M-1) units
+    nv_t = ((N - 1) * M * wire_b(S, a.bits_intra, a.group) + (M - 1) * wire_b(S, a.bits_inter, a.group)
+            if transport == "p2p" else 0)
     collectives = {}
     for name, t, pre, nv in (("qwd_all_gather", t_qwd, D * 4, nv_q), ("tlq_hs_reduce_scatter", t_tlq, D * g_bytes, nv_t)):
         collectives[name] = {"ms": round(t, 4), "pre_quant_GBps": round(P * pre / (t * 1e-3) / 1e9, 1),
