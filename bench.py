@@ -307,6 +307,9 @@ def run_sdp4(a, rank, world, local_rank):
     ms_prof = timed(step, a.steps)
     prof = comm.profile_read()
     comm.profile_enable(False)
+    if os.environ.get("SDP4_BENCH_RANKS"):   # diagnostics: every rank's per-kernel / wait times
+        print(f"rank {rank}: " + ", ".join(f"{n} {t / a.steps:.3f}" for n, (t, c) in sorted(prof.items())),
+              file=sys.stderr, flush=True)
 
     pre_bytes_rank = D * (4 + g_bytes)
     value = P * pre_bytes_rank / (ms * 1e-3) / 1e9
@@ -318,7 +321,7 @@ def run_sdp4(a, rank, world, local_rank):
     kern = {}
     transport = comm.transport if world > 1 else "local"
     for name, (tms, cnt) in prof.items():
-        if name.startswith("nccl_"):
+        if name.startswith("nccl_") or name.startswith("wait_"):
             continue
         kb = kernel_bytes(name, D, S, P, M, N, a)
         nb = kernel_nvlink_bytes(name, D, S, P, M, N, a, transport)
@@ -329,7 +332,7 @@ def run_sdp4(a, rank, world, local_rank):
             kern[name]["nvlink_bytes"] = nb
             kern[name]["nvlink_gbs"] = round(nb / (avg * 1e-3) / 1e9, 1)
     comm_ops = {n: {"ms_per_step": round(t / a.steps, 4), "calls": c} for n, (t, c) in prof.items()
-                if n.startswith("nccl_")}
+                if n.startswith("nccl_") or n.startswith("wait_")}
     tot = sum(v["avg_ms"] * v["launches"] for v in kern.values()) or 1.0
     for v in kern.values():
         v["share_of_kernel_time"] = round(v["avg_ms"] * v["launches"] / tot, 4)

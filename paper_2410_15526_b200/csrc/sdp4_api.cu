@@ -318,12 +318,23 @@ sdp4_status signal_peers(sdp4_comm* c, cudaStream_t st, const SymBuf& b, int sta
   return SDP4_OK;
 }
 // Before the consuming kernel on `st`: wait until every source rank raised its flag.
+// With profiling on, the time the stream spends in these waits is recorded as `name`.
 sdp4_status wait_peers(sdp4_comm* c, cudaStream_t st, const SymBuf& b, int stage, const std::vector<int>& srcs,
-                       uint32_t epoch) {
+                       uint32_t epoch, const char* name = "wait") {
+  cudaEvent_t ea = nullptr, eb = nullptr;
+  if (c->profiling) {
+    ea = c->ev();
+    eb = c->ev();
+    cudaEventRecord(ea, st);
+  }
   for (int q : srcs) {
     if (q == c->rank) continue;
     CUresult r = c->wait_value((CUstream)st, flag_ptr(b, c->rank, stage, q), epoch, CU_STREAM_WAIT_VALUE_GEQ);
     if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+  }
+  if (c->profiling) {
+    cudaEventRecord(eb, st);
+    c->pending.push_back({name, ea, eb});
   }
   return SDP4_OK;
 }
@@ -654,13 +665,14 @@ sdp4_status weight_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes,
     const uint32_t ep = c->epoch_qwd;
     std::vector<int> all(P);
     for (int q = 0; q < P; ++q) all[q] = q;
-    if ((s = wait_peers(c, st, c->sym_qwd, 0, all, ep)) != SDP4_OK) return s;
+    if ((s = wait_peers(c, st, c->sym_qwd, 0, all, ep, "wait_qwd_allgather")) != SDP4_OK) return s;
     sdp4::Dests u;
     u.n = P;
     u.remote = 0;
     for (int q = 0; q < P; ++q) u.p[q] = sym_region(c->sym_qwd, q, ep);
     return launch(c, kname, st, [&] {
-      return sdp4::launch_qwd_apply(u, P, S, S, bits, group, w_model_full, model_dtype, add, c->sm_count, st);
+      return sdp4::launch_qwd_apply(u, P, S, S, bits, group, w_model_full, model_dtype, add, c->sm_count, st,
+                                    c->rank);
     });
   }
   if (P > 1) c->link(st, c->side);  // the units of every chunk were written on st (K1)
@@ -777,7 +789,7 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     });
     if (s != SDP4_OK) return s;
     if ((s = signal_peers(c, st, c->sym_tlq, 1, group_ranks, ep)) != SDP4_OK) return s;
-    if ((s = wait_peers(c, st, c->sym_tlq, 1, group_ranks, ep)) != SDP4_OK) return s;
+    if ((s = wait_peers(c, st, c->sym_tlq, 1, group_ranks, ep, "wait_tlq_intra")) != SDP4_OK) return s;
     // K4: unit m' -> slot m (this node) of rank (m', l)'s inter receive region
     sdp4::Dests d4;
     d4.n = M;
@@ -791,7 +803,7 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     });
     if (s != SDP4_OK) return s;
     if ((s = signal_peers(c, st, c->sym_tlq, 2, node_ranks, ep)) != SDP4_OK) return s;
-    if ((s = wait_peers(c, st, c->sym_tlq, 2, node_ranks, ep)) != SDP4_OK) return s;
+    if ((s = wait_peers(c, st, c->sym_tlq, 2, node_ranks, ep, "wait_tlq_inter")) != SDP4_OK) return s;
     return launch(c, "K5_tlq_dq_reduce_had", st, [&] {
       return sdp4::launch_tlq_dq_reduce_had(my + intra_bytes, w4, bits_inter, M, S, group, b, kappa, out_shard,
                                             c->sm_count, st);
@@ -904,12 +916,12 @@ sdp4_status sdp4_ring_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dtype
     auto slot = [&](int owner, int t) { return sym_region(c->sym_ring, owner, ep) + (size_t)t * W; };
     auto val = [&](int t) { return (ep << 6) + (uint32_t)t + 1; };
     for (int t = 0; t < P - 1; ++t) {
-      if (t > 0 && (s = wait_peers(c, st, c->sym_ring, 0, {prev}, val(t - 1))) != SDP4_OK) return s;
+      if (t > 0 && (s = wait_peers(c, st, c->sym_ring, 0, {prev}, val(t - 1), "wait_ring")) != SDP4_OK) return s;
       if ((s = hop((r - t - 1 + 2 * P) % P, t ? slot(r, t - 1) : nullptr, slot(next, t), nullptr)) != SDP4_OK)
         return s;
       if ((s = signal_peers(c, st, c->sym_ring, 0, {next}, val(t))) != SDP4_OK) return s;
     }
-    if ((s = wait_peers(c, st, c->sym_ring, 0, {prev}, val(P - 2))) != SDP4_OK) return s;
+    if ((s = wait_peers(c, st, c->sym_ring, 0, {prev}, val(P - 2), "wait_ring")) != SDP4_OK) return s;
     return hop(r, slot(r, P - 2), nullptr, out_shard);
   }
   uint8_t* send = static_cast<uint8_t*>(workspace);

@@ -754,11 +754,15 @@ __device__ __forceinline__ void k2_apply(const uint4* cw, float sc, uint4* mw, T
 
 template <typename TM, int BITS, bool ADD>
 __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply(const Dests units, size_t S, size_t stride, int P,
-                                                               int lg, TM* __restrict__ w_model, float z) {
+                                                               int rot, int lg, TM* __restrict__ w_model, float z) {
   constexpr int TILE = kVecThreads * 32;
   const size_t tpu = (S + TILE - 1) / TILE;
+  // unit index fastest and rotated by this rank: at any moment every rank pulls from every
+  // source, instead of all ranks draining the same source's NVLink port together
   for (size_t tile = blockIdx.x; tile < tpu * P; tile += gridDim.x) {
-    const size_t j = tile / tpu, ts = tile - j * tpu;
+    const size_t ts = tile / P;
+    size_t j = tile - ts * P + rot;
+    if (j >= (size_t)P) j -= P;
     const uint8_t* unit = units.p[j];  // unit j: local, or rank j's own buffer (P2P pull over NVLink)
     const float* scales = reinterpret_cast<const float*>(unit + S * (BITS == 32 ? 4 : BITS) / 8);
     TM* wm = w_model + j * stride;
@@ -1564,10 +1568,10 @@ cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, 
 }
 
 cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride, int bits, int G, void* w_model,
-                             int model_dtype, bool add, int sms, cudaStream_t st) {
+                             int model_dtype, bool add, int sms, cudaStream_t st, int rot) {
   const int grid = grid_for((S + kVecThreads * 32 - 1) / (kVecThreads * 32) * P, sms * kVecCtas);
 #define K2(TM, B, AD)                                                                              \
-  k2_qwd_apply<TM, B, AD><<<grid, kVecThreads, 0, st>>>(units, S, stride, P, __builtin_ctz(G), \
+  k2_qwd_apply<TM, B, AD><<<grid, kVecThreads, 0, st>>>(units, S, stride, P, rot % P, __builtin_ctz(G), \
                                                         static_cast<TM*>(w_model), -0.0f)
 #define K2B(TM, AD) \
   if (bits == 2) K2(TM, 2, AD); else if (bits == 4) K2(TM, 4, AD); else if (bits == 8) K2(TM, 8, AD); else K2(TM, 32, AD)

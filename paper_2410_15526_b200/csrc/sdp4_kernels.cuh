@@ -37,8 +37,9 @@ cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, 
 
 // K2: Alg. 2 l.5 -- for every shard j < P: w_model[j*stride ..+S] += dequant(unit units.p[j])
 // (local or peer memory), in place.  add = false (qW): w_model[...] = dequant(unit), no read.
+// Tiles are visited unit-fastest, starting at unit `rot` (this rank: spreads the P2P pulls).
 cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride, int bits, int G, void* w_model,
-                             int model_dtype, bool add, int sms, cudaStream_t st);
+                             int model_dtype, bool add, int sms, cudaStream_t st, int rot = 0);
 
 // K6: one hop of the ring reduce-scatter with per-hop quantization (sec. 2.3, ablation):
 // acc = (recv ? rn(dequant(recv) + g) : g) over S elements of one chunk (grad dtype);
