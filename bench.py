@@ -55,7 +55,7 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-comparators", action="store_true")
     p.add_argument("--intra-pull", type=str, default=None,
-                   help="P2P: num/den of the intra all-to-all pulled by K4 (default: the library's 1/2)")
+                   help="P2P: num/den of the intra all-to-all pulled by K4 (default: the library's auto split)")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle timing")
     return p.parse_args()
 
@@ -147,7 +147,7 @@ def kernel_nvlink_bytes(name, D, S, P, M, N, a, transport):
         return n * k / 8 + (4 * n / G if k != 32 else 0)
     if name.startswith("K2"):
         return (P - 1) * wire(S, a.bits_w, a.qwd_group)
-    num, den = [int(x) for x in (a.intra_pull or "1/2").split("/")]
+    num, den = [int(x) for x in (a.intra_pull or ("0/1" if N <= 2 else "1/2")).split("/")]   # library default
     f = num / den if N > 1 else 0.0                      # share of intra tiles K4 pulls
     intra = (N - 1) * M * wire(S, a.bits_intra, a.group)
     if name.startswith("K3"):                            # pushed intra tiles (egress)
@@ -470,7 +470,7 @@ def run_sdp4(a, rank, world, local_rank):
                 "config": {"workload": workload, "D": D, "D_unpadded": D0, "M": M, "N": N, "G": a.group,
                            "pipeline_chunks": comm.chunks(D, a.group),
                            "transport": comm.transport if world > 1 else "local",
-                           "intra_pull": a.intra_pull or "1/2",
+                           "intra_pull": a.intra_pull or ("auto: " + ("0/1" if N <= 2 else "1/2")),
                            "G_w": a.qwd_group, "hadamard_block": a.hadamard,
                            "bits": {"qwd": a.bits_w, "intra": a.bits_intra, "inter": a.bits_inter},
                            "grad_dtype": a.grad_dtype, "model_dtype": a.model_dtype,

@@ -110,8 +110,9 @@ int sdp4_comm_transport(sdp4_comm_t comm);
  * tile_index % den < num are PULLED -- K3 stores them into this rank's own outbox and K4 on
  * the destination bulk-loads them over NVLink -- and the rest are PUSHED by K3 into the
  * destination's receive block.  Splitting the bytes between the two kernels overlaps them
- * with both kernels' HBM streams.  num = 0: push only.  Default 1/2.  Results do not depend
- * on the split (R16).  EINVAL unless 0 <= num <= den, 1 <= den <= 64. */
+ * with both kernels' HBM streams.  num = 0: push only.  Default (never set): push only when
+ * N = 2, 1/2 for N >= 3 (measured).  Results do not depend on the split
+ * (R16).  EINVAL unless 0 <= num <= den, 1 <= den <= 64. */
 sdp4_status sdp4_comm_set_intra_pull(sdp4_comm_t comm, int num, int den);
 
 /* Host, collective.  Destroys the NCCL communicators and frees the comm. */

@@ -140,7 +140,7 @@ struct sdp4_comm {
   int sm_count = 148;
   int nccl_ctas = kDefaultNcclCtas;
   int chunks_cfg = 0;  // 0 = auto
-  int pull_num = 1, pull_den = 2;  // P2P intra all-to-all: share of peer tiles pulled by K4 (IntraPull)
+  int pull_num = -1, pull_den = 2;  // P2P intra all-to-all: share of peer tiles pulled by K4 (IntraPull); -1 = auto
   ncclComm_t world_c = nullptr, intra = nullptr, inter = nullptr;
   cudaStream_t side = nullptr;
   uint64_t launches = 0;
@@ -762,7 +762,10 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     // Symmetric region: [intra receive: N blocks][inter receive: M units][outbox: N blocks].
     const size_t w8 = unit_bytes(S, bits_intra, group), w4 = unit_bytes(S, bits_inter, group);
     const size_t intra_bytes = (size_t)N * M * w8, inter_bytes = (size_t)M * w4;
-    const bool pulling = N > 1 && c->pull_num > 0;
+    // auto split (measured): push only with two local ranks, half pulled beyond
+    const int pnum = c->pull_num >= 0 ? c->pull_num : (N <= 2 ? 0 : 1);
+    const int pden = c->pull_num >= 0 ? c->pull_den : 2;
+    const bool pulling = N > 1 && pnum > 0;
     const size_t outbox_off = intra_bytes + inter_bytes;
     if ((s = sym_ensure(c, c->sym_tlq, outbox_off + (pulling ? intra_bytes : 0), &c->epoch_tlq)) != SDP4_OK) return s;
     const uint32_t ep = ++c->epoch_tlq;
@@ -777,8 +780,8 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     sdp4::IntraPull pull;
     memset(&pull, 0, sizeof(pull));
     pull.mask = pulling ? remote : 0u;
-    pull.num = pulling ? c->pull_num : 0;
-    pull.den = c->pull_den;
+    pull.num = pulling ? pnum : 0;
+    pull.den = pden;
     for (int lp = 0; lp < N; ++lp) {
       pull.outbox[lp] = sym_region(c->sym_tlq, c->rank, ep) + outbox_off + (size_t)lp * M * w8;  // mine, for l'
       pull.src[lp] = sym_region(c->sym_tlq, m * N + lp, ep) + outbox_off + (size_t)l * M * w8;   // l''s, for me
