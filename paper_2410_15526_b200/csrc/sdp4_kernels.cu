@@ -658,122 +658,93 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
 // for every shard j (w_model shard j at w_model + j*stride), unit j read through units.p[j]:
 // the gathered local copy (NCCL transport) or, with the P2P transport, rank j's own buffer
 // over NVLink -- the all-gather (Alg. 2 l.4) fused into the consumer as a pull, so the
-// NVLink ingress overlaps the HBM-bound replica update.  Each thread updates two 16-element
-// vectors per tile, all loads issued up front.  ADD = false is the qW ablation codec
-// (Alg. 1): the replica becomes the dequantized weights, w_model = dtype_rn(x^).
+// NVLink ingress overlaps the HBM-bound replica update.  K1's layout: 8 elements per thread
+// (one 16-byte replica vector), few registers, full occupancy.  ADD = false is the qW
+// ablation codec (Alg. 1): the replica becomes the dequantized weights.
 // =====================================================================================
-template <int BITS>
-struct K2Vec {
-  static constexpr int CB = BITS == 32 ? 64 : 16 * BITS / 8;  // code bytes per 16 elements
-};
-
-template <typename TM, int BITS, bool ADD>
-__device__ __forceinline__ void k2_load(const uint8_t* unit, const float* scales, const TM* wm, size_t e, int lg,
-                                        uint4* cw, float& sc, uint4* mw) {
-  if constexpr (BITS == 32) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) cw[i] = *reinterpret_cast<const uint4*>(unit + e * 4 + 16 * i);
-  } else if constexpr (BITS == 8) {
-    cw[0] = *reinterpret_cast<const uint4*>(unit + e);
-    sc = scales[e >> lg];
-  } else if constexpr (BITS == 4) {
-    const uint2 w = *reinterpret_cast<const uint2*>(unit + e / 2);
-    cw[0] = make_uint4(w.x, w.y, 0u, 0u);
-    sc = scales[e >> lg];
-  } else {
-    cw[0] = make_uint4(*reinterpret_cast<const uint32_t*>(unit + e / 4), 0u, 0u, 0u);
-    sc = scales[e >> lg];
-  }
-  if constexpr (!ADD) {
-    return;
-  } else if constexpr (sizeof(TM) == 2) {
-    mw[0] = *reinterpret_cast<const uint4*>(wm + e);
-    mw[1] = *reinterpret_cast<const uint4*>(wm + e + 8);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) mw[i] = *reinterpret_cast<const uint4*>(wm + e + 4 * i);
-  }
-}
-
-template <typename TM, int BITS, bool ADD>
-__device__ __forceinline__ void k2_apply(const uint4* cw, float sc, uint4* mw, TM* wm, size_t e, float z) {
-  constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
-  float x[16];
-  if constexpr (BITS == 32) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      x[4 * i] = __uint_as_float(cw[i].x); x[4 * i + 1] = __uint_as_float(cw[i].y);
-      x[4 * i + 2] = __uint_as_float(cw[i].z); x[4 * i + 3] = __uint_as_float(cw[i].w);
-    }
-  } else {
-    const float ds = __fdiv_rn(sc, q);
-    float f[16];
-    if constexpr (BITS == 2) {
-      dec2x16(cw[0].x, f);
-    } else if constexpr (BITS == 4) {
-      dec4x8(cw[0].x, f);
-      dec4x8(cw[0].y, f + 8);
-    } else {
-      dec8x4(cw[0].x, f); dec8x4(cw[0].y, f + 4); dec8x4(cw[0].z, f + 8); dec8x4(cw[0].w, f + 12);
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) x[i] = mulz(f[i], ds, z);  // the product is added next: fusion barrier
-  }
-  if constexpr (!ADD) {
-    if constexpr (sizeof(TM) == 2) {
-      uint4 o[2];
-      uint32_t* w = &o[0].x;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = pack_bf16x2(x[2 * i], x[2 * i + 1]);
-      reinterpret_cast<uint4*>(wm + e)[0] = o[0];
-      reinterpret_cast<uint4*>(wm + e + 8)[0] = o[1];
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        reinterpret_cast<float4*>(wm + e + 4 * i)[0] = make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
-    }
-  } else if constexpr (sizeof(TM) == 2) {
-    uint32_t* w = &mw[0].x;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      w[i] = pack_bf16x2(__fadd_rn(bf16_lo(w[i]), x[2 * i]), __fadd_rn(bf16_hi(w[i]), x[2 * i + 1]));
-    reinterpret_cast<uint4*>(wm + e)[0] = mw[0];
-    reinterpret_cast<uint4*>(wm + e + 8)[0] = mw[1];
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float4 t;
-      t.x = __fadd_rn(__uint_as_float(mw[i].x), x[4 * i]);
-      t.y = __fadd_rn(__uint_as_float(mw[i].y), x[4 * i + 1]);
-      t.z = __fadd_rn(__uint_as_float(mw[i].z), x[4 * i + 2]);
-      t.w = __fadd_rn(__uint_as_float(mw[i].w), x[4 * i + 3]);
-      reinterpret_cast<float4*>(wm + e + 4 * i)[0] = t;
-    }
-  }
-}
-
 template <typename TM, int BITS, bool ADD>
 __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply(const Dests units, size_t S, size_t stride, int P,
                                                                int rot, int lg, TM* __restrict__ w_model, float z) {
-  constexpr int TILE = kVecThreads * 32;
+  constexpr int TILE = kVecThreads * 8;
+  constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
   const size_t tpu = (S + TILE - 1) / TILE;
+  const size_t sc_off = S * (BITS == 32 ? 4 : BITS) / 8;
   // unit index fastest and rotated by this rank: at any moment every rank pulls from every
   // source, instead of all ranks draining the same source's NVLink port together
   for (size_t tile = blockIdx.x; tile < tpu * P; tile += gridDim.x) {
     const size_t ts = tile / P;
     size_t j = tile - ts * P + rot;
     if (j >= (size_t)P) j -= P;
+    const size_t e = ts * TILE + threadIdx.x * 8;
+    if (e >= S) continue;
     const uint8_t* unit = units.p[j];  // unit j: local, or rank j's own buffer (P2P pull over NVLink)
-    const float* scales = reinterpret_cast<const float*>(unit + S * (BITS == 32 ? 4 : BITS) / 8);
     TM* wm = w_model + j * stride;
-    const size_t ea = ts * TILE + threadIdx.x * 16, eb = ea + TILE / 2;
-    uint4 ca[4], cb[4], ma[4], mb[4];
-    float sa = 0.f, sb = 0.f;
-    const bool aa = ea < S, ab = eb < S;
-    if (aa) k2_load<TM, BITS, ADD>(unit, scales, wm, ea, lg, ca, sa, ma);
-    if (ab) k2_load<TM, BITS, ADD>(unit, scales, wm, eb, lg, cb, sb, mb);
-    if (aa) k2_apply<TM, BITS, ADD>(ca, sa, ma, wm, ea, z);
-    if (ab) k2_apply<TM, BITS, ADD>(cb, sb, mb, wm, eb, z);
+    // ---- loads (all issued before any use)
+    uint4 cw0 = make_uint4(0u, 0u, 0u, 0u), cw1 = make_uint4(0u, 0u, 0u, 0u);
+    float sc = 0.f;
+    if constexpr (BITS == 32) {
+      cw0 = *reinterpret_cast<const uint4*>(unit + e * 4);
+      cw1 = *reinterpret_cast<const uint4*>(unit + e * 4 + 16);
+    } else {
+      if constexpr (BITS == 8) {
+        const uint2 w = *reinterpret_cast<const uint2*>(unit + e);
+        cw0.x = w.x;
+        cw0.y = w.y;
+      } else if constexpr (BITS == 4) {
+        cw0.x = *reinterpret_cast<const uint32_t*>(unit + e / 2);
+      } else {
+        cw0.x = *reinterpret_cast<const uint16_t*>(unit + e / 4);
+      }
+      sc = reinterpret_cast<const float*>(unit + sc_off)[e >> lg];
+    }
+    uint4 m0 = make_uint4(0u, 0u, 0u, 0u), m1 = make_uint4(0u, 0u, 0u, 0u);
+    if constexpr (ADD) {
+      m0 = *reinterpret_cast<const uint4*>(wm + e);
+      if constexpr (sizeof(TM) == 4) m1 = *reinterpret_cast<const uint4*>(wm + e + 4);
+    }
+    // ---- dequantize x^ = rn(code * rn(s / q)) (R5)
+    float x[8];
+    if constexpr (BITS == 32) {
+      x[0] = __uint_as_float(cw0.x); x[1] = __uint_as_float(cw0.y); x[2] = __uint_as_float(cw0.z);
+      x[3] = __uint_as_float(cw0.w); x[4] = __uint_as_float(cw1.x); x[5] = __uint_as_float(cw1.y);
+      x[6] = __uint_as_float(cw1.z); x[7] = __uint_as_float(cw1.w);
+    } else {
+      float f[8];
+      if constexpr (BITS == 8) {
+        dec8x4(cw0.x, f);
+        dec8x4(cw0.y, f + 4);
+      } else if constexpr (BITS == 4) {
+        dec4x8(cw0.x, f);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = float((int)(((cw0.x >> (2 * i)) & 3u) ^ 2u) - 2);
+      }
+      const float ds = __fdiv_rn(sc, q);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = ADD ? mulz(f[i], ds, z) : __fmul_rn(f[i], ds);  // added next: barrier
+    }
+    // ---- apply (R11): bf16_rn(widen(w) + x^), fp32 add for fp32 replicas; qW assigns
+    if constexpr (sizeof(TM) == 2) {
+      uint32_t* w = &m0.x;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        w[i] = ADD ? pack_bf16x2(__fadd_rn(bf16_lo(w[i]), x[2 * i]), __fadd_rn(bf16_hi(w[i]), x[2 * i + 1]))
+                   : pack_bf16x2(x[2 * i], x[2 * i + 1]);
+      *reinterpret_cast<uint4*>(wm + e) = m0;
+    } else {
+      float4 a, b;
+      if constexpr (ADD) {
+        a = make_float4(__fadd_rn(__uint_as_float(m0.x), x[0]), __fadd_rn(__uint_as_float(m0.y), x[1]),
+                        __fadd_rn(__uint_as_float(m0.z), x[2]), __fadd_rn(__uint_as_float(m0.w), x[3]));
+        b = make_float4(__fadd_rn(__uint_as_float(m1.x), x[4]), __fadd_rn(__uint_as_float(m1.y), x[5]),
+                        __fadd_rn(__uint_as_float(m1.z), x[6]), __fadd_rn(__uint_as_float(m1.w), x[7]));
+      } else {
+        a = make_float4(x[0], x[1], x[2], x[3]);
+        b = make_float4(x[4], x[5], x[6], x[7]);
+      }
+      reinterpret_cast<float4*>(wm + e)[0] = a;
+      reinterpret_cast<float4*>(wm + e + 4)[0] = b;
+    }
   }
 }
 
@@ -1569,7 +1540,7 @@ cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, 
 
 cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride, int bits, int G, void* w_model,
                              int model_dtype, bool add, int sms, cudaStream_t st, int rot) {
-  const int grid = grid_for((S + kVecThreads * 32 - 1) / (kVecThreads * 32) * P, sms * kVecCtas);
+  const int grid = grid_for((S + kVecThreads * 8 - 1) / (kVecThreads * 8) * P, sms * kVecCtas);
 #define K2(TM, B, AD)                                                                              \
   k2_qwd_apply<TM, B, AD><<<grid, kVecThreads, 0, st>>>(units, S, stride, P, rot % P, __builtin_ctz(G), \
                                                         static_cast<TM*>(w_model), -0.0f)

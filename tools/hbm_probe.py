@@ -36,6 +36,13 @@ def main():
     big = x.view(8, n // 8)
     ms = t(lambda: big.copy_(small.expand(8, n // 8)))
     res["read1_write8_GBps"] = (4 * n // 8 + 4 * n) / ms / 1e6
+    # in-place read-modify-write of a bf16 buffer (K2's replica pattern) vs a bf16 copy
+    wb = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    wb2 = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    ms = t(lambda: wb.add_(1.0))
+    res["bf16_inplace_rmw_GBps"] = 4 * n / ms / 1e6
+    ms = t(lambda: wb2.copy_(wb))
+    res["bf16_copy_GBps"] = 4 * n / ms / 1e6
     print(json.dumps({k: round(v, 1) for k, v in res.items()}))
 
 
