@@ -120,7 +120,7 @@ size_t qwd_total(int P, size_t S, int bits, int group, int C) {
 
 // Library-owned receive buffer, mapped on every rank (CUDA IPC).  Layout:
 // [flags: kFlagBytes][parity 0 region][parity 1 region].
-constexpr size_t kFlagBytes = 4096;  // flags[stage][src] uint32, stage < 4, src < 256
+constexpr size_t kFlagBytes = 64 * 256 * 4;  // flags[stage][src] uint32, stage < 64, src < 256
 struct SymBuf {
   uint8_t* local = nullptr;
   size_t bytes = 0, region = 0;
@@ -177,8 +177,9 @@ struct sdp4_comm {
     cudaStreamWaitEvent(to, e, 0);
   }
   int chunks(size_t S) const {
-    if (world == 1 || transport == kTransportP2P) return 1;
+    if (world == 1) return 1;
     if (chunks_cfg > 0) return std::min(chunks_cfg, kMaxChunks);
+    if (transport == kTransportP2P) return 1;
     const size_t c = S / ((size_t)16 << 20);  // ~16M elements per chunk and shard
     return (int)std::max<size_t>(1, std::min<size_t>(c, 8));
   }
@@ -668,7 +669,7 @@ sdp4_status weight_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes,
     if ((s = wait_peers(c, st, c->sym_qwd, 0, all, ep, "wait_qwd_allgather")) != SDP4_OK) return s;
     sdp4::Dests u;
     u.n = P;
-    u.remote = 0;
+    u.remote = P > 1 ? (uint32_t)(((uint64_t)1 << std::min(P, 32)) - 1) & ~(1u << (c->rank & 31)) : 0u;  // peers
     for (int q = 0; q < P; ++q) u.p[q] = sym_region(c->sym_qwd, q, ep);
     return launch(c, kname, st, [&] {
       return sdp4::launch_qwd_apply(u, P, S, S, bits, group, w_model_full, model_dtype, add, c->sm_count, st,
@@ -758,59 +759,76 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
   const uint32_t key8 = sr_key(seed, kStageIntra, c->rank), key4 = sr_key(seed, kStageInter, c->rank);
   if (c->transport == kTransportP2P) {
     // Alg. 3 with both all-to-alls fused into the producing kernels: the intra one (l.4) split
-    // between K3 pushes and K4 pulls (IntraPull), the inter one (l.10) pushed by K4.
-    // Symmetric region: [intra receive: N blocks][inter receive: M units][outbox: N blocks].
-    const size_t w8 = unit_bytes(S, bits_intra, group), w4 = unit_bytes(S, bits_inter, group);
-    const size_t intra_bytes = (size_t)N * M * w8, inter_bytes = (size_t)M * w4;
-    // auto split (measured): push only with two local ranks, half pulled beyond
-    const int pnum = c->pull_num >= 0 ? c->pull_num : (N <= 2 ? 0 : 1);
+    // between K3 pushes and K4 pulls (IntraPull), the inter one (l.10) pushed by K4.  With
+    // C > 1 chunks (sub-ranges of every shard, independent end to end) the chunks alternate
+    // between the caller's stream and the side stream, so K4/K5 of chunk k overlap the
+    // NVLink-bound K3 of chunk k+1 (the overlap of P:344).  Symmetric region, per chunk:
+    // [intra receive: N blocks][inter receive: M units][outbox: N blocks].
+    const int pnum = c->pull_num >= 0 ? c->pull_num : (N <= 2 ? 0 : 1);  // auto split
     const int pden = c->pull_num >= 0 ? c->pull_den : 2;
     const bool pulling = N > 1 && pnum > 0;
-    const size_t outbox_off = intra_bytes + inter_bytes;
-    if ((s = sym_ensure(c, c->sym_tlq, outbox_off + (pulling ? intra_bytes : 0), &c->epoch_tlq)) != SDP4_OK) return s;
+    if (C > kMaxChunks) return fail(SDP4_EINVAL, "too many chunks");
+    std::vector<size_t> base(C + 1, 0);
+    for (int k = 0; k < C; ++k) {
+      const size_t w8 = unit_bytes(chunks[k].len, bits_intra, group), w4 = unit_bytes(chunks[k].len, bits_inter, group);
+      base[k + 1] = base[k] + (size_t)N * M * w8 * (pulling ? 2 : 1) + (size_t)M * w4;
+    }
+    if ((s = sym_ensure(c, c->sym_tlq, base[C], &c->epoch_tlq)) != SDP4_OK) return s;
     const uint32_t ep = ++c->epoch_tlq;
     const int m = c->m, l = c->l;
     std::vector<int> group_ranks(N), node_ranks(M);
     for (int q = 0; q < N; ++q) group_ranks[q] = m * N + q;
     for (int q = 0; q < M; ++q) node_ranks[q] = q * N + l;
-    // K3: shard m'N + l' -> unit m' of block l (this rank) in rank (m, l')'s intra receive region
-    uint8_t* blocks[sdp4::kMaxN];
-    for (int lp = 0; lp < N; ++lp) blocks[lp] = sym_region(c->sym_tlq, m * N + lp, ep) + (size_t)l * M * w8;
     const uint32_t remote = ((1u << N) - 1u) & ~(1u << l);
-    sdp4::IntraPull pull;
-    memset(&pull, 0, sizeof(pull));
-    pull.mask = pulling ? remote : 0u;
-    pull.num = pulling ? pnum : 0;
-    pull.den = pden;
-    for (int lp = 0; lp < N; ++lp) {
-      pull.outbox[lp] = sym_region(c->sym_tlq, c->rank, ep) + outbox_off + (size_t)lp * M * w8;  // mine, for l'
-      pull.src[lp] = sym_region(c->sym_tlq, m * N + lp, ep) + outbox_off + (size_t)l * M * w8;   // l''s, for me
+    if (C > 1) c->link(st, c->side);
+    for (int k = 0; k < C; ++k) {
+      const Chunk& ch = chunks[k];
+      cudaStream_t sk = (k & 1) ? c->side : st;
+      const size_t w8 = unit_bytes(ch.len, bits_intra, group), w4 = unit_bytes(ch.len, bits_inter, group);
+      const size_t intra_bytes = (size_t)N * M * w8, outbox_off = intra_bytes + (size_t)M * w4;
+      auto region = [&](int rank) { return sym_region(c->sym_tlq, rank, ep) + base[k]; };
+      // K3: shard m'N + l' -> unit m' of block l (this rank) in rank (m, l')'s intra receive region
+      uint8_t* blocks[sdp4::kMaxN];
+      for (int lp = 0; lp < N; ++lp) blocks[lp] = region(m * N + lp) + (size_t)l * M * w8;
+      sdp4::IntraPull pull;
+      memset(&pull, 0, sizeof(pull));
+      pull.mask = pulling ? remote : 0u;
+      pull.num = pulling ? pnum : 0;
+      pull.den = pden;
+      for (int lp = 0; lp < N; ++lp) {
+        pull.outbox[lp] = region(c->rank) + outbox_off + (size_t)lp * M * w8;  // mine, for l'
+        pull.src[lp] = region(m * N + lp) + outbox_off + (size_t)l * M * w8;   // l''s, for me
+      }
+      s = launch(c, "K3_tlq_had_quant", sk, [&] {
+        return sdp4::launch_tlq_had_quant(static_cast<const uint8_t*>(grad) + ch.off * es, S, grad_dtype, ch.len, M, N,
+                                          group, b, cb, bits_intra, blocks, remote, w8, sr, key8, ch.off, c->sm_count,
+                                          sk, &pull);
+      });
+      if (s != SDP4_OK) return s;
+      const int st_intra = 1 + 2 * k, st_inter = 2 + 2 * k;  // flag slots of chunk k
+      if ((s = signal_peers(c, sk, c->sym_tlq, st_intra, group_ranks, ep)) != SDP4_OK) return s;
+      if ((s = wait_peers(c, sk, c->sym_tlq, st_intra, group_ranks, ep, "wait_tlq_intra")) != SDP4_OK) return s;
+      // K4: unit m' -> slot m (this node) of rank (m', l)'s inter receive region
+      sdp4::Dests d4;
+      d4.n = M;
+      d4.remote = ((1u << M) - 1u) & ~(1u << m);
+      for (int mp = 0; mp < M; ++mp) d4.p[mp] = region(mp * N + l) + intra_bytes + (size_t)m * w4;
+      uint8_t* my = region(c->rank);
+      s = launch(c, "K4_tlq_dq_reduce_q", sk, [&] {
+        return sdp4::launch_tlq_dq_reduce_q(my, w8, bits_intra, N, M, ch.len, group, d4, bits_inter, sr, key4, l, S,
+                                            ch.off, c->sm_count, sk, &pull);
+      });
+      if (s != SDP4_OK) return s;
+      if ((s = signal_peers(c, sk, c->sym_tlq, st_inter, node_ranks, ep)) != SDP4_OK) return s;
+      if ((s = wait_peers(c, sk, c->sym_tlq, st_inter, node_ranks, ep, "wait_tlq_inter")) != SDP4_OK) return s;
+      s = launch(c, "K5_tlq_dq_reduce_had", sk, [&] {
+        return sdp4::launch_tlq_dq_reduce_had(my + intra_bytes, w4, bits_inter, M, ch.len, group, b, kappa,
+                                              out_shard + ch.off, c->sm_count, sk);
+      });
+      if (s != SDP4_OK) return s;
     }
-    s = launch(c, "K3_tlq_had_quant", st, [&] {
-      return sdp4::launch_tlq_had_quant(grad, S, grad_dtype, S, M, N, group, b, cb, bits_intra, blocks, remote, w8,
-                                        sr, key8, 0, c->sm_count, st, &pull);
-    });
-    if (s != SDP4_OK) return s;
-    if ((s = signal_peers(c, st, c->sym_tlq, 1, group_ranks, ep)) != SDP4_OK) return s;
-    if ((s = wait_peers(c, st, c->sym_tlq, 1, group_ranks, ep, "wait_tlq_intra")) != SDP4_OK) return s;
-    // K4: unit m' -> slot m (this node) of rank (m', l)'s inter receive region
-    sdp4::Dests d4;
-    d4.n = M;
-    d4.remote = ((1u << M) - 1u) & ~(1u << m);
-    for (int mp = 0; mp < M; ++mp)
-      d4.p[mp] = sym_region(c->sym_tlq, mp * N + l, ep) + intra_bytes + (size_t)m * w4;
-    uint8_t* my = sym_region(c->sym_tlq, c->rank, ep);
-    s = launch(c, "K4_tlq_dq_reduce_q", st, [&] {
-      return sdp4::launch_tlq_dq_reduce_q(my, w8, bits_intra, N, M, S, group, d4, bits_inter, sr, key4, l, S, 0,
-                                          c->sm_count, st, &pull);
-    });
-    if (s != SDP4_OK) return s;
-    if ((s = signal_peers(c, st, c->sym_tlq, 2, node_ranks, ep)) != SDP4_OK) return s;
-    if ((s = wait_peers(c, st, c->sym_tlq, 2, node_ranks, ep, "wait_tlq_inter")) != SDP4_OK) return s;
-    return launch(c, "K5_tlq_dq_reduce_had", st, [&] {
-      return sdp4::launch_tlq_dq_reduce_had(my + intra_bytes, w4, bits_inter, M, S, group, b, kappa, out_shard,
-                                            c->sm_count, st);
-    });
+    if (C > 1) c->link(c->side, st);
+    return SDP4_OK;
   }
   std::vector<TlqRegions> reg;
   size_t base = 0;

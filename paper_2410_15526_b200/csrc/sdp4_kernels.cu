@@ -748,6 +748,124 @@ __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply(const Dests units, s
   }
 }
 
+// K2 for the P2P transport (units read over NVLink): two 16-element vectors per thread, so
+// each thread has 16 code bytes of remote loads in flight (a warp pulls 2 x 256 contiguous
+// bytes) -- measured faster than the 8-element layout once 3/4 of the codes come from peers.
+template <int BITS>
+struct K2Vec {
+  static constexpr int CB = BITS == 32 ? 64 : 16 * BITS / 8;  // code bytes per 16 elements
+};
+
+template <typename TM, int BITS, bool ADD>
+__device__ __forceinline__ void k2p_load(const uint8_t* unit, const float* scales, const TM* wm, size_t e, int lg,
+                                        uint4* cw, float& sc, uint4* mw) {
+  if constexpr (BITS == 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cw[i] = *reinterpret_cast<const uint4*>(unit + e * 4 + 16 * i);
+  } else if constexpr (BITS == 8) {
+    cw[0] = *reinterpret_cast<const uint4*>(unit + e);
+    sc = scales[e >> lg];
+  } else if constexpr (BITS == 4) {
+    const uint2 w = *reinterpret_cast<const uint2*>(unit + e / 2);
+    cw[0] = make_uint4(w.x, w.y, 0u, 0u);
+    sc = scales[e >> lg];
+  } else {
+    cw[0] = make_uint4(*reinterpret_cast<const uint32_t*>(unit + e / 4), 0u, 0u, 0u);
+    sc = scales[e >> lg];
+  }
+  if constexpr (!ADD) {
+    return;
+  } else if constexpr (sizeof(TM) == 2) {
+    mw[0] = *reinterpret_cast<const uint4*>(wm + e);
+    mw[1] = *reinterpret_cast<const uint4*>(wm + e + 8);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mw[i] = *reinterpret_cast<const uint4*>(wm + e + 4 * i);
+  }
+}
+
+template <typename TM, int BITS, bool ADD>
+__device__ __forceinline__ void k2p_apply(const uint4* cw, float sc, uint4* mw, TM* wm, size_t e, float z) {
+  constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
+  float x[16];
+  if constexpr (BITS == 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      x[4 * i] = __uint_as_float(cw[i].x); x[4 * i + 1] = __uint_as_float(cw[i].y);
+      x[4 * i + 2] = __uint_as_float(cw[i].z); x[4 * i + 3] = __uint_as_float(cw[i].w);
+    }
+  } else {
+    const float ds = __fdiv_rn(sc, q);
+    float f[16];
+    if constexpr (BITS == 2) {
+      dec2x16(cw[0].x, f);
+    } else if constexpr (BITS == 4) {
+      dec4x8(cw[0].x, f);
+      dec4x8(cw[0].y, f + 8);
+    } else {
+      dec8x4(cw[0].x, f); dec8x4(cw[0].y, f + 4); dec8x4(cw[0].z, f + 8); dec8x4(cw[0].w, f + 12);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = mulz(f[i], ds, z);  // the product is added next: fusion barrier
+  }
+  if constexpr (!ADD) {
+    if constexpr (sizeof(TM) == 2) {
+      uint4 o[2];
+      uint32_t* w = &o[0].x;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = pack_bf16x2(x[2 * i], x[2 * i + 1]);
+      reinterpret_cast<uint4*>(wm + e)[0] = o[0];
+      reinterpret_cast<uint4*>(wm + e + 8)[0] = o[1];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        reinterpret_cast<float4*>(wm + e + 4 * i)[0] = make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
+    }
+  } else if constexpr (sizeof(TM) == 2) {
+    uint32_t* w = &mw[0].x;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      w[i] = pack_bf16x2(__fadd_rn(bf16_lo(w[i]), x[2 * i]), __fadd_rn(bf16_hi(w[i]), x[2 * i + 1]));
+    reinterpret_cast<uint4*>(wm + e)[0] = mw[0];
+    reinterpret_cast<uint4*>(wm + e + 8)[0] = mw[1];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float4 t;
+      t.x = __fadd_rn(__uint_as_float(mw[i].x), x[4 * i]);
+      t.y = __fadd_rn(__uint_as_float(mw[i].y), x[4 * i + 1]);
+      t.z = __fadd_rn(__uint_as_float(mw[i].z), x[4 * i + 2]);
+      t.w = __fadd_rn(__uint_as_float(mw[i].w), x[4 * i + 3]);
+      reinterpret_cast<float4*>(wm + e + 4 * i)[0] = t;
+    }
+  }
+}
+
+template <typename TM, int BITS, bool ADD>
+__global__ void __launch_bounds__(kVecThreads) k2_qwd_apply_pull(const Dests units, size_t S, size_t stride, int P,
+                                                               int rot, int lg, TM* __restrict__ w_model, float z) {
+  constexpr int TILE = kVecThreads * 32;
+  const size_t tpu = (S + TILE - 1) / TILE;
+  // unit index fastest and rotated by this rank: at any moment every rank pulls from every
+  // source, instead of all ranks draining the same source's NVLink port together
+  for (size_t tile = blockIdx.x; tile < tpu * P; tile += gridDim.x) {
+    const size_t ts = tile / P;
+    size_t j = tile - ts * P + rot;
+    if (j >= (size_t)P) j -= P;
+    const uint8_t* unit = units.p[j];  // unit j: local, or rank j's own buffer (P2P pull over NVLink)
+    const float* scales = reinterpret_cast<const float*>(unit + S * (BITS == 32 ? 4 : BITS) / 8);
+    TM* wm = w_model + j * stride;
+    const size_t ea = ts * TILE + threadIdx.x * 16, eb = ea + TILE / 2;
+    uint4 ca[4], cb[4], ma[4], mb[4];
+    float sa = 0.f, sb = 0.f;
+    const bool aa = ea < S, ab = eb < S;
+    if (aa) k2p_load<TM, BITS, ADD>(unit, scales, wm, ea, lg, ca, sa, ma);
+    if (ab) k2p_load<TM, BITS, ADD>(unit, scales, wm, eb, lg, cb, sb, mb);
+    if (aa) k2p_apply<TM, BITS, ADD>(ca, sa, ma, wm, ea, z);
+    if (ab) k2p_apply<TM, BITS, ADD>(cb, sb, mb, wm, eb, z);
+  }
+}
+
 // =====================================================================================
 // K6  one hop of the ring reduce-scatter with per-hop quantization (sec. 2.3) -- the
 // ablation baseline TLq-HS is measured against.  acc = rn(dequant(recv) + g) (RECV) or g;
@@ -1541,9 +1659,16 @@ cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, 
 cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride, int bits, int G, void* w_model,
                              int model_dtype, bool add, int sms, cudaStream_t st, int rot) {
   const int grid = grid_for((S + kVecThreads * 8 - 1) / (kVecThreads * 8) * P, sms * kVecCtas);
-#define K2(TM, B, AD)                                                                              \
-  k2_qwd_apply<TM, B, AD><<<grid, kVecThreads, 0, st>>>(units, S, stride, P, rot % P, __builtin_ctz(G), \
-                                                        static_cast<TM*>(w_model), -0.0f)
+  const int grid_p = grid_for((S + kVecThreads * 32 - 1) / (kVecThreads * 32) * P, sms * kVecCtas);
+#define K2(TM, B, AD)                                                                                         \
+  do {                                                                                                      \
+    if (units.remote)  /* P2P pulls: the 2 x 16-element layout */                                          \
+      k2_qwd_apply_pull<TM, B, AD><<<grid_p, kVecThreads, 0, st>>>(units, S, stride, P, rot % P,             \
+                                                                   __builtin_ctz(G), static_cast<TM*>(w_model), -0.0f); \
+    else                                                                                                    \
+      k2_qwd_apply<TM, B, AD><<<grid, kVecThreads, 0, st>>>(units, S, stride, P, rot % P, __builtin_ctz(G),    \
+                                                            static_cast<TM*>(w_model), -0.0f);              \
+  } while (0)
 #define K2B(TM, AD) \
   if (bits == 2) K2(TM, 2, AD); else if (bits == 4) K2(TM, 4, AD); else if (bits == 8) K2(TM, 8, AD); else K2(TM, 32, AD)
   if (model_dtype == kBF16) {
