@@ -82,11 +82,15 @@ sdp4_status sdp4_get_unique_id(unsigned char id[SDP4_UNIQUE_ID_BYTES]);
 sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, int world,
                            int groups_M, int group_size_N, int nccl_ctas);
 
-/* Host.  Pipelining: every shard is processed in `chunks` sub-ranges (0 = automatic,
- * about 16M elements per chunk, at most 8; 1 = no pipelining; at most 16); the kernels of
- * chunk c run on the caller's stream while the exchanges of other chunks run on the
- * internal stream.  Results do not depend on the chunk count (R16).  World size 1 never
- * pipelines.  sdp4_comm_chunks returns the chunk count a call with (numel, group) uses. */
+/* Host.  Pipelining: every shard is processed in `chunks` sub-ranges (0 = automatic; 1 = no
+ * pipelining; at most 16).  NCCL transport: automatic = about 16M elements per chunk, at
+ * most 8; the kernels of chunk c run on the caller's stream while the exchanges of other
+ * chunks run on the internal stream.  P2P transport (TLq-HS only): automatic = 2 for shards
+ * of at least 2^25 elements, else 1; with C > 1
+ * the chunks alternate between the caller's stream and the internal stream, so K4/K5 of
+ * one chunk overlap the NVLink-bound K3 of the next.  Results do not depend on the chunk
+ * count (R16).  World size 1 never pipelines.  sdp4_comm_chunks returns the chunk count a
+ * call with (numel, group) uses. */
 sdp4_status sdp4_comm_set_chunks(sdp4_comm_t comm, int chunks);
 int sdp4_comm_chunks(sdp4_comm_t comm, size_t numel, int group);
 
@@ -99,7 +103,7 @@ int sdp4_comm_chunks(sdp4_comm_t comm, size_t numel, int group);
  *     (unit j read from rank j's buffer while the replica update streams HBM).  Those receive buffers are library-
  *     owned, symmetric, double-buffered by call parity and allocated collectively on first
  *     use (the caller's workspace is then unused and may be NULL / 0 bytes); completion is signalled per source with
- *     epoch flags (cuStreamWriteValue32 / cuStreamWaitValue32).  P2P never chunks.
+ *     epoch flags (cuStreamWriteValue32 / cuStreamWaitValue32).
  * Results are bit-identical across transports (R16).  sdp4_comm_transport returns the
  * current one. */
 sdp4_status sdp4_comm_set_transport(sdp4_comm_t comm, int transport);
