@@ -239,7 +239,7 @@ class Comm:
         return torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
 
     # -- qWD (Alg. 2 l.2-5) ----------------------------------------------------------
-    def qwd_quantize(self, w_main_shard: torch.Tensor, w_model: torch.Tensor, workspace: torch.Tensor,
+    def qwd_quantize(self, w_main_shard: torch.Tensor, w_model: torch.Tensor, workspace: Optional[torch.Tensor],
                      bits: int = 4, group: int = 128, seed=None, stream=None):
         """seed: stochastic rounding (R14) with this seed; None: round to nearest even."""
         if w_main_shard.dtype != torch.float32:
@@ -248,13 +248,13 @@ class Comm:
                                        w_model.numel(), bits, group, RNE if seed is None else STOCHASTIC,
                                        seed or 0, _ptr(workspace), _nbytes(workspace), _stream(stream)))
 
-    def qwd_allgather_apply(self, workspace: torch.Tensor, w_model: torch.Tensor, bits: int = 4,
+    def qwd_allgather_apply(self, workspace: Optional[torch.Tensor], w_model: torch.Tensor, bits: int = 4,
                             group: int = 128, stream=None):
         _check(lib().sdp4_qwd_allgather_apply(self._h, _ptr(workspace), _nbytes(workspace), w_model.numel(), bits,
                                               group, _ptr(w_model), _DT[w_model.dtype], _stream(stream)))
 
     # -- ablation baselines ---------------------------------------------
-    def qw_quantize(self, w_main_shard: torch.Tensor, numel: int, workspace: torch.Tensor, bits: int = 4,
+    def qw_quantize(self, w_main_shard: torch.Tensor, numel: int, workspace: Optional[torch.Tensor], bits: int = 4,
                     group: int = 128, seed=None, stream=None):
         """qW (Alg. 1, QSDP / ZeRO++): quantize the main-weight shard itself."""
         if w_main_shard.dtype != torch.float32:
@@ -263,7 +263,7 @@ class Comm:
                                       RNE if seed is None else STOCHASTIC, seed or 0, _ptr(workspace),
                                       _nbytes(workspace), _stream(stream)))
 
-    def qw_allgather_apply(self, workspace: torch.Tensor, w_model: torch.Tensor, bits: int = 4, group: int = 128,
+    def qw_allgather_apply(self, workspace: Optional[torch.Tensor], w_model: torch.Tensor, bits: int = 4, group: int = 128,
                            stream=None):
         """qW all-gather + dequantize: the replica becomes the gathered quantized weights."""
         _check(lib().sdp4_qw_allgather_apply(self._h, _ptr(workspace), _nbytes(workspace), w_model.numel(), bits,
@@ -272,7 +272,7 @@ class Comm:
     def ring_workspace_bytes(self, numel: int, bits: int = 4, group: int = 128) -> int:
         return ring_workspace_bytes(self.world, numel, bits, group)
 
-    def ring_reduce_scatter(self, grad: torch.Tensor, out_shard: torch.Tensor, workspace: torch.Tensor,
+    def ring_reduce_scatter(self, grad: torch.Tensor, out_shard: torch.Tensor, workspace: Optional[torch.Tensor],
                             bits: int = 4, group: int = 128, average: bool = True, stream=None):
         """Ring reduce-scatter with per-hop quantization (sec. 2.3), ablation baseline."""
         if out_shard.dtype != torch.float32:
@@ -282,7 +282,7 @@ class Comm:
                                               _nbytes(workspace), _stream(stream)))
 
     # -- TLq-HS (Alg. 3) -------------------------------------------------------------
-    def tlq_hs_reduce_scatter(self, grad: torch.Tensor, out_shard: torch.Tensor, workspace: torch.Tensor,
+    def tlq_hs_reduce_scatter(self, grad: torch.Tensor, out_shard: torch.Tensor, workspace: Optional[torch.Tensor],
                               bits_intra: int = 8, bits_inter: int = 4, group: int = 128,
                               hadamard_block: int = 64, average: bool = True, seed=None, stream=None):
         """seed: stochastic rounding (R14) of both quantizers with this seed; None: nearest even."""
