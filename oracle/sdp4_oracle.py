@@ -32,7 +32,7 @@ __all__ = [
     "group_scales", "quantize", "dequantize", "fwht_unnormalized", "hadamard_normalized",
     "pack_codes", "unpack_codes", "wire_unit_bytes", "wire_unit", "wire_unit_decode",
     "Topology", "qwd_quantize", "qwd_allgather_apply", "qwd_step", "qw_quantize", "qw_allgather_apply", "qw_step",
-    "ring_reduce_scatter", "RingTrace",
+    "ring_reduce_scatter", "RingTrace", "unfused_tlq_hs_reduce_scatter",
     "TlqTrace", "tlq_hs_reduce_scatter", "naive_tlq_hs_reduce_scatter", "mix32", "sr_key", "sr_uniform",
     "STAGE_QWD", "STAGE_INTRA", "STAGE_INTER",
     "exact_reduce_scatter_f64", "comm_bits_per_param",
@@ -539,6 +539,17 @@ def ring_reduce_scatter(grads, k: int, G: int, average: bool = True) -> RingTrac
             acc = (acc * F32(F32(1.0) / F32(P))).astype(F32)
         tr.out[c] = acc
     return tr
+
+
+def unfused_tlq_hs_reduce_scatter(grads, topo: Topology, G: int, b: int, k_intra: int = 8, k_inter: int = 4,
+                                  average: bool = True):
+    """TLq-HS with the Hadamard transforms as separate passes ("SDP4Bit (HS w/o fused)",
+    P:645, ablation comparator): h_r = H_b g_r on every rank (normalized),
+    the b = 0 two-level reduce-scatter of the h_r, then H_b on each reduced shard (l.13 moved
+    after the final reduction; H = H^T = H^-1).  Returns the P output shards."""
+    h = [hadamard_normalized(np.asarray(g, dtype=F32), b) for g in grads]
+    tr = tlq_hs_reduce_scatter(h, topo, G, 0, k_intra, k_inter, average)
+    return [hadamard_normalized(o, b) for o in tr.out]
 
 
 def exact_reduce_scatter_f64(grads, P: int, average: bool = True):

@@ -4,8 +4,9 @@ the ring reduce-scatter with per-hop quantization (sec. 2.3)."""
 import numpy as np
 import pytest
 
-from oracle import (F32, bf16_round, dequantize, exact_reduce_scatter_f64, pack_codes, q_levels, quantize,
-                    qw_step, qwd_step, ring_reduce_scatter, unpack_codes, wire_unit, wire_unit_decode)
+from oracle import (F32, Topology, bf16_round, dequantize, exact_reduce_scatter_f64, pack_codes, q_levels, quantize,
+                    qw_step, qwd_step, ring_reduce_scatter, tlq_hs_reduce_scatter, unfused_tlq_hs_reduce_scatter,
+                    unpack_codes, wire_unit, wire_unit_decode)
 from synth import main_weights, model_weights, spiky_numpy
 from tests.conftest import golden
 
@@ -134,3 +135,30 @@ def test_ring_error_grows_with_P():
     e4 = np.median([err(4, s) for s in range(12)])
     e16 = np.median([err(16, s) for s in range(12)])
     assert e16 > e4
+
+
+# ------------------------------------------------------- unfused Hadamard (KP4)
+@pytest.mark.parametrize("b", [4, 64, 256])
+def test_unfused_identity_codec_recovers_the_mean(b):
+    # H (mean of H g) = mean of g (H H = I, linearity): with lossless codecs the
+    # unfused passes reproduce the exact reduce-scatter up to fp32 rounding
+    P, G = 4, 256
+    D = P * G * 4
+    grads = [spiky_numpy(D, seed=80 + r) for r in range(P)]
+    out = np.concatenate(unfused_tlq_hs_reduce_scatter(grads, Topology(2, 2), G, b, 32, 32, True))
+    ex = np.concatenate(exact_reduce_scatter_f64(grads, P))
+    assert np.max(np.abs(out - ex)) <= 1e-5 * np.max(np.abs(ex))
+
+
+def test_unfused_and_fused_agree_within_quantization_error():
+    # the fused (pruned, R6-R8) and the unfused paths differ only by rounding placement: both
+    # are within the same few quantization steps of the exact mean, and close to each other
+    P, G, b = 4, 128, 64
+    D = P * G * 8
+    grads = [spiky_numpy(D, seed=90 + r) for r in range(P)]
+    fused = np.concatenate(tlq_hs_reduce_scatter(grads, Topology(2, 2), G, b, 8, 4, True).out)
+    unf = np.concatenate(unfused_tlq_hs_reduce_scatter(grads, Topology(2, 2), G, b, 8, 4, True))
+    ex = np.concatenate(exact_reduce_scatter_f64(grads, P))
+    ef, eu = np.linalg.norm(fused - ex), np.linalg.norm(unf - ex)
+    assert abs(ef - eu) < 0.1 * ef
+    assert np.linalg.norm(fused - unf) < 0.5 * ef
