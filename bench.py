@@ -374,6 +374,25 @@ def run_sdp4(a, rank, world, local_rank):
                              "nvlink_GBps": round(nv / (t * 1e-3) / 1e9, 1) if nv else None,
                              "nvlink_frac_of_900": round(nv / (t * 1e-3) / 900e9, 4) if nv else None}
 
+    # ablation (NEXT-3): TLq-HS with the Hadamard transforms as separate passes ("SDP4Bit (HS
+    # w/o fused)") -- K3 identity codec forward pass, the b = 0 reduce-scatter, K5
+    # identity codec inverse pass -- against the fused path
+    ablation = None
+    if not a.no_comparators and a.hadamard > 0:
+        from paper_2410_15526_b200 import tlq_stage_final, tlq_stage_quantize
+        hbuf = torch.empty(D, dtype=torch.float32, device=dev)
+        red = torch.empty(S, dtype=torch.float32, device=dev)
+        out2 = torch.empty(S, dtype=torch.float32, device=dev)
+
+        def unfused():
+            tlq_stage_quantize(grad, hbuf.view(torch.uint8), 1, 1, 32, a.group, a.hadamard)
+            comm.tlq_hs_reduce_scatter(hbuf, red, ws_t, a.bits_intra, a.bits_inter, a.group, 0, True)
+            tlq_stage_final(red.view(torch.uint8), out2, S, 1, 1, 32, a.group, a.hadamard, False)
+        t_unf = timed(unfused, max(3, a.steps // 2))
+        ablation = {"tlq_hs_fused_ms": round(t_tlq, 4), "tlq_hs_unfused_hadamard_ms": round(t_unf, 4),
+                    "fusion_speedup": round(t_unf / t_tlq, 3)}
+        del hbuf, red, out2
+
     # unquantized NCCL comparators on the same buffers (sec. 2.1), N > 1 only
     comparators = None
     if world > 1 and not a.no_comparators:
@@ -479,7 +498,8 @@ def run_sdp4(a, rank, world, local_rank):
                            "storage": "bf16/fp32 storage, fp32 arithmetic, int8/int4 wire codes"},
                 "clocks": clk.summary(), "gpu_launches": int(launches), "kernels": kern, "comm_ops": comm_ops,
                 "ms_per_step_profiled": round(ms_prof, 4), "roofline": roofline,
-                "collectives": collectives, "e2e": e2e, "comparators": comparators, "cpu_baseline": cpu}
+                "collectives": collectives, "e2e": e2e, "comparators": comparators, "ablation": ablation,
+                "cpu_baseline": cpu}
         emit(line)
     comm.close()
 

@@ -14,7 +14,7 @@ import torch
 
 import oracle
 import synth
-from paper_2410_15526_b200 import Comm
+from paper_2410_15526_b200 import Comm, tlq_stage_final, tlq_stage_quantize
 from tests.test_gpu_parity import assert_unit_equal, bf16_equal, f32_equal
 
 pytestmark = pytest.mark.gpu
@@ -143,3 +143,31 @@ def test_counterexample_alg4_on_gpu(comm):
     assert np.all(qw == np.array([1.0, -1.0], np.float32))                 # stuck for every t
     qwd = _gpu_run(comm, "qWD", br, eta)
     assert np.linalg.norm(qwd[-1]) < 1e-2                                  # converges to w* = 0
+
+
+# ------------------------------------------- unfused Hadamard comparator (NEXT-3)
+def unfused_on_gpu(comm, grad, G, b, bi=8, be=4):
+    """Separate Hadamard passes around the b = 0 reduce-scatter, from the library's own
+    kernels: K3 with the identity codec writes rn(H_unnorm(g) * c_b) (R12), the TLq
+    reduce-scatter runs with b = 0, and K5 with the identity codec, M = 1 and no averaging
+    applies rn(H_unnorm(x) * c_b) to the reduced shard."""
+    D = grad.numel()
+    S = D // comm.world
+    h = torch.empty(D, dtype=torch.float32, device="cuda")
+    tlq_stage_quantize(grad, h.view(torch.uint8), 1, 1, 32, G, b)
+    red = torch.empty(S, dtype=torch.float32, device="cuda")
+    ws = torch.zeros(comm.tlq_workspace_bytes(D, bi, be, G), dtype=torch.uint8, device="cuda")
+    comm.tlq_hs_reduce_scatter(h, red, ws, bi, be, G, 0, True)
+    out = torch.empty(S, dtype=torch.float32, device="cuda")
+    tlq_stage_final(red.view(torch.uint8), out, S, 1, 1, 32, G, b, False)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("G,b", [(128, 64), (256, 256), (64, 16)])
+def test_unfused_hadamard_comparator(comm, G, b):
+    D = 16384 * 2 + max(G, 64) * 5
+    g = synth.gradient(D, seed=41 + b, dtype=torch.bfloat16)
+    got = unfused_on_gpu(comm, g.cuda(), G, b)
+    want = oracle.unfused_tlq_hs_reduce_scatter([g.float().numpy()], oracle.Topology(1, 1), G, b)[0]
+    assert f32_equal(got, want)
