@@ -29,6 +29,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -136,6 +137,7 @@ struct sdp4_comm {
   uint32_t epoch_qwd = 0, epoch_tlq = 0, epoch_ring = 0;
   PFN_cuStreamWriteValue32_v11070 write_value = nullptr;
   PFN_cuStreamWaitValue32_v11070 wait_value = nullptr;
+  PFN_cuStreamBatchMemOp_v11070 batch_memop = nullptr;  // all flag writes / waits of a step in one call
   int device = 0;
   int sm_count = 148;
   int nccl_ctas = kDefaultNcclCtas;
@@ -311,6 +313,23 @@ CUdeviceptr flag_ptr(const SymBuf& b, int owner, int stage, int src) {
 // After the producing kernel on `st`: raise flag[stage][me] on every destination rank.
 sdp4_status signal_peers(sdp4_comm* c, cudaStream_t st, const SymBuf& b, int stage, const std::vector<int>& dsts,
                          uint32_t epoch) {
+  if (c->batch_memop) {  // one batched stream memory operation for every destination
+    CUstreamBatchMemOpParams ops[sdp4::kMaxDests];
+    unsigned n = 0;
+    for (int q : dsts) {
+      if (q == c->rank || n >= (unsigned)sdp4::kMaxDests) continue;
+      memset(&ops[n], 0, sizeof(ops[n]));
+      ops[n].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+      ops[n].writeValue.address = flag_ptr(b, q, stage, c->rank);
+      ops[n].writeValue.value = epoch;
+      ops[n].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+      ++n;
+    }
+    if (!n) return SDP4_OK;
+    CUresult r = c->batch_memop((CUstream)st, n, ops, 0);
+    if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamBatchMemOp (write) failed (%d)", (int)r);
+    return SDP4_OK;
+  }
   for (int q : dsts) {
     if (q == c->rank) continue;
     CUresult r = c->write_value((CUstream)st, flag_ptr(b, q, stage, c->rank), epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
@@ -328,10 +347,28 @@ sdp4_status wait_peers(sdp4_comm* c, cudaStream_t st, const SymBuf& b, int stage
     eb = c->ev();
     cudaEventRecord(ea, st);
   }
-  for (int q : srcs) {
-    if (q == c->rank) continue;
-    CUresult r = c->wait_value((CUstream)st, flag_ptr(b, c->rank, stage, q), epoch, CU_STREAM_WAIT_VALUE_GEQ);
-    if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+  if (c->batch_memop) {
+    CUstreamBatchMemOpParams ops[sdp4::kMaxDests];
+    unsigned n = 0;
+    for (int q : srcs) {
+      if (q == c->rank || n >= (unsigned)sdp4::kMaxDests) continue;
+      memset(&ops[n], 0, sizeof(ops[n]));
+      ops[n].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+      ops[n].waitValue.address = flag_ptr(b, c->rank, stage, q);
+      ops[n].waitValue.value = epoch;
+      ops[n].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+      ++n;
+    }
+    if (n) {
+      CUresult r = c->batch_memop((CUstream)st, n, ops, 0);
+      if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamBatchMemOp (wait) failed (%d)", (int)r);
+    }
+  } else {
+    for (int q : srcs) {
+      if (q == c->rank) continue;
+      CUresult r = c->wait_value((CUstream)st, flag_ptr(b, c->rank, stage, q), epoch, CU_STREAM_WAIT_VALUE_GEQ);
+      if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+    }
   }
   if (c->profiling) {
     cudaEventRecord(eb, st);
@@ -461,6 +498,11 @@ sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, 
     cudaGetDriverEntryPoint("cuStreamWaitValue32", &fwt, cudaEnableDefault, &q2);
     c->write_value = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(fw);
     c->wait_value = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(fwt);
+    void* fb = nullptr;
+    cudaDriverEntryPointQueryResult q3;
+    cudaGetDriverEntryPoint("cuStreamBatchMemOp", &fb, cudaEnableDefault, &q3);
+    c->batch_memop = reinterpret_cast<PFN_cuStreamBatchMemOp_v11070>(fb);
+    if (getenv("SDP4_NO_BATCH_MEMOP")) c->batch_memop = nullptr;  // measurement switch
     const bool p2p_ok = c->write_value && c->wait_value && group_size_N <= sdp4::kMaxN &&
                         groups_M <= sdp4::kMaxDests && world <= sdp4::kMaxDests;
     c->transport = p2p_ok ? kTransportP2P : kTransportNccl;
