@@ -323,8 +323,9 @@ def run_sdp4(a, rank, world, local_rank):
     for name, (tms, cnt) in prof.items():
         if name.startswith("nccl_") or name.startswith("wait_"):
             continue
-        kb = kernel_bytes(name, D, S, P, M, N, a)
-        nb = kernel_nvlink_bytes(name, D, S, P, M, N, a, transport)
+        per_step = max(1, round(cnt / a.steps))          # launches per step (pipeline chunks)
+        kb = kernel_bytes(name, D, S, P, M, N, a) / per_step   # algorithmic bytes per launch
+        nb = kernel_nvlink_bytes(name, D, S, P, M, N, a, transport) / per_step
         avg = tms / max(cnt, 1)
         kern[name] = {"avg_ms": round(avg, 4), "launches": cnt, "share": None,
                       "alg_bytes": kb, "gbs": round(kb / (avg * 1e-3) / 1e9, 1) if kb and avg > 0 else None}
@@ -403,6 +404,16 @@ def run_sdp4(a, rank, world, local_rank):
         rs_out = torch.empty(S, dtype=gdt, device=dev)
         t_ag = timed(lambda: dist.all_gather_into_tensor(big, d_shard), max(3, a.steps // 2))
         t_rs = timed(lambda: dist.reduce_scatter_tensor(rs_out, grad, op=dist.ReduceOp.AVG), max(3, a.steps // 2))
+        # Megatron-realistic pair: bf16 model-weight all-gather and
+        # fp32 gradient reduce-scatter
+        w_shard16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
+        big16 = big.view(torch.bfloat16)[:D]
+        t_ag16 = timed(lambda: dist.all_gather_into_tensor(big16, w_shard16), max(3, a.steps // 2))
+        del big16
+        g32 = grad.float() if gdt != torch.float32 else grad
+        rs32 = torch.empty(S, dtype=torch.float32, device=dev)
+        t_rs32 = timed(lambda: dist.reduce_scatter_tensor(rs32, g32, op=dist.ReduceOp.AVG), max(3, a.steps // 2))
+        del g32, rs32, w_shard16
         del big
         # ablation baselines through libsdp4 (NEXT-3): 4-bit ring reduce-scatter with per-hop
         # quantization and the qW direct-weight all-gather (Alg. 1)
@@ -416,7 +427,10 @@ def run_sdp4(a, rank, world, local_rank):
                        "unquantized_GBps": round(P * pre_bytes_rank / ((t_ag + t_rs) * 1e-3) / 1e9, 2),
                        "speedup_vs_unquantized": round((t_ag + t_rs) / ms, 3),
                        "speedup_all_gather": round(t_ag / t_qwd, 3), "speedup_reduce_scatter": round(t_rs / t_tlq, 3),
-                       f"ring_q{a.bits_inter}_reduce_scatter_ms": round(t_ring, 3)}
+                       f"ring_q{a.bits_inter}_reduce_scatter_ms": round(t_ring, 3),
+                       "megatron_pair": {"nccl_all_gather_bf16_ms": round(t_ag16, 3),
+                                         "nccl_reduce_scatter_fp32_ms": round(t_rs32, 3),
+                                         "speedup_vs_pair": round((t_ag16 + t_rs32) / ms, 3)}}
 
     # end to end through the public API with host buffers (pinned), copies inside the region.
     # Pipelined like a data loader: step i+1's inputs are copied host->device on one stream

@@ -85,8 +85,7 @@ sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, 
 /* Host.  Pipelining: every shard is processed in `chunks` sub-ranges (0 = automatic; 1 = no
  * pipelining; at most 16).  NCCL transport: automatic = about 16M elements per chunk, at
  * most 8; the kernels of chunk c run on the caller's stream while the exchanges of other
- * chunks run on the internal stream.  P2P transport (TLq-HS only): automatic = 2 for shards
- * of at least 2^25 elements, else 1; with C > 1
+ * chunks run on the internal stream.  P2P transport (TLq-HS only): automatic = 1; with C > 1
  * the chunks alternate between the caller's stream and the internal stream, so K4/K5 of
  * one chunk overlap the NVLink-bound K3 of the next.  Results do not depend on the chunk
  * count (R16).  World size 1 never pipelines.  sdp4_comm_chunks returns the chunk count a

@@ -181,7 +181,7 @@ struct sdp4_comm {
   int chunks(size_t S) const {
     if (world == 1) return 1;
     if (chunks_cfg > 0) return std::min(chunks_cfg, kMaxChunks);
-    if (transport == kTransportP2P) return S >= ((size_t)1 << 25) ? 2 : 1;  // measured, DESIGN.md sec. 9
+    if (transport == kTransportP2P) return 1;  // chunking gains ~2%; opt in with set_chunks
     const size_t c = S / ((size_t)16 << 20);  // ~16M elements per chunk and shard
     return (int)std::max<size_t>(1, std::min<size_t>(c, 8));
   }
