@@ -118,7 +118,10 @@ int sdp4_comm_transport(sdp4_comm_t comm);
  * (R16).  EINVAL unless 0 <= num <= den, 1 <= den <= 64. */
 sdp4_status sdp4_comm_set_intra_pull(sdp4_comm_t comm, int num, int den);
 
-/* Host, collective.  Destroys the NCCL communicators and frees the comm. */
+/* Host, collective (every rank calls it).  Waits for this rank's work, then -- if symmetric
+ * buffers were allocated -- barriers with the peers (they may still be pulling from this
+ * rank's buffers) before unmapping and freeing them; destroys the NCCL communicators and
+ * frees the comm. */
 sdp4_status sdp4_comm_destroy(sdp4_comm_t comm);
 
 /* ---------------------------------------------------------------------------

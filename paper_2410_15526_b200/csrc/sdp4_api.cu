@@ -546,6 +546,18 @@ sdp4_status sdp4_comm_destroy(sdp4_comm_t c) {
   }
   for (auto e : c->pool) cudaEventDestroy(e);
   for (auto e : c->deps) cudaEventDestroy(e);
+  const bool any_sym = c->sym_qwd.local || c->sym_tlq.local || c->sym_ring.local;
+  if (any_sym && c->world_c) {
+    // peers may still be reading this rank's symmetric buffers (K2 / K4 pulls): every rank
+    // finishes its own work, then a barrier, then the mappings are closed and freed
+    cudaDeviceSynchronize();
+    int* tok = nullptr;
+    if (cudaMalloc(&tok, sizeof(int)) == cudaSuccess) {
+      ncclAllReduce(tok, tok, 1, ncclInt32, ncclSum, c->world_c, c->side);
+      cudaStreamSynchronize(c->side);
+      cudaFree(tok);
+    }
+  }
   for (SymBuf* b : {&c->sym_qwd, &c->sym_tlq, &c->sym_ring}) {
     if (!b->local) continue;
     cudaDeviceSynchronize();
