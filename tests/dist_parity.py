@@ -55,8 +55,8 @@ def main():
     for tr in a.transports.split(","):
         runs += [(tr, ch, None) for ch in ([int(x) for x in a.chunks.split(",")] if tr == "nccl" else [0])]
         runs.append((tr, 3 if tr == "nccl" else 0, 2 ** 34 + 2410))     # stochastic rounding (R14)
-    if "p2p" in a.transports:   # intra all-to-all split between K3 pushes and K4 pulls
-        runs += [("p2p", -1, None), ("p2p", -3, 2410)]
+    if "p2p" in a.transports:   # intra all-to-all split between K3 pushes and K4 pulls; chunked P2P
+        runs += [("p2p", -1, None), ("p2p", -3, 2410), ("p2p", 2, None), ("p2p", 3, 2411)]
     for tr, chunks, seed in runs:
         comm.set_transport(tr)
         comm.set_chunks(max(chunks, 0))
