@@ -493,8 +493,11 @@ def run_sdp4(a, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        v, desc, cores = oracle_sample_rate(a, a.cpu_seconds, D)
-        cpu = {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc}
+        try:   # host-only and single-rank: a failure here must not cost the GPU line
+            v, desc, cores = oracle_sample_rate(a, a.cpu_seconds, D)
+            cpu = {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"error": f"{type(ex).__name__}: {ex}"[:300], "kind": "oracle"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": a.steps,
