@@ -73,6 +73,9 @@ def test_validation_errors_before_any_launch():
     assert st == sdp4.EINVAL and b"bits" in L.sdp4_last_error()        # int2 is a weight codec only
     assert L.sdp4_ring_workspace_bytes(4, 4096, 4, 128) == 2 * oracle.wire_unit_bytes(1024, 4, 128)
     assert L.sdp4_wire_unit_bytes(4096, 2, 64) == oracle.wire_unit_bytes(4096, 2, 64)
+    st = L.sdp4_tlq_hs_reduce_scatter(c._h, None, 0, 0, 8, 4, 128, 64, 1, 0, 0, None, None, 0, None)
+    assert st == sdp4.EALIGN and b"nonzero" in L.sdp4_last_error()      # empty buffers are rejected
+    assert L.sdp4_qwd_workspace_bytes(1, 0, 4, 128) == 0
     bad = ctypes.c_void_p()
     assert L.sdp4_comm_init(ctypes.byref(bad), None, 0, 8, 3, 3, 0) == sdp4.EINVAL
     assert L.sdp4_comm_set_chunks(c._h, 17) == sdp4.EINVAL

@@ -213,3 +213,16 @@ def test_tlq_stochastic_parity(comm, dtype, G, b, bi, be):
     D = 16384 * 2 + max(G, 64) * 7
     grad = synth.gradient(D, seed=31 + G, dtype=dtype)
     check_tlq(comm, grad, bi, be, G, b, True, seed=2 ** 35 + G)
+
+
+@pytest.mark.parametrize("D,G,b", [(64, 64, 64), (128, 32, 32), (384, 128, 64), (2048, 2048, 256)])
+def test_tiny_buffers(comm, D, G, b):
+    # smallest valid buffers (one row, less than one tile, one group): every kernel's ragged tail
+    grad = synth.gradient(D, seed=D + G, dtype=torch.float32)
+    check_tlq(comm, grad, 8, 4, G, b)
+    w_model = synth.model_weights(D, seed=D)
+    w_main = synth.main_weights(w_model, seed=D + 1)
+    unit, new = run_qwd(comm, w_main, w_model, 4, G)
+    (codes, scales), want_new = oracle_qwd(w_main, w_model, 4, G)
+    assert_unit_equal(unit, codes, scales, 4, G, D, "tiny qWD unit")
+    assert bf16_equal(synth.bf16_bits(new), want_new)
