@@ -20,6 +20,7 @@
 #include "sdp4_kernels.cuh"
 
 #include <cfloat>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <cuda.h>
@@ -749,121 +750,135 @@ __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply(const Dests units, s
   }
 }
 
-// K2 for the P2P transport (units read over NVLink): two 16-element vectors per thread, so
-// each thread has 16 code bytes of remote loads in flight (a warp pulls 2 x 256 contiguous
-// bytes) -- measured faster than the 8-element layout once 3/4 of the codes come from peers.
+// K2 for the P2P transport, ring variant: thread 0 streams each tile's codes and scales from
+// the source rank's buffer into a STAGES-deep shared-memory ring with 1-D bulk copies (4 KB
+// per copy for 4-bit codes, so the NVLink pull moves large requests and many of them are in
+// flight), while every thread runs K1's 8-element layout on the replica (four rounds per
+// 8192-element tile, the four 16-byte replica loads issued up front).
+constexpr int kK2rTile = 8192;
+constexpr int kK2rStages = 6;
 template <int BITS>
-struct K2Vec {
-  static constexpr int CB = BITS == 32 ? 64 : 16 * BITS / 8;  // code bytes per 16 elements
+struct K2rCfg {
+  static constexpr int CODE_BYTES = kK2rTile * (BITS == 32 ? 32 : BITS) / 8;
+  static constexpr int SC_BYTES = BITS == 32 ? 0 : kK2rTile / 32 * 4;  // G >= 32
+  static constexpr int STAGE = CODE_BYTES + SC_BYTES;
+  static constexpr int SMEM = kK2rStages * STAGE + kK2rStages * 8 + 128;
 };
 
 template <typename TM, int BITS, bool ADD>
-__device__ __forceinline__ void k2p_load(const uint8_t* unit, const float* scales, const TM* wm, size_t e, int lg,
-                                        uint4* cw, float& sc, uint4* mw) {
-  if constexpr (BITS == 32) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) cw[i] = *reinterpret_cast<const uint4*>(unit + e * 4 + 16 * i);
-  } else if constexpr (BITS == 8) {
-    cw[0] = *reinterpret_cast<const uint4*>(unit + e);
-    sc = scales[e >> lg];
-  } else if constexpr (BITS == 4) {
-    const uint2 w = *reinterpret_cast<const uint2*>(unit + e / 2);
-    cw[0] = make_uint4(w.x, w.y, 0u, 0u);
-    sc = scales[e >> lg];
-  } else {
-    cw[0] = make_uint4(*reinterpret_cast<const uint32_t*>(unit + e / 4), 0u, 0u, 0u);
-    sc = scales[e >> lg];
-  }
-  if constexpr (!ADD) {
-    return;
-  } else if constexpr (sizeof(TM) == 2) {
-    mw[0] = *reinterpret_cast<const uint4*>(wm + e);
-    mw[1] = *reinterpret_cast<const uint4*>(wm + e + 8);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) mw[i] = *reinterpret_cast<const uint4*>(wm + e + 4 * i);
-  }
-}
-
-template <typename TM, int BITS, bool ADD>
-__device__ __forceinline__ void k2p_apply(const uint4* cw, float sc, uint4* mw, TM* wm, size_t e, float z) {
+__global__ void __launch_bounds__(kVecThreads) k2_qwd_apply_ring(const Dests units, size_t S, size_t stride, int P,
+                                                                    int rot, int lg, TM* __restrict__ w_model, float z) {
+  using C = K2rCfg<BITS>;
+  constexpr int ROUNDS = kK2rTile / (kVecThreads * 8);
   constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
-  float x[16];
-  if constexpr (BITS == 32) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      x[4 * i] = __uint_as_float(cw[i].x); x[4 * i + 1] = __uint_as_float(cw[i].y);
-      x[4 * i + 2] = __uint_as_float(cw[i].z); x[4 * i + 3] = __uint_as_float(cw[i].w);
-    }
-  } else {
-    const float ds = __fdiv_rn(sc, q);
-    float f[16];
-    if constexpr (BITS == 2) {
-      dec2x16(cw[0].x, f);
-    } else if constexpr (BITS == 4) {
-      dec4x8(cw[0].x, f);
-      dec4x8(cw[0].y, f + 8);
-    } else {
-      dec8x4(cw[0].x, f); dec8x4(cw[0].y, f + 4); dec8x4(cw[0].z, f + 8); dec8x4(cw[0].w, f + 12);
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) x[i] = mulz(f[i], ds, z);  // the product is added next: fusion barrier
-  }
-  if constexpr (!ADD) {
-    if constexpr (sizeof(TM) == 2) {
-      uint4 o[2];
-      uint32_t* w = &o[0].x;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = pack_bf16x2(x[2 * i], x[2 * i + 1]);
-      reinterpret_cast<uint4*>(wm + e)[0] = o[0];
-      reinterpret_cast<uint4*>(wm + e + 8)[0] = o[1];
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        reinterpret_cast<float4*>(wm + e + 4 * i)[0] = make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
-    }
-  } else if constexpr (sizeof(TM) == 2) {
-    uint32_t* w = &mw[0].x;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      w[i] = pack_bf16x2(__fadd_rn(bf16_lo(w[i]), x[2 * i]), __fadd_rn(bf16_hi(w[i]), x[2 * i + 1]));
-    reinterpret_cast<uint4*>(wm + e)[0] = mw[0];
-    reinterpret_cast<uint4*>(wm + e + 8)[0] = mw[1];
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float4 t;
-      t.x = __fadd_rn(__uint_as_float(mw[i].x), x[4 * i]);
-      t.y = __fadd_rn(__uint_as_float(mw[i].y), x[4 * i + 1]);
-      t.z = __fadd_rn(__uint_as_float(mw[i].z), x[4 * i + 2]);
-      t.w = __fadd_rn(__uint_as_float(mw[i].w), x[4 * i + 3]);
-      reinterpret_cast<float4*>(wm + e + 4 * i)[0] = t;
-    }
-  }
-}
-
-template <typename TM, int BITS, bool ADD>
-__global__ void __launch_bounds__(kVecThreads) k2_qwd_apply_pull(const Dests units, size_t S, size_t stride, int P,
-                                                               int rot, int lg, TM* __restrict__ w_model, float z) {
-  constexpr int TILE = kVecThreads * 32;
-  const size_t tpu = (S + TILE - 1) / TILE;
-  // unit index fastest and rotated by this rank: at any moment every rank pulls from every
-  // source, instead of all ranks draining the same source's NVLink port together
-  for (size_t tile = blockIdx.x; tile < tpu * P; tile += gridDim.x) {
-    const size_t ts = tile / P;
-    size_t j = tile - ts * P + rot;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kK2rStages * C::STAGE);
+  const int t = threadIdx.x;
+  const size_t tpu = (S + kK2rTile - 1) / kK2rTile, ntiles = tpu * P;
+  const size_t sc_off = S * (BITS == 32 ? 4 : BITS) / 8;
+  auto tile_of = [&](size_t tile, size_t& ts, size_t& j) {  // unit fastest, rotated by this rank
+    ts = tile / P;
+    j = tile - ts * P + rot;
     if (j >= (size_t)P) j -= P;
-    const uint8_t* unit = units.p[j];  // unit j: local, or rank j's own buffer (P2P pull over NVLink)
-    const float* scales = reinterpret_cast<const float*>(unit + S * (BITS == 32 ? 4 : BITS) / 8);
+  };
+  if (t == 0) {
+    for (int s = 0; s < kK2rStages; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t k) {  // thread 0: tile k of this CTA into stage k % STAGES
+    const size_t tile = blockIdx.x + (size_t)k * gridDim.x;
+    if (tile >= ntiles) return;
+    size_t ts, j;
+    tile_of(tile, ts, j);
+    const size_t e0 = ts * kK2rTile;
+    const uint32_t n = (uint32_t)min((size_t)kK2rTile, S - e0);
+    const uint32_t cb = n * (BITS == 32 ? 32 : BITS) / 8;
+    uint32_t sb = 0;
+    if constexpr (BITS != 32) sb = ((((n >> lg) * 4) + 15) & ~15u);
+    const int s = k % kK2rStages;
+    mbar_arrive_tx(&bar[s], cb + sb);
+    const uint8_t* unit = units.p[j];
+    bulk_load(smem + s * C::STAGE, unit + e0 * (BITS == 32 ? 32 : BITS) / 8, cb, &bar[s]);
+    if constexpr (BITS != 32)
+      bulk_load(smem + s * C::STAGE + C::CODE_BYTES, unit + sc_off + (e0 >> lg) * 4, sb, &bar[s]);
+  };
+  if (t == 0)
+    for (int k = 0; k < kK2rStages; ++k) issue(k);
+  for (uint32_t k = 0;; ++k) {
+    const size_t tile = blockIdx.x + (size_t)k * gridDim.x;
+    if (tile >= ntiles) break;
+    size_t ts, j;
+    tile_of(tile, ts, j);
     TM* wm = w_model + j * stride;
-    const size_t ea = ts * TILE + threadIdx.x * 16, eb = ea + TILE / 2;
-    uint4 ca[4], cb[4], ma[4], mb[4];
-    float sa = 0.f, sb = 0.f;
-    const bool aa = ea < S, ab = eb < S;
-    if (aa) k2p_load<TM, BITS, ADD>(unit, scales, wm, ea, lg, ca, sa, ma);
-    if (ab) k2p_load<TM, BITS, ADD>(unit, scales, wm, eb, lg, cb, sb, mb);
-    if (aa) k2p_apply<TM, BITS, ADD>(ca, sa, ma, wm, ea, z);
-    if (ab) k2p_apply<TM, BITS, ADD>(cb, sb, mb, wm, eb, z);
+    const size_t e0 = ts * kK2rTile;
+    // replica loads first (local HBM), then wait for the pulled codes
+    uint4 m0[ROUNDS], m1[ROUNDS];
+#pragma unroll
+    for (int r = 0; r < ROUNDS; ++r) {
+      const size_t e = e0 + r * (kVecThreads * 8) + t * 8;
+      m0[r] = m1[r] = make_uint4(0u, 0u, 0u, 0u);
+      if (ADD && e < S) {
+        m0[r] = *reinterpret_cast<const uint4*>(wm + e);
+        if constexpr (sizeof(TM) == 4) m1[r] = *reinterpret_cast<const uint4*>(wm + e + 4);
+      }
+    }
+    const int s = k % kK2rStages;
+    mbar_wait(&bar[s], (k / kK2rStages) & 1);
+    const uint8_t* st = smem + s * C::STAGE;
+#pragma unroll
+    for (int r = 0; r < ROUNDS; ++r) {
+      const uint32_t el = r * (kVecThreads * 8) + t * 8;  // element offset within the tile
+      const size_t e = e0 + el;
+      if (e >= S) continue;
+      float x[8];
+      if constexpr (BITS == 32) {
+        const uint4 a = *reinterpret_cast<const uint4*>(st + el * 4);
+        const uint4 b = *reinterpret_cast<const uint4*>(st + el * 4 + 16);
+        x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y); x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
+        x[4] = __uint_as_float(b.x); x[5] = __uint_as_float(b.y); x[6] = __uint_as_float(b.z); x[7] = __uint_as_float(b.w);
+      } else {
+        float f[8];
+        if constexpr (BITS == 8) {
+          const uint2 w = *reinterpret_cast<const uint2*>(st + el);
+          dec8x4(w.x, f);
+          dec8x4(w.y, f + 4);
+        } else if constexpr (BITS == 4) {
+          dec4x8(*reinterpret_cast<const uint32_t*>(st + el / 2), f);
+        } else {
+          const uint32_t w = *reinterpret_cast<const uint16_t*>(st + el / 4);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[i] = float((int)(((w >> (2 * i)) & 3u) ^ 2u) - 2);
+        }
+        const float ds = __fdiv_rn(reinterpret_cast<const float*>(st + C::CODE_BYTES)[el >> lg], q);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = ADD ? mulz(f[i], ds, z) : __fmul_rn(f[i], ds);  // added next: barrier
+      }
+      if constexpr (sizeof(TM) == 2) {
+        uint32_t* w = &m0[r].x;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          w[i] = ADD ? pack_bf16x2(__fadd_rn(bf16_lo(w[i]), x[2 * i]), __fadd_rn(bf16_hi(w[i]), x[2 * i + 1]))
+                     : pack_bf16x2(x[2 * i], x[2 * i + 1]);
+        *reinterpret_cast<uint4*>(wm + e) = m0[r];
+      } else {
+        float4 a, b;
+        if constexpr (ADD) {
+          a = make_float4(__fadd_rn(__uint_as_float(m0[r].x), x[0]), __fadd_rn(__uint_as_float(m0[r].y), x[1]),
+                          __fadd_rn(__uint_as_float(m0[r].z), x[2]), __fadd_rn(__uint_as_float(m0[r].w), x[3]));
+          b = make_float4(__fadd_rn(__uint_as_float(m1[r].x), x[4]), __fadd_rn(__uint_as_float(m1[r].y), x[5]),
+                          __fadd_rn(__uint_as_float(m1[r].z), x[6]), __fadd_rn(__uint_as_float(m1[r].w), x[7]));
+        } else {
+          a = make_float4(x[0], x[1], x[2], x[3]);
+          b = make_float4(x[4], x[5], x[6], x[7]);
+        }
+        reinterpret_cast<float4*>(wm + e)[0] = a;
+        reinterpret_cast<float4*>(wm + e + 4)[0] = b;
+      }
+    }
+    __syncthreads();  // every thread is done with stage s
+    if (t == 0) issue(k + kK2rStages);
   }
 }
 
@@ -1670,13 +1685,14 @@ cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, 
 cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride, int bits, int G, void* w_model,
                              int model_dtype, bool add, int sms, cudaStream_t st, int rot) {
   const int grid = grid_for((S + kVecThreads * 8 - 1) / (kVecThreads * 8) * P, sms * kVecCtas);
-  const int grid_p = grid_for((S + kVecThreads * 32 - 1) / (kVecThreads * 32) * P, sms * kVecCtas);
+  const int grid_r = grid_for((S + kK2rTile - 1) / kK2rTile * P, sms * 4);
 #define K2(TM, B, AD)                                                                                         \
   do {                                                                                                      \
-    if (units.remote)  /* P2P pulls: the 2 x 16-element layout */                                          \
-      k2_qwd_apply_pull<TM, B, AD><<<grid_p, kVecThreads, 0, st>>>(units, S, stride, P, rot % P,             \
-                                                                   __builtin_ctz(G), static_cast<TM*>(w_model), -0.0f); \
-    else                                                                                                    \
+    if (units.remote) { /* P2P pulls: bulk-copy ring */                                                     \
+      set_smem(k2_qwd_apply_ring<TM, B, AD>, K2rCfg<B>::SMEM);                                              \
+      k2_qwd_apply_ring<TM, B, AD><<<grid_r, kVecThreads, K2rCfg<B>::SMEM, st>>>(                            \
+          units, S, stride, P, rot % P, __builtin_ctz(G), static_cast<TM*>(w_model), -0.0f);                \
+    } else                                                                                                  \
       k2_qwd_apply<TM, B, AD><<<grid, kVecThreads, 0, st>>>(units, S, stride, P, rot % P, __builtin_ctz(G),    \
                                                             static_cast<TM*>(w_model), -0.0f);              \
   } while (0)
