@@ -986,14 +986,19 @@ sdp4_status sdp4_ring_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dtype
   if (P == 1) return hop(0, nullptr, nullptr, out_shard);
   const int next = (r + 1) % P, prev = (r + P - 1) % P;
   if (c->transport == kTransportP2P) {
-    if ((s = sym_ensure(c, c->sym_ring, (size_t)(P - 1) * W, &c->epoch_ring)) != SDP4_OK) return s;
+    // region: P-1 receive slots + one local send slot; K6 writes the hop's unit locally and
+    // the copy engine moves it into the next rank's slot (large NVLink writes)
+    if ((s = sym_ensure(c, c->sym_ring, (size_t)P * W, &c->epoch_ring)) != SDP4_OK) return s;
     const uint32_t ep = ++c->epoch_ring;
     auto slot = [&](int owner, int t) { return sym_region(c->sym_ring, owner, ep) + (size_t)t * W; };
     auto val = [&](int t) { return (ep << 6) + (uint32_t)t + 1; };
+    uint8_t* send_local = slot(r, P - 1);
     for (int t = 0; t < P - 1; ++t) {
       if (t > 0 && (s = wait_peers(c, st, c->sym_ring, 0, {prev}, val(t - 1), "wait_ring")) != SDP4_OK) return s;
-      if ((s = hop((r - t - 1 + 2 * P) % P, t ? slot(r, t - 1) : nullptr, slot(next, t), nullptr)) != SDP4_OK)
+      if ((s = hop((r - t - 1 + 2 * P) % P, t ? slot(r, t - 1) : nullptr, send_local, nullptr)) != SDP4_OK)
         return s;
+      cudaError_t e = cudaMemcpyAsync(slot(next, t), send_local, W, cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return fail(SDP4_ECUDA, "ring hop copy: %s", cudaGetErrorString(e));
       if ((s = signal_peers(c, st, c->sym_ring, 0, {next}, val(t))) != SDP4_OK) return s;
     }
     if ((s = wait_peers(c, st, c->sym_ring, 0, {prev}, val(P - 2), "wait_ring")) != SDP4_OK) return s;
