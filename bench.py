@@ -282,7 +282,9 @@ def run_sdp4(a, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    def timed(fn, steps):
+    def timed(fn, steps, warm=0):
+        for _ in range(warm):   # comparators: first-call setup (NCCL channels, symmetric buffers) untimed
+            fn()
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -389,7 +391,7 @@ def run_sdp4(a, rank, world, local_rank):
             tlq_stage_quantize(grad, hbuf.view(torch.uint8), 1, 1, 32, a.group, a.hadamard)
             comm.tlq_hs_reduce_scatter(hbuf, red, ws_t, a.bits_intra, a.bits_inter, a.group, 0, True)
             tlq_stage_final(red.view(torch.uint8), out2, S, 1, 1, 32, a.group, a.hadamard, False)
-        t_unf = timed(unfused, max(3, a.steps // 2))
+        t_unf = timed(unfused, max(3, a.steps // 2), 2)
         ablation = {"tlq_hs_fused_ms": round(t_tlq, 4), "tlq_hs_unfused_hadamard_ms": round(t_unf, 4),
                     "fusion_speedup": round(t_unf / t_tlq, 3)}
         del hbuf, red, out2
@@ -402,17 +404,17 @@ def run_sdp4(a, rank, world, local_rank):
         big = torch.empty(D, dtype=torch.float32, device=dev)
         d_shard = torch.empty(S, dtype=torch.float32, device=dev)
         rs_out = torch.empty(S, dtype=gdt, device=dev)
-        t_ag = timed(lambda: dist.all_gather_into_tensor(big, d_shard), max(3, a.steps // 2))
-        t_rs = timed(lambda: dist.reduce_scatter_tensor(rs_out, grad, op=dist.ReduceOp.AVG), max(3, a.steps // 2))
+        t_ag = timed(lambda: dist.all_gather_into_tensor(big, d_shard), max(3, a.steps // 2), 2)
+        t_rs = timed(lambda: dist.reduce_scatter_tensor(rs_out, grad, op=dist.ReduceOp.AVG), max(3, a.steps // 2), 2)
         # Megatron-realistic pair: bf16 model-weight all-gather and
         # fp32 gradient reduce-scatter
         w_shard16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
         big16 = big.view(torch.bfloat16)[:D]
-        t_ag16 = timed(lambda: dist.all_gather_into_tensor(big16, w_shard16), max(3, a.steps // 2))
+        t_ag16 = timed(lambda: dist.all_gather_into_tensor(big16, w_shard16), max(3, a.steps // 2), 2)
         del big16
         g32 = grad.float() if gdt != torch.float32 else grad
         rs32 = torch.empty(S, dtype=torch.float32, device=dev)
-        t_rs32 = timed(lambda: dist.reduce_scatter_tensor(rs32, g32, op=dist.ReduceOp.AVG), max(3, a.steps // 2))
+        t_rs32 = timed(lambda: dist.reduce_scatter_tensor(rs32, g32, op=dist.ReduceOp.AVG), max(3, a.steps // 2), 2)
         del g32, rs32, w_shard16
         del big
         # ablation baselines through libsdp4 (NEXT-3): 4-bit ring reduce-scatter with per-hop
@@ -420,7 +422,7 @@ def run_sdp4(a, rank, world, local_rank):
         ws_r = None if comm.transport == "p2p" else torch.empty(comm.ring_workspace_bytes(D, a.bits_inter, a.group),
                                                                  dtype=torch.uint8, device=dev)
         t_ring = timed(lambda: comm.ring_reduce_scatter(grad, out, ws_r, a.bits_inter, a.group, True),
-                       max(3, a.steps // 2))
+                       max(3, a.steps // 2), 2)
         del ws_r
         comparators = {"nccl_all_gather_fp32_ms": round(t_ag, 3), "nccl_reduce_scatter_grad_ms": round(t_rs, 3),
                        "unquantized_ms_per_step": round(t_ag + t_rs, 3),
