@@ -2,7 +2,8 @@
 """bench.py -- SDP4Bit hot path: qWD all-gather + TLq-HS reduce-scatter, GB/s of pre-quant bytes.
 
 One step = one pass of the whole hot path over one synthetic GPT-shaped buffer:
-  qWD   sdp4_qwd_quantize + sdp4_qwd_allgather_apply   (Alg. 2 l.2-5)
+  qWD   sdp4_qwd_step (= sdp4_qwd_quantize + sdp4_qwd_allgather_apply, owner's update in K1;
+        Alg. 2 l.2-5; --qwd-two-call times the two calls instead)
   TLq-HS sdp4_tlq_hs_reduce_scatter                     (Alg. 3)
 Pre-quant bytes per rank per step = D*4 (the fp32 weight-difference buffer gathered) +
 D*g (the gradient reduce-scattered, g = 2 for bf16); `value` sums them over all ranks.
@@ -51,6 +52,8 @@ def parse_args():
     p.add_argument("--nccl-ctas", type=int, default=0, help="SMs left to NCCL while pipelining (0 = default)")
     p.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
                    help="exchange transport (auto = fused P2P push when available)")
+    p.add_argument("--qwd-two-call", action="store_true",
+                   help="qWD as sdp4_qwd_quantize + sdp4_qwd_allgather_apply (K2 applies every unit)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-comparators", action="store_true")
@@ -120,10 +123,11 @@ def kernel_bytes(name, D, S, P, M, N, a):
 
     def wire(n, k, G):
         return n * k / 8 + (4 * n / G if k != 32 else 0)
+    own = 0 if a.qwd_two_call else 1          # sdp4_qwd_step: K1 applies the owner's unit
     if name.startswith("K1"):
-        return S * (4 + m) + wire(S, a.bits_w, a.qwd_group)
+        return S * (4 + m) + wire(S, a.bits_w, a.qwd_group) + own * S * m
     if name.startswith("K2"):
-        return wire(D, a.bits_w, a.qwd_group) + 2 * m * D
+        return wire(D - own * S, a.bits_w, a.qwd_group) + 2 * m * (D - own * S)
     if name.startswith("K3"):
         return D * g + wire(D, a.bits_intra, a.group)
     if name.startswith("K4"):
@@ -266,9 +270,15 @@ def run_sdp4(a, rank, world, local_rank):
         ws_t = torch.empty(comm.tlq_workspace_bytes(D, a.bits_intra, a.bits_inter, a.group), dtype=torch.uint8,
                            device=dev)
 
+    def qwd(wmain):
+        if a.qwd_two_call:
+            comm.qwd_quantize(wmain, w_model, ws_q, a.bits_w, a.qwd_group)
+            comm.qwd_allgather_apply(ws_q, w_model, a.bits_w, a.qwd_group)
+        else:
+            comm.qwd_step(wmain, w_model, ws_q, a.bits_w, a.qwd_group)
+
     def step():
-        comm.qwd_quantize(w_main, w_model, ws_q, a.bits_w, a.qwd_group)
-        comm.qwd_allgather_apply(ws_q, w_model, a.bits_w, a.qwd_group)
+        qwd(w_main)
         comm.tlq_hs_reduce_scatter(grad, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
 
     def barrier():
@@ -360,8 +370,7 @@ def run_sdp4(a, rank, world, local_rank):
     # each collective alone (K steps each): effective pre-quantization GB/s and, with the P2P
     # transport, the NVLink bytes this rank moves against the 900 GB/s per-direction NVLink 5
     # figure the north star names (the fused kernels are the collectives: no NCCL kernel runs)
-    t_qwd = timed(lambda: (comm.qwd_quantize(w_main, w_model, ws_q, a.bits_w, a.qwd_group),
-                           comm.qwd_allgather_apply(ws_q, w_model, a.bits_w, a.qwd_group)), a.steps)
+    t_qwd = timed(lambda: qwd(w_main), a.steps)
     t_tlq = timed(lambda: comm.tlq_hs_reduce_scatter(grad, out, ws_t, a.bits_intra, a.bits_inter, a.group,
                                                      a.hadamard, True), a.steps)
     nv_q = kernel_nvlink_bytes("K2", D, S, P, M, N, a, transport)
@@ -394,6 +403,13 @@ def run_sdp4(a, rank, world, local_rank):
         t_unf = timed(unfused, max(3, a.steps // 2), 2)
         ablation = {"tlq_hs_fused_ms": round(t_tlq, 4), "tlq_hs_unfused_hadamard_ms": round(t_unf, 4),
                     "fusion_speedup": round(t_unf / t_tlq, 3)}
+    if not a.no_comparators:   # qWD as two calls (K2 applies every unit, the owner's included)
+        def qwd_two():
+            comm.qwd_quantize(w_main, w_model, ws_q, a.bits_w, a.qwd_group)
+            comm.qwd_allgather_apply(ws_q, w_model, a.bits_w, a.qwd_group)
+        t_two = timed(qwd_two, a.steps, 1)
+        ablation = dict(ablation or {}, qwd_step_ms=round(t_qwd, 4), qwd_two_call_ms=round(t_two, 4),
+                        qwd_own_fusion_speedup=round(t_two / t_qwd, 3))
         del hbuf, red, out2
 
     # unquantized NCCL comparators on the same buffers (sec. 2.1), N > 1 only
@@ -467,8 +483,7 @@ def run_sdp4(a, rank, world, local_rank):
                 ev["in_ready"][sl].record(s_in)
             comp.wait_event(ev["in_ready"][sl])
             comp.wait_event(ev["out_free"][sl])
-            comm.qwd_quantize(wmn[sl], w_model, ws_q, a.bits_w, a.qwd_group)
-            comm.qwd_allgather_apply(ws_q, w_model, a.bits_w, a.qwd_group)
+            qwd(wmn[sl])
             comm.tlq_hs_reduce_scatter(gd[sl], outs[sl], ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
             ev["in_free"][sl].record(comp)
             ev["out_ready"][sl].record(comp)
@@ -510,6 +525,7 @@ def run_sdp4(a, rank, world, local_rank):
                            "transport": comm.transport if world > 1 else "local",
                            "intra_pull": a.intra_pull or ("auto: " + ("0/1" if N <= 2 else "1/2")),
                            "G_w": a.qwd_group, "hadamard_block": a.hadamard,
+                           "qwd_call": "two calls" if a.qwd_two_call else "sdp4_qwd_step",
                            "bits": {"qwd": a.bits_w, "intra": a.bits_intra, "inter": a.bits_inter},
                            "grad_dtype": a.grad_dtype, "model_dtype": a.model_dtype,
                            "l2": "inputs larger than L2 (>= 2.6 GB per tensor), no flush",

@@ -180,6 +180,18 @@ sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t comm, void* workspace, size_t w
                                      size_t numel, int bits, int group, void* w_model_full,
                                      sdp4_dtype model_dtype, void* stream);
 
+/* Alg. 2 l.2-5 in one call: the same result as sdp4_qwd_quantize followed by
+ * sdp4_qwd_allgather_apply, bit for bit, with the owner's own update fused into the quantize
+ * kernel: K1 holds widen(w_model[r]) and the codes of d~[r] in registers, so it also writes
+ *   w_model[r] <- bf16_rn(widen(w_model[r]) + code * rn(s / q_k))
+ * (K2's arithmetic, element by element) and K2 then applies only the P - 1 other units.
+ * Saves one read of the replica shard and of unit r per step (at P = 1, K2 does not run).
+ * w_model_full is read and written (shard r by K1, the others by K2); all other arguments,
+ * the workspace and the errors are those of the two calls.  The wire unit r is identical. */
+sdp4_status sdp4_qwd_step(sdp4_comm_t comm, const float* w_main_shard, void* w_model_full,
+                          sdp4_dtype model_dtype, size_t numel, int bits, int group, sdp4_round rnd,
+                          uint64_t seed, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Ablation baselines: the codecs SDP4Bit is compared against.
  * ------------------------------------------------------------------------- */

@@ -636,7 +636,8 @@ namespace {
 // Alg. 2 l.2-3 (qWD, diff) or Alg. 1's "Quantize weights" (qW, !diff: w_model_full unused).
 sdp4_status weight_quantize(sdp4_comm_t c, bool diff, const float* w_main_shard, const void* w_model_full,
                             sdp4_dtype model_dtype, size_t numel, int bits, int group, sdp4_round rnd, uint64_t seed,
-                            void* workspace, size_t workspace_bytes, void* stream, const char* kname) {
+                            void* workspace, size_t workspace_bytes, void* stream, const char* kname,
+                            bool apply_own = false) {
   g_err.clear();
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (!valid_round(rnd)) return fail(SDP4_EINVAL, "bad rounding mode %d", (int)rnd);
@@ -673,7 +674,7 @@ sdp4_status weight_quantize(sdp4_comm_t c, bool diff, const float* w_main_shard,
     for (int q = 0; q < c->world; ++q) all[q] = q;
     s = launch(c, kname, st, [&] {
       return sdp4::launch_qwd_quantize(w_main_shard, shard_of(0), model_dtype, S, bits, group, d, sr, key,
-                                       (uint64_t)c->rank * S, c->sm_count, st);
+                                       (uint64_t)c->rank * S, c->sm_count, st, apply_own);
     });
     if (s != SDP4_OK) return s;
     return signal_peers(c, st, c->sym_qwd, 0, all, ep);
@@ -687,7 +688,7 @@ sdp4_status weight_quantize(sdp4_comm_t c, bool diff, const float* w_main_shard,
     d.p[0] = region + (size_t)c->rank * W;
     s = launch(c, kname, st, [&] {
       return sdp4::launch_qwd_quantize(w_main_shard + ch.off, shard_of(ch.off), model_dtype, ch.len, bits, group, d,
-                                       sr, key, (uint64_t)c->rank * S + ch.off, sms, st);
+                                       sr, key, (uint64_t)c->rank * S + ch.off, sms, st, apply_own);
     });
     if (s != SDP4_OK) return s;
     region += (size_t)c->world * W;
@@ -697,7 +698,8 @@ sdp4_status weight_quantize(sdp4_comm_t c, bool diff, const float* w_main_shard,
 
 // Alg. 2 l.4-5 (qWD: add) or Alg. 1's "AllGather" + dequantize (qW: assign).
 sdp4_status weight_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes, size_t numel, int bits, int group,
-                         void* w_model_full, sdp4_dtype model_dtype, void* stream, bool add, const char* kname) {
+                         void* w_model_full, sdp4_dtype model_dtype, void* stream, bool add, const char* kname,
+                         bool skip_own = false) {
   g_err.clear();
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (!valid_wbits(bits)) return fail(SDP4_EINVAL, "bits %d not in {2, 4, 8, 32}", bits);
@@ -716,6 +718,7 @@ sdp4_status weight_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes,
   const int sms = c->sms(overlap);
   const int P = c->world;
   if (P > sdp4::kMaxDests) return fail(SDP4_EINVAL, "world %d > %d", P, sdp4::kMaxDests);
+  if (skip_own && P == 1) return SDP4_OK;  // the only unit was applied by K1 (flags are >= waits)
   if (c->transport == kTransportP2P) {  // wait for every rank's unit; K2 pulls unit j from rank j
     const uint32_t ep = c->epoch_qwd;
     std::vector<int> all(P);
@@ -727,7 +730,7 @@ sdp4_status weight_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes,
     for (int q = 0; q < P; ++q) u.p[q] = sym_region(c->sym_qwd, q, ep);
     return launch(c, kname, st, [&] {
       return sdp4::launch_qwd_apply(u, P, S, S, bits, group, w_model_full, model_dtype, add, c->sm_count, st,
-                                    c->rank);
+                                    c->rank, skip_own);
     });
   }
   if (P > 1) c->link(st, c->side);  // the units of every chunk were written on st (K1)
@@ -748,7 +751,8 @@ sdp4_status weight_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes,
     u.remote = 0;
     for (int q = 0; q < P && q < sdp4::kMaxDests; ++q) u.p[q] = region + (size_t)q * W;
     s = launch(c, kname, st, [&] {
-      return sdp4::launch_qwd_apply(u, P, ch.len, S, bits, group, wm, model_dtype, add, sms, st);
+      return sdp4::launch_qwd_apply(u, P, ch.len, S, bits, group, wm, model_dtype, add, sms, st,
+                                    skip_own ? c->rank : 0, skip_own);
     });
     if (s != SDP4_OK) return s;
     region += (size_t)P * W;
@@ -768,6 +772,16 @@ sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t c, void* workspace, size_t work
                                      int group, void* w_model_full, sdp4_dtype model_dtype, void* stream) {
   return weight_apply(c, workspace, workspace_bytes, numel, bits, group, w_model_full, model_dtype, stream, true,
                       "K2_qwd_apply");
+}
+
+sdp4_status sdp4_qwd_step(sdp4_comm_t c, const float* w_main_shard, void* w_model_full, sdp4_dtype model_dtype,
+                          size_t numel, int bits, int group, sdp4_round rnd, uint64_t seed, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  sdp4_status s = weight_quantize(c, true, w_main_shard, w_model_full, model_dtype, numel, bits, group, rnd, seed,
+                                  workspace, workspace_bytes, stream, "K1_qwd_quantize", true);
+  if (s != SDP4_OK) return s;
+  return weight_apply(c, workspace, workspace_bytes, numel, bits, group, w_model_full, model_dtype, stream, true,
+                      "K2_qwd_apply", true);
 }
 
 sdp4_status sdp4_qw_quantize(sdp4_comm_t c, const float* w_main_shard, size_t numel, int bits, int group,

@@ -560,15 +560,37 @@ struct TileIter {
 // per G-group s = max|d|, codes = RNE(d * rn(q/s)) (R3: fused, exact product).  8 elements per
 // thread, a group is G/8 consecutive threads.  Output: one wire unit [codes][scales].
 // DIFF = false is the qW ablation codec (Alg. 1, QSDP / ZeRO++): d = w_main itself.
+// APPLY: the owner also applies its own unit to its replica shard here (Alg. 2 l.5 for
+// j = rank), decoding the codes it just packed with K2's exact arithmetic, so the replica
+// shard it already holds in registers is not read again by K2 (sdp4_qwd_step).
 // =====================================================================================
 constexpr int kVecThreads = 256;  // K1 / K2: 256-thread CTAs, kVecCtas per SM (persistent)
+
+// w[i] = rn(m[i] + x[i]) for 8 replica elements (m = widen(w) already in registers), stored
+// with one 16-byte (bf16) or two 16-byte (fp32) stores -- K2's update, element by element.
+template <typename TM>
+__device__ __forceinline__ void apply_own(TM* w, const float* m, const float* x) {
+  if constexpr (sizeof(TM) == 2) {
+    uint4 o;
+    uint32_t* ow = &o.x;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ow[i] = pack_bf16x2(__fadd_rn(m[2 * i], x[2 * i]), __fadd_rn(m[2 * i + 1], x[2 * i + 1]));
+    *reinterpret_cast<uint4*>(w) = o;
+  } else {
+    reinterpret_cast<float4*>(w)[0] = make_float4(__fadd_rn(m[0], x[0]), __fadd_rn(m[1], x[1]), __fadd_rn(m[2], x[2]),
+                                                  __fadd_rn(m[3], x[3]));
+    reinterpret_cast<float4*>(w)[1] = make_float4(__fadd_rn(m[4], x[4]), __fadd_rn(m[5], x[5]), __fadd_rn(m[6], x[6]),
+                                                  __fadd_rn(m[7], x[7]));
+  }
+}
 constexpr int kVecCtas = 8;
 
-template <typename TM, int BITS, bool DIFF>
+template <typename TM, int BITS, bool DIFF, bool APPLY>
 __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __restrict__ w_main,
-                                                                   const TM* __restrict__ w_model, size_t S,
+                                                                   TM* __restrict__ w_model, size_t S,
                                                                    int lg, const Dests dst, const SR sr,
-                                                                   uint64_t idx0) {
+                                                                   uint64_t idx0, float z) {
+  static_assert(!APPLY || DIFF, "the owner's apply is the qWD update");
   constexpr int TILE = kVecThreads * 8;
   __shared__ float red[kVecThreads / 32];
   constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
@@ -576,26 +598,39 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
   const size_t ntiles = (S + TILE - 1) / TILE;
   const size_t sc_off = S * (BITS == 32 ? 4 : BITS) / 8;
   const int t = threadIdx.x;
+  // the next tile's inputs are loaded before this tile's arithmetic (one tile of prefetch)
+  float4 na0, na1;
+  uint4 nu0, nu1;
+  auto load = [&](size_t tile) {
+    const size_t e = tile * TILE + t * 8;
+    if (tile < ntiles && e < S) {
+      na0 = *reinterpret_cast<const float4*>(w_main + e);
+      na1 = *reinterpret_cast<const float4*>(w_main + e + 4);
+      if constexpr (DIFF) {
+        nu0 = *reinterpret_cast<const uint4*>(w_model + e);
+        if constexpr (sizeof(TM) == 4) nu1 = *reinterpret_cast<const uint4*>(w_model + e + 4);
+      }
+    }
+  };
+  load(blockIdx.x);
   for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const size_t e0 = tile * TILE + t * 8;
     const bool act = e0 < S;
-    float d[8];
+    const float4 a0 = na0, a1 = na1;
+    const uint4 u0 = nu0, u1 = nu1;
+    load(tile + gridDim.x);
+    float d[8], m[8];
     if (act) {
-      const float4 a0 = *reinterpret_cast<const float4*>(w_main + e0);
-      const float4 a1 = *reinterpret_cast<const float4*>(w_main + e0 + 4);
-      float m[8];
       if constexpr (!DIFF) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) m[i] = 0.f;
       } else if constexpr (sizeof(TM) == 2) {
-        const uint4 u = *reinterpret_cast<const uint4*>(w_model + e0);
-        m[0] = bf16_lo(u.x); m[1] = bf16_hi(u.x); m[2] = bf16_lo(u.y); m[3] = bf16_hi(u.y);
-        m[4] = bf16_lo(u.z); m[5] = bf16_hi(u.z); m[6] = bf16_lo(u.w); m[7] = bf16_hi(u.w);
+        m[0] = bf16_lo(u0.x); m[1] = bf16_hi(u0.x); m[2] = bf16_lo(u0.y); m[3] = bf16_hi(u0.y);
+        m[4] = bf16_lo(u0.z); m[5] = bf16_hi(u0.z); m[6] = bf16_lo(u0.w); m[7] = bf16_hi(u0.w);
       } else {
-        const float4 b0 = *reinterpret_cast<const float4*>(w_model + e0);
-        const float4 b1 = *reinterpret_cast<const float4*>(w_model + e0 + 4);
-        m[0] = b0.x; m[1] = b0.y; m[2] = b0.z; m[3] = b0.w;
-        m[4] = b1.x; m[5] = b1.y; m[6] = b1.z; m[7] = b1.w;
+        m[0] = __uint_as_float(u0.x); m[1] = __uint_as_float(u0.y); m[2] = __uint_as_float(u0.z);
+        m[3] = __uint_as_float(u0.w); m[4] = __uint_as_float(u1.x); m[5] = __uint_as_float(u1.y);
+        m[6] = __uint_as_float(u1.z); m[7] = __uint_as_float(u1.w);
       }
       if constexpr (DIFF) {
         d[0] = __fsub_rn(a0.x, m[0]); d[1] = __fsub_rn(a0.y, m[1]);
@@ -617,6 +652,9 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
           o[0] = make_float4(d[0], d[1], d[2], d[3]);
           o[1] = make_float4(d[4], d[5], d[6], d[7]);
         }
+      if constexpr (APPLY) {
+        if (act) apply_own<TM>(w_model + e0, m, d);
+      }
     } else {
       float a = 0.f;
 #pragma unroll
@@ -650,6 +688,15 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
           const float sv = stored_scale(a, 1.f);
           for (int k = 0; k < dst.n; ++k) reinterpret_cast<float*>(dst.p[k] + sc_off)[e0 >> lg] = sv;
         }
+        if constexpr (APPLY) {  // K2's update from the codes just packed: x = mulz(code, rn(s/q)), w += x
+          // r[i] holds code + 1.5*2^23 exactly (|code| <= q when p.ok), so code = r - 1.5*2^23:
+          // the value K2 decodes from the packed word; !p.ok packs zero codes
+          const float ds = __fdiv_rn(stored_scale(a, 1.f), q);
+          float f[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[i] = mulz(p.ok ? __fsub_rn(__uint_as_float(r[i]), kMagic) : 0.f, ds, z);
+          apply_own<TM>(w_model + e0, m, f);
+        }
       }
     }
   }
@@ -681,7 +728,8 @@ struct K2rCfg {
 
 template <typename TM, int BITS, bool ADD>
 __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply_ring(const Dests units, size_t S, size_t stride, int P,
-                                                                    int rot, int lg, TM* __restrict__ w_model, float z) {
+                                                                    int rot, int U, int lg, TM* __restrict__ w_model,
+                                                                    float z) {
   using C = K2rCfg<BITS>;
   constexpr int ROUNDS = kK2rTile / (kVecThreads * 8);
   constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
@@ -689,11 +737,12 @@ __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply_ring(const Dests uni
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kK2rStages * C::STAGE);
   const int t = threadIdx.x;
-  const size_t tpu = (S + kK2rTile - 1) / kK2rTile, ntiles = tpu * P;
+  // U units (U = P, or P - 1 when the owner applied its own in K1), unit fastest, starting at rot
+  const size_t tpu = (S + kK2rTile - 1) / kK2rTile, ntiles = tpu * U;
   const size_t sc_off = S * (BITS == 32 ? 4 : BITS) / 8;
-  auto tile_of = [&](size_t tile, size_t& ts, size_t& j) {  // unit fastest, rotated by this rank
-    ts = tile / P;
-    j = tile - ts * P + rot;
+  auto tile_of = [&](size_t tile, size_t& ts, size_t& j) {
+    ts = tile / U;
+    j = tile - ts * U + rot;
     if (j >= (size_t)P) j -= P;
   };
   if (t == 0) {
@@ -1452,6 +1501,13 @@ inline int grid_for(size_t ntiles, int cap) {
 }
 
 template <typename K>
+int occ_blocks(K kernel, int threads, size_t smem = 0) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem) != cudaSuccess || nb < 1) nb = 1;
+  return nb;
+}
+
+template <typename K>
 cudaError_t set_smem(K kernel, int bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
@@ -1576,20 +1632,29 @@ cudaError_t k4_launch(const uint8_t* recv, size_t in_unit_bytes, int N, int M, s
 // ------------------------------- launchers -------------------------------------------
 cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, int model_dtype,
                                 size_t S, int bits, int G, const Dests& dst, int sr_on, uint32_t sr_key,
-                                uint64_t idx0, int sms, cudaStream_t st) {
+                                uint64_t idx0, int sms, cudaStream_t st, bool apply_own) {
   const SR sr{sr_on, sr_key};
-  const int grid = grid_for((S + kVecThreads * 8 - 1) / (kVecThreads * 8), sms * kVecCtas);
-#define K1(TM, B, DF) \
-  k1_qwd_quantize<TM, B, DF><<<grid, kVecThreads, 0, st>>>(w_main, static_cast<const TM*>(w_model_shard), S, \
-                                                           __builtin_ctz(G), dst, sr, idx0)
-#define K1B(TM, DF) \
-  if (bits == 2) K1(TM, 2, DF); else if (bits == 4) K1(TM, 4, DF); else if (bits == 8) K1(TM, 8, DF); else K1(TM, 32, DF)
+  if (apply_own && !w_model_shard) return cudaErrorInvalidValue;
+  void* wm = const_cast<void*>(w_model_shard);  // written only by the APPLY variants
+  const size_t ntiles = (S + kVecThreads * 8 - 1) / (kVecThreads * 8);
+  // persistent grid: as many CTAs per SM as the variant's registers allow (at most kVecCtas)
+#define K1(TM, B, DF, AP)                                                                                    \
+  do {                                                                                                       \
+    static const int nb = std::min(kVecCtas, occ_blocks(k1_qwd_quantize<TM, B, DF, AP>, kVecThreads));      \
+    k1_qwd_quantize<TM, B, DF, AP><<<grid_for(ntiles, sms * nb), kVecThreads, 0, st>>>(                      \
+        w_main, static_cast<TM*>(wm), S, __builtin_ctz(G), dst, sr, idx0, -0.0f);                            \
+  } while (0)
+#define K1B(TM, DF, AP)                 \
+  if (bits == 2) K1(TM, 2, DF, AP);     \
+  else if (bits == 4) K1(TM, 4, DF, AP); \
+  else if (bits == 8) K1(TM, 8, DF, AP); \
+  else K1(TM, 32, DF, AP)
   if (!w_model_shard) {
-    K1B(float, false);
+    K1B(float, false, false);
   } else if (model_dtype == kBF16) {
-    K1B(uint16_t, true);
+    if (apply_own) { K1B(uint16_t, true, true); } else { K1B(uint16_t, true, false); }
   } else {
-    K1B(float, true);
+    if (apply_own) { K1B(float, true, true); } else { K1B(float, true, false); }
   }
 #undef K1B
 #undef K1
@@ -1597,13 +1662,16 @@ cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, 
 }
 
 cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride, int bits, int G, void* w_model,
-                             int model_dtype, bool add, int sms, cudaStream_t st, int rot) {
-  const int grid_r = grid_for((S + kK2rTile - 1) / kK2rTile * P, sms * 4);
+                             int model_dtype, bool add, int sms, cudaStream_t st, int rot, bool skip_rot) {
+  const int U = skip_rot ? P - 1 : P;  // skip_rot: unit `rot` was applied by its owner's K1
+  if (skip_rot) rot = (rot + 1) % P;
+  if (U <= 0 || S == 0) return cudaSuccess;
+  const int grid_r = grid_for((S + kK2rTile - 1) / kK2rTile * U, sms * 4);
 #define K2(TM, B, AD)                                                                          \
   do {                                                                                                 \
     set_smem(k2_qwd_apply_ring<TM, B, AD>, K2rCfg<B>::SMEM);                                           \
     k2_qwd_apply_ring<TM, B, AD><<<grid_r, kVecThreads, K2rCfg<B>::SMEM, st>>>(                         \
-        units, S, stride, P, rot % P, __builtin_ctz(G), static_cast<TM*>(w_model), -0.0f);             \
+        units, S, stride, P, rot % P, U, __builtin_ctz(G), static_cast<TM*>(w_model), -0.0f);          \
   } while (0)
 #define K2B(TM, AD) \
   if (bits == 2) K2(TM, 2, AD); else if (bits == 4) K2(TM, 4, AD); else if (bits == 8) K2(TM, 8, AD); else K2(TM, 32, AD)

@@ -31,15 +31,19 @@ struct Dests {
 // into the wire unit at every destination dst.p[0..n) (n = 1: local; n = P: all-gather push).
 // w_model_shard = nullptr: the qW codec (Alg. 1), d = w_main.  bits in {2, 4, 8, 32}.
 // sr_on: stochastic rounding (R14) with key sr_key; element e has global index idx0 + e.
+// apply_own: also w_model_shard += dequant(own unit) in place (Alg. 2 l.5 for this shard,
+// K2's arithmetic); K2 then runs with skip_rot.
 cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, int model_dtype,
                                 size_t S, int bits, int G, const Dests& dst, int sr_on, uint32_t sr_key,
-                                uint64_t idx0, int sms, cudaStream_t st);
+                                uint64_t idx0, int sms, cudaStream_t st, bool apply_own = false);
 
 // K2: Alg. 2 l.5 -- for every shard j < P: w_model[j*stride ..+S] += dequant(unit units.p[j])
 // (local or peer memory), in place.  add = false (qW): w_model[...] = dequant(unit), no read.
 // Tiles are visited unit-fastest, starting at unit `rot` (this rank: spreads the P2P pulls).
+// skip_rot: unit `rot` is not applied (its owner did it in K1 with apply_own); P = 1 -> no launch.
 cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride, int bits, int G, void* w_model,
-                             int model_dtype, bool add, int sms, cudaStream_t st, int rot = 0);
+                             int model_dtype, bool add, int sms, cudaStream_t st, int rot = 0,
+                             bool skip_rot = false);
 
 // K6: one hop of the ring reduce-scatter with per-hop quantization (sec. 2.3, ablation):
 // acc = (recv ? rn(dequant(recv) + g) : g) over S elements of one chunk (grad dtype);

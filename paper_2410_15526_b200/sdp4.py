@@ -47,6 +47,7 @@ SIGNATURES = {
     "sdp4_tlq_workspace_offset": (_c_size, [_ci, _ci, _c_size, _ci, _ci, _ci, _ci]),
     "sdp4_qwd_quantize": (_ci, [_vp, _vp, _vp, _ci, _c_size, _ci, _ci, _ci, _u64, _vp, _c_size, _vp]),
     "sdp4_qwd_allgather_apply": (_ci, [_vp, _vp, _c_size, _c_size, _ci, _ci, _vp, _ci, _vp]),
+    "sdp4_qwd_step": (_ci, [_vp, _vp, _vp, _ci, _c_size, _ci, _ci, _ci, _u64, _vp, _c_size, _vp]),
     "sdp4_qw_quantize": (_ci, [_vp, _vp, _c_size, _ci, _ci, _ci, _u64, _vp, _c_size, _vp]),
     "sdp4_qw_allgather_apply": (_ci, [_vp, _vp, _c_size, _c_size, _ci, _ci, _vp, _ci, _vp]),
     "sdp4_ring_workspace_bytes": (_c_size, [_ci, _c_size, _ci, _ci]),
@@ -252,6 +253,16 @@ class Comm:
                             group: int = 128, stream=None):
         _check(lib().sdp4_qwd_allgather_apply(self._h, _ptr(workspace), _nbytes(workspace), w_model.numel(), bits,
                                               group, _ptr(w_model), _DT[w_model.dtype], _stream(stream)))
+
+    def qwd_step(self, w_main_shard: torch.Tensor, w_model: torch.Tensor, workspace: Optional[torch.Tensor],
+                 bits: int = 4, group: int = 128, seed=None, stream=None):
+        """Alg. 2 l.2-5 in one call (qwd_quantize + qwd_allgather_apply, bit-identical), the
+        owner's own update fused into K1."""
+        if w_main_shard.dtype != torch.float32:
+            raise TypeError("w_main_shard must be fp32 (P:211)")
+        _check(lib().sdp4_qwd_step(self._h, _ptr(w_main_shard), _ptr(w_model), _DT[w_model.dtype], w_model.numel(),
+                                   bits, group, RNE if seed is None else STOCHASTIC, seed or 0, _ptr(workspace),
+                                   _nbytes(workspace), _stream(stream)))
 
     # -- ablation baselines (SURVEY NEXT-3) ---------------------------------------------
     def qw_quantize(self, w_main_shard: torch.Tensor, numel: int, workspace: Optional[torch.Tensor], bits: int = 4,

@@ -3,7 +3,7 @@
     torchrun --nproc-per-node P --master-addr 127.0.0.1 tests/dist_parity.py [--groups M]
 
 Every rank draws all P ranks' synthetic inputs (seeded, CPU), runs
-  qWD:    sdp4_qwd_quantize + sdp4_qwd_allgather_apply  (ncclAllGather)
+  qWD:    sdp4_qwd_quantize + sdp4_qwd_allgather_apply  (ncclAllGather), and sdp4_qwd_step
   TLq-HS: sdp4_tlq_hs_reduce_scatter                     (2 x ncclAlltoAll, intra/inter split)
 through the C ABI, and checks against the oracle (bit-exact codes/outputs), plus the
 replica identity of w_model across ranks, and the ablation baselines (qW all-gather,
@@ -89,8 +89,7 @@ def run_full(comm, rank, P, M, N, G=128, b=64, win=16384, nwin=6):
     ws_q = torch.empty(comm.qwd_workspace_bytes(D, 4, G), dtype=torch.uint8, device=dev)
     ws_t = torch.empty(comm.tlq_workspace_bytes(D, 8, 4, G), dtype=torch.uint8, device=dev)
     out = torch.empty(S, dtype=torch.float32, device=dev)
-    comm.qwd_quantize(w_main, w_model, ws_q, 4, G)
-    comm.qwd_allgather_apply(ws_q, w_model, 4, G)
+    comm.qwd_step(w_main, w_model, ws_q, 4, G)   # the call bench.py times
     comm.tlq_hs_reduce_scatter(grad, out, ws_t, 8, 4, G, b, True)
     torch.cuda.synchronize()
     del grad, ws_q, ws_t
@@ -153,6 +152,14 @@ def run_checks(comm, rank, P, M, N, G, b, S, seed=None):
     if len({int(x.item()) for x in hs}) != 1:
         ok = False
         msgs.append("w_model replicas differ across ranks")
+    # the same iteration in one call (owner's update fused into K1, K2 skips unit `rank`)
+    wm = w_model.cuda()
+    comm.qwd_step(mains[rank].cuda(), wm, ws, 4, G, seed=seed)
+    torch.cuda.synchronize()
+    got = synth.bf16_bits(wm.cpu())
+    if not np.array_equal(got, want):
+        ok = False
+        msgs.append(f"qwd_step replica differs from oracle in {int(np.sum(got != want))} elements")
 
     # ---- TLq-HS (Alg. 3)
     for dtype in (torch.bfloat16, torch.float32):

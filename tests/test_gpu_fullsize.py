@@ -46,8 +46,7 @@ def run():
     ws_q = torch.empty(comm.qwd_workspace_bytes(D, BITS_W, GW), dtype=torch.uint8, device=dev)
     ws_t = torch.empty(comm.tlq_workspace_bytes(D, BI, BE, G), dtype=torch.uint8, device=dev)
     out = torch.empty(D, dtype=torch.float32, device=dev)
-    comm.qwd_quantize(w_main, w_model, ws_q, BITS_W, GW)
-    comm.qwd_allgather_apply(ws_q, w_model, BITS_W, GW)
+    comm.qwd_step(w_main, w_model, ws_q, BITS_W, GW)   # the call bench.py times
     comm.tlq_hs_reduce_scatter(grad, out, ws_t, BI, BE, G, B, True)
     torch.cuda.synchronize()
     yield dict(D=D, w_model0=wm0, w_model=w_model, w_main=w_main, grad=grad, out=out, ws_q=ws_q, ws_t=ws_t)

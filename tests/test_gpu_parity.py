@@ -226,3 +226,58 @@ def test_tiny_buffers(comm, D, G, b):
     (codes, scales), want_new = oracle_qwd(w_main, w_model, 4, G)
     assert_unit_equal(unit, codes, scales, 4, G, D, "tiny qWD unit")
     assert bf16_equal(synth.bf16_bits(new), want_new)
+
+
+# ------------------------------------------- qWD in one call (owner's update fused into K1)
+def run_qwd_step(comm, w_main, w_model, bits, G, seed=None):
+    D = w_model.numel()
+    ws = torch.zeros(comm.qwd_workspace_bytes(D, bits, G), dtype=torch.uint8, device="cuda")
+    wm = w_model.cuda()
+    comm.qwd_step(w_main.cuda(), wm, ws, bits, G, seed=seed)
+    torch.cuda.synchronize()
+    return ws.cpu().numpy().copy(), wm.cpu()
+
+
+@pytest.mark.parametrize("model_dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("bits,G,seed", [(4, 128, None), (4, 32, None), (8, 256, None), (32, 128, None),
+                                         (4, 2048, None), (4, 128, 5), (8, 32, 2 ** 40 + 3)])
+def test_qwd_step_parity(comm, model_dtype, bits, G, seed):
+    # Alg. 2 l.2-5 in one call: the unit and the replica equal the oracle's bit for bit
+    D = max(G, 64) * 41 + (0 if G >= 2048 else max(G, 64) * 5)
+    w_model = synth.model_weights(D, seed=21, dtype=model_dtype)
+    w_main = synth.main_weights(w_model, seed=22, lr=2e-4)
+    unit, new = run_qwd_step(comm, w_main, w_model, bits, G, seed)
+    (codes, scales), want_new = oracle_qwd(w_main, w_model, bits, G, seed)
+    assert_unit_equal(unit, codes, scales, bits, G, D, "qwd_step unit")
+    if model_dtype == torch.bfloat16:
+        assert bf16_equal(synth.bf16_bits(new), want_new)
+    else:
+        assert f32_equal(new.numpy(), want_new)
+
+
+@pytest.mark.parametrize("G", [32, 128])
+def test_qwd_step_edge_cases(comm, G):
+    # zero / tiny / NaN / Inf / huge / tie groups: the fused update decodes what it packed
+    x = synth.edge_case_groups(G)
+    D = x.numel()
+    for dt in (torch.float32, torch.bfloat16):
+        w_model = torch.zeros(D, dtype=dt)
+        unit, new = run_qwd_step(comm, x, w_model, 4, G)
+        (codes, scales), want_new = oracle_qwd(x, w_model, 4, G)
+        assert_unit_equal(unit, codes, scales, 4, G, D, "qwd_step edge unit")
+        if dt == torch.bfloat16:
+            assert bf16_equal(synth.bf16_bits(new), want_new)
+        else:
+            assert f32_equal(new.numpy(), want_new)
+
+
+def test_qwd_step_launches(comm):
+    # at P = 1 the step is K1 alone (no K2 launch: the only unit is the owner's)
+    D = 8192 * 3
+    w_model = synth.model_weights(D, seed=3).cuda()
+    w_main = synth.main_weights(w_model.cpu(), seed=4).cuda()
+    ws = torch.zeros(comm.qwd_workspace_bytes(D, 4, 128), dtype=torch.uint8, device="cuda")
+    n0 = comm.launch_count()
+    comm.qwd_step(w_main, w_model, ws)
+    torch.cuda.synchronize()
+    assert comm.launch_count() - n0 == 1
