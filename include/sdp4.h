@@ -39,7 +39,9 @@ typedef enum {
   SDP4_EALIGN = 2, /* size/alignment rule violated (numel, G % b, pointer alignment)          */
   SDP4_ECUDA = 3,  /* a CUDA runtime error (launch failure, bad device pointer)                */
   SDP4_ENCCL = 4,  /* an NCCL error, including an asynchronous one from a previous call         */
-  SDP4_ESTATE = 5  /* workspace too small or comm unusable                                      */
+  SDP4_ESTATE = 5,  /* workspace too small, call out of order, or comm unusable                  */
+  SDP4_ETIMEOUT = 6 /* a P2P flag wait of an earlier call passed its deadline (a peer never
+                       signalled); the comm is unusable and must be destroyed                     */
 } sdp4_status;
 
 typedef enum { SDP4_F32 = 0, SDP4_BF16 = 1 } sdp4_dtype;
@@ -96,17 +98,39 @@ int sdp4_comm_chunks(sdp4_comm_t comm, size_t numel, int group);
 /* Host.  Transport of the exchanges (world > 1):
  *   0 NCCL: kernels write the caller's workspace; ncclAllGather / ncclAlltoAll move it
  *     (with the chunked two-stream pipeline above);
- *   1 P2P (default when available: N <= 8, P <= 64): the exchanges are fused into the
- *     kernels over NVLink (CUDA IPC): K3 and K4 push their quantized tiles straight into the
- *     receive buffers of the ranks that own them; the qWD all-gather is a pull inside K2
- *     (unit j read from rank j's buffer while the replica update streams HBM).  Those receive buffers are library-
- *     owned, symmetric, double-buffered by call parity and allocated collectively on first
- *     use (the caller's workspace is then unused and may be NULL / 0 bytes); completion is signalled per source with
- *     epoch flags (cuStreamWriteValue32 / cuStreamWaitValue32).
+ *   1 P2P (default when every rank can map every other rank's memory with CUDA IPC -- one OS
+ *     instance, peer access between the devices or ranks sharing one device -- and N <= 8,
+ *     P <= 64; checked collectively by sdp4_comm_init): the exchanges are fused into the
+ *     kernels over NVLink: K3 and K4 push their quantized tiles straight into the receive
+ *     regions of the ranks that own them; the qWD all-gather is a pull inside K2 (unit j read
+ *     from rank j's buffer while the replica update streams HBM).  The receive regions are
+ *     library-owned, symmetric and allocated collectively on first use (the caller's workspace
+ *     is then unused and may be NULL / 0 bytes).  Completion and reuse are signalled per
+ *     (stage, source) with binary flags: a producer raises data[stage][me] in the consumer's
+ *     buffer after its kernel, the consumer raises free[stage][me] in the producer's buffer
+ *     after consuming; each side waits for (and resets) the flag before its kernel.  No
+ *     host-side epoch: a P2P call captured in a CUDA graph replays correctly (make one eager
+ *     call of the same size first, so no buffer grows during capture: ESTATE otherwise).
+ *     P2P qWD allows one outstanding quantize per comm (quantize, apply, quantize, ...).
  * Results are bit-identical across transports (R16).  sdp4_comm_transport returns the
- * current one. */
+ * current one.  EINVAL for P2P if it is unavailable, for NCCL on a sdp4_comm_init_p2p comm. */
 sdp4_status sdp4_comm_set_transport(sdp4_comm_t comm, int transport);
 int sdp4_comm_transport(sdp4_comm_t comm);
+
+/* Host.  Deadline of every P2P flag wait (seconds; default 300, or SDP4_WAIT_TIMEOUT_S).  A
+ * wait is a one-warp polling kernel: if a peer has not signalled by the deadline (it died or
+ * skipped a collective call), the kernel writes a host-mapped error word and returns instead
+ * of blocking the stream forever; the next call on this comm (or sdp4_comm_check) returns
+ * SDP4_ETIMEOUT, and results of the timed-out call are garbage.  0: unbounded waits with
+ * stream memory operations (cuStreamWaitValue32), no kernel.  Ranks that share one GPU
+ * (sdp4_comm_init_p2p emulation) always wait with stream memory operations -- kernels of
+ * different processes are not guaranteed to run concurrently, so no kernel may wait for
+ * another rank -- and EINVAL is returned for seconds > 0. */
+sdp4_status sdp4_comm_set_timeout(sdp4_comm_t comm, double seconds);
+
+/* Host, no synchronization.  SDP4_OK, or the asynchronous error of an earlier call
+ * (SDP4_ETIMEOUT from a P2P wait, SDP4_ENCCL from NCCL) visible so far. */
+sdp4_status sdp4_comm_check(sdp4_comm_t comm);
 
 /* Host.  P2P transport only: how the intra all-to-all (Alg. 3 l.4) moves over NVLink.  Of
  * the K3 tiles (16384 elements of a shard) bound for another local rank, those with
@@ -121,8 +145,24 @@ sdp4_status sdp4_comm_set_intra_pull(sdp4_comm_t comm, int num, int den);
 /* Host, collective (every rank calls it).  Waits for this rank's work, then -- if symmetric
  * buffers were allocated -- barriers with the peers (they may still be pulling from this
  * rank's buffers) before unmapping and freeing them; destroys the NCCL communicators and
- * frees the comm. */
+ * frees the comm.  Call it explicitly on every rank (not from a garbage collector). */
 sdp4_status sdp4_comm_destroy(sdp4_comm_t comm);
+
+/* Host bootstrap callback of sdp4_comm_init_p2p: collective over the `world` ranks, blocking;
+ * gathers `bytes` bytes from every rank into recv (rank r's at recv + r * bytes).  Returns 0
+ * on success.  Called only from sdp4_comm_init_p2p, from calls that (re)allocate symmetric
+ * buffers, and from sdp4_comm_destroy, on the calling thread. */
+typedef int (*sdp4_host_allgather_fn)(const void* send, void* recv, size_t bytes, void* ctx);
+
+/* Host, collective.  A P2P-only comm bootstrapped WITHOUT NCCL: `allgather` (e.g. over a
+ * torch.distributed gloo group) exchanges the CUDA-IPC handles and reachability records.
+ * Every rank must reach every other through CUDA IPC (same OS instance; peer access between
+ * the devices) -- ranks may share ONE device, so P ranks (any M x N, N <= 8, P <= 64) run on a
+ * single GPU through exactly the product P2P path (NCCL refuses duplicate GPUs).  Binds to the
+ * current device.  The transport is P2P and cannot be changed; the NCCL comparators return
+ * ESTATE.  ESTATE if some rank cannot reach another. */
+sdp4_status sdp4_comm_init_p2p(sdp4_comm_t* out, int rank, int world, int groups_M, int group_size_N,
+                               sdp4_host_allgather_fn allgather, void* ctx);
 
 /* ---------------------------------------------------------------------------
  * Sizes and workspace layout (R15).  One "wire unit" carries n elements at k

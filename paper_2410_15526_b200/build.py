@@ -39,21 +39,36 @@ def needs_rebuild() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every source to an object in parallel (one nvcc per translation unit), then link."""
     if not force and not needs_rebuild():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     inc, lib = nccl_dirs()
-    cmd = [nvcc(), "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
-           "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "--fmad=false",
-           "-I", os.path.join(ROOT, "include"), "-I", inc]
+    flags = [nvcc(), "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
+             "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "--fmad=false",
+             "-I", os.path.join(ROOT, "include"), "-I", inc]
     if verbose:
-        cmd += ["-Xptxas", "-v"]
-    cmd += [os.path.join(CSRC, s) for s in SOURCES]
-    cmd += ["-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}", "-o", LIB + ".tmp"]
+        flags += ["-Xptxas", "-v"]
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        cmd = flags + ["-c", os.path.join(CSRC, src), "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+        if verbose:
+            sys.stderr.write(r.stderr)
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a"] + objs + \
+        ["-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}", "-o", LIB + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc link failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

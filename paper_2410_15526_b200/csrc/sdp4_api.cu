@@ -13,16 +13,17 @@
 // Results are bit-identical for every C (tests/test_gpu_dist.py).
 //
 // Transports.  NCCL: kernels write local send buffers, NCCL moves them (the baseline).
-// P2P (default when world > 1): the producing kernel IS the exchange -- K1 stores its unit
-// into every rank's gather buffer, K3 stores each tile into the receive block of the local
-// rank that owns it, K4 stores each requantized unit into its node's receive slot, all
-// through CUDA-IPC-mapped peer memory over NVLink/NVSwitch, tile by tile while computing.
-// Receive buffers are library-owned, symmetric across ranks and double-buffered by call
-// parity; completion is signalled per (stage, source rank) with an epoch written into the
-// destination's flag word by cuStreamWriteValue32 after the producing kernel, and awaited
-// with cuStreamWaitValue32 before the consuming kernel (no spinning kernels).  Parity
-// double-buffering makes the write-after-read safe: a producer reuses a receive buffer two
-// calls later only after a flag the consumer raised after consuming it.
+// P2P (default when every rank reaches every other through CUDA IPC): the producing kernel IS
+// the exchange -- K1 publishes its unit in its own buffer and every K2 pulls it, K3 stores each
+// tile into the receive block of the local rank that owns it, K4 stores each requantized unit
+// into its node's receive slot, all through CUDA-IPC-mapped peer memory over NVLink/NVSwitch,
+// tile by tile while computing.  Receive regions are library-owned and symmetric across ranks;
+// completion and reuse are signalled with binary data/free flags (the sync protocol below):
+// raised by stream memory operations after the producing / consuming kernel, awaited by a
+// one-warp polling kernel with a deadline (or, with the timeout set to 0, by
+// cuStreamWaitValue32).  No host-side epoch: a captured CUDA graph replays correctly.
+// Ranks may share one GPU (sdp4_comm_init_p2p with a host bootstrap), which emulates any
+// M x N topology on a single device.
 #include "sdp4.h"
 
 #include <algorithm>
@@ -35,6 +36,8 @@
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -46,6 +49,7 @@ namespace {
 
 constexpr int kMaxChunks = 16;
 constexpr int kDefaultNcclCtas = 16;
+constexpr double kDefaultTimeoutS = 300.0;  // P2P flag waits (SDP4_WAIT_TIMEOUT_S; 0 = unbounded memop waits)
 
 thread_local std::string g_err;
 
@@ -120,8 +124,14 @@ size_t qwd_total(int P, size_t S, int bits, int group, int C) {
 }  // namespace
 
 // Library-owned receive buffer, mapped on every rank (CUDA IPC).  Layout:
-// [flags: kFlagBytes][parity 0 region][parity 1 region].
-constexpr size_t kFlagBytes = 64 * 256 * 4;  // flags[stage][src] uint32, stage < 64, src < 256
+// [flags: kFlagBytes][region].  Flags are binary words flag[kind][stage][src] (see the sync
+// protocol below); one region, reused every call.
+constexpr int kFlagStages = 64, kFlagSrcs = 256;
+constexpr size_t kFlagBytes = 2 * (size_t)kFlagStages * kFlagSrcs * sizeof(uint32_t);
+enum FlagKind { kData = 0, kFree = 1 };
+inline size_t flag_off(int kind, int stage, int src) {
+  return (((size_t)kind * kFlagStages + stage) * kFlagSrcs + src) * sizeof(uint32_t);
+}
 struct SymBuf {
   uint8_t* local = nullptr;
   size_t bytes = 0, region = 0;
@@ -130,11 +140,34 @@ struct SymBuf {
 
 enum Transport { kTransportNccl = 0, kTransportP2P = 1 };
 
+// Host-side allgather the library uses for its own bootstrap (IPC handles, reachability,
+// barriers): the caller's callback (sdp4_comm_init_p2p), else ncclAllGather on the world comm.
+typedef int (*HostAllgather)(const void* send, void* recv, size_t bytes, void* ctx);
+
+// What a rank tells its peers at init so that each can decide whether CUDA IPC reaches them:
+// the same OS instance (host name + kernel boot id) and a device this process can map.
+struct PeerInfo {
+  char host[96];
+  unsigned char uuid[16];
+  int pid;
+};
+
 struct sdp4_comm {
   int rank = 0, world = 1, M = 1, N = 1, m = 0, l = 0;
   int transport = kTransportNccl;
+  bool p2p_ok = false;  // every rank reaches every other through CUDA IPC (same host, P2P-capable)
+  bool shared_gpu = false;  // some ranks share a device: flag waits must not be polling kernels
+  HostAllgather ag_fn = nullptr;
+  void* ag_ctx = nullptr;
   SymBuf sym_qwd, sym_tlq, sym_ring;
-  uint32_t epoch_qwd = 0, epoch_tlq = 0, epoch_ring = 0;
+  struct QwdPending {  // P2P: the unit K1 published and K2 has not yet consumed
+    bool valid = false;
+    size_t numel = 0;
+    int bits = 0, group = 0;
+  } qwd_pending;
+  unsigned long long timeout_ns = 0;  // > 0: flag waits are polling kernels with this deadline
+  uint32_t* err_host = nullptr;       // host-mapped error word written by a timed-out wait
+  uint32_t* err_dev = nullptr;
   PFN_cuStreamWriteValue32_v11070 write_value = nullptr;
   PFN_cuStreamWaitValue32_v11070 wait_value = nullptr;
   PFN_cuStreamBatchMemOp_v11070 batch_memop = nullptr;  // all flag writes / waits of a step in one call
@@ -232,7 +265,16 @@ sdp4_status nccl_op(sdp4_comm* c, const char* name, cudaStream_t st, F&& f) {
   return SDP4_OK;
 }
 
+// Errors raised asynchronously by earlier calls: NCCL's, and a P2P flag wait that timed out
+// (the comm is then unusable: the exchange it guarded never completed).
 sdp4_status async_check(sdp4_comm* c) {
+  if (c->err_host) {
+    const uint32_t e = *reinterpret_cast<volatile uint32_t*>(c->err_host);
+    if (e)
+      return fail(SDP4_ETIMEOUT, "a P2P wait timed out: %s flag of stage %u from rank %u never arrived; the comm is "
+                                 "unusable (destroy it)",
+                  ((e >> 24) & 1) ? "free" : "data", (e >> 16) & 0xff, e & 0xffff);
+  }
   ncclComm_t cs[3] = {c->world_c, c->intra, c->inter};
   for (ncclComm_t x : cs) {
     if (!x) continue;
@@ -244,130 +286,287 @@ sdp4_status async_check(sdp4_comm* c) {
   return SDP4_OK;
 }
 
-// Collectively (re)allocate a symmetric buffer with two parity regions of `region` bytes.
-sdp4_status sym_ensure(sdp4_comm* c, SymBuf& b, size_t region, uint32_t* epoch) {
-  if (b.local && region <= b.region) return SDP4_OK;
-  region = round_up(region + region / 16, 1 << 21);
-  cudaError_t e = cudaDeviceSynchronize();  // no kernel of ours still touches the old buffers
-  if (e != cudaSuccess) return fail(SDP4_ECUDA, "sync before symmetric alloc: %s", cudaGetErrorString(e));
-  int* tok = nullptr;
-  cudaMalloc(&tok, sizeof(int) * 64);
-  if (b.local) {  // every rank reached this point: peers are done with the old buffers
-    ncclResult_t r = ncclAllReduce(tok, tok, 1, ncclInt32, ncclSum, c->world_c, c->side);
-    cudaStreamSynchronize(c->side);
-    if (r != ncclSuccess) return fail(SDP4_ENCCL, "barrier: %s", ncclGetErrorString(r));
-    for (int q = 0; q < c->world; ++q)
-      if (q != c->rank && b.peer[q]) cudaIpcCloseMemHandle(b.peer[q]);
-    cudaFree(b.local);
-    b = SymBuf();
-  }
-  const size_t bytes = kFlagBytes + 2 * region;
-  if ((e = cudaMalloc(&b.local, bytes)) != cudaSuccess) {
-    cudaFree(tok);
-    return fail(SDP4_ECUDA, "symmetric buffer of %zu bytes: %s", bytes, cudaGetErrorString(e));
-  }
-  cudaMemset(b.local, 0, kFlagBytes);
-  b.bytes = bytes;
-  b.region = region;
-  *epoch = 0;
-  cudaIpcMemHandle_t h;
-  if ((e = cudaIpcGetMemHandle(&h, b.local)) != cudaSuccess) return fail(SDP4_ECUDA, "ipc handle: %s", cudaGetErrorString(e));
-  uint8_t* dh = nullptr;
-  cudaMalloc(&dh, sizeof(h) * c->world);
-  cudaMemcpy(dh + sizeof(h) * c->rank, &h, sizeof(h), cudaMemcpyHostToDevice);
-  ncclResult_t r = ncclAllGather(dh + sizeof(h) * c->rank, dh, sizeof(h), ncclUint8, c->world_c, c->side);
-  cudaStreamSynchronize(c->side);
-  std::vector<cudaIpcMemHandle_t> all(c->world);
-  cudaMemcpy(all.data(), dh, sizeof(h) * c->world, cudaMemcpyDeviceToHost);
-  cudaFree(dh);
-  cudaFree(tok);
-  if (r != ncclSuccess) return fail(SDP4_ENCCL, "handle exchange: %s", ncclGetErrorString(r));
-  b.peer.assign(c->world, nullptr);
-  for (int q = 0; q < c->world; ++q) {
-    if (q == c->rank) {
-      b.peer[q] = b.local;
-      continue;
-    }
-    void* p = nullptr;
-    if ((e = cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess)) != cudaSuccess)
-      return fail(SDP4_ECUDA, "open peer %d buffer: %s (no NVLink P2P? use the NCCL transport)", q,
-                  cudaGetErrorString(e));
-    b.peer[q] = static_cast<uint8_t*>(p);
-  }
-  e = cudaDeviceSynchronize();  // zeroed flags visible on every rank before any peer signals
-  int* tok2 = nullptr;
-  cudaMalloc(&tok2, sizeof(int));
-  ncclResult_t r2 = ncclAllReduce(tok2, tok2, 1, ncclInt32, ncclSum, c->world_c, c->side);
-  cudaStreamSynchronize(c->side);
-  cudaFree(tok2);
-  if (r2 != ncclSuccess) return fail(SDP4_ENCCL, "barrier: %s", ncclGetErrorString(r2));
-  return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "%s", cudaGetErrorString(e));
-}
-
-uint8_t* sym_region(const SymBuf& b, int rank, uint32_t epoch) {
-  return b.peer[rank] + kFlagBytes + (size_t)(epoch & 1) * b.region;
-}
-CUdeviceptr flag_ptr(const SymBuf& b, int owner, int stage, int src) {
-  return (CUdeviceptr)(b.peer[owner] + ((size_t)stage * 256 + src) * sizeof(uint32_t));
-}
-// After the producing kernel on `st`: raise flag[stage][me] on every destination rank.
-sdp4_status signal_peers(sdp4_comm* c, cudaStream_t st, const SymBuf& b, int stage, const std::vector<int>& dsts,
-                         uint32_t epoch) {
-  if (c->batch_memop) {  // one batched stream memory operation for every destination
-    CUstreamBatchMemOpParams ops[sdp4::kMaxDests];
-    unsigned n = 0;
-    for (int q : dsts) {
-      if (q == c->rank || n >= (unsigned)sdp4::kMaxDests) continue;
-      memset(&ops[n], 0, sizeof(ops[n]));
-      ops[n].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
-      ops[n].writeValue.address = flag_ptr(b, q, stage, c->rank);
-      ops[n].writeValue.value = epoch;
-      ops[n].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
-      ++n;
-    }
-    if (!n) return SDP4_OK;
-    CUresult r = c->batch_memop((CUstream)st, n, ops, 0);
-    if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamBatchMemOp (write) failed (%d)", (int)r);
+// Host allgather of `bytes` per rank (rank-major into recv) over the bootstrap channel.
+sdp4_status host_allgather(sdp4_comm* c, const void* send, void* recv, size_t bytes) {
+  if (c->world == 1) {
+    memcpy(recv, send, bytes);
     return SDP4_OK;
   }
-  for (int q : dsts) {
-    if (q == c->rank) continue;
-    CUresult r = c->write_value((CUstream)st, flag_ptr(b, q, stage, c->rank), epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
-    if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+  if (c->ag_fn) {
+    if (c->ag_fn(send, recv, bytes, c->ag_ctx) != 0) return fail(SDP4_ESTATE, "host allgather callback failed");
+    return SDP4_OK;
+  }
+  if (!c->world_c) return fail(SDP4_ESTATE, "no bootstrap channel");
+  uint8_t* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, bytes * c->world);
+  if (e != cudaSuccess) return fail(SDP4_ECUDA, "bootstrap buffer: %s", cudaGetErrorString(e));
+  cudaMemcpy(d + bytes * c->rank, send, bytes, cudaMemcpyHostToDevice);
+  ncclResult_t r = ncclAllGather(d + bytes * c->rank, d, bytes, ncclUint8, c->world_c, c->side);
+  cudaStreamSynchronize(c->side);
+  e = cudaMemcpy(recv, d, bytes * c->world, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (r != ncclSuccess) return fail(SDP4_ENCCL, "bootstrap allgather: %s", ncclGetErrorString(r));
+  return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "bootstrap copy: %s", cudaGetErrorString(e));
+}
+// Host allgather of one status byte per rank; returns the first failing rank or -1.
+int host_agree(sdp4_comm* c, bool ok, sdp4_status* st) {
+  std::vector<uint8_t> all(c->world);
+  const uint8_t mine = ok ? 1 : 0;
+  *st = host_allgather(c, &mine, all.data(), 1);
+  if (*st != SDP4_OK) return c->rank;
+  for (int q = 0; q < c->world; ++q)
+    if (!all[q]) return q;
+  return -1;
+}
+
+PeerInfo my_peer_info(int device) {
+  PeerInfo pi;
+  memset(&pi, 0, sizeof(pi));
+  char host[64] = {0}, boot[40] = {0};
+  gethostname(host, sizeof(host) - 1);
+  if (FILE* f = fopen("/proc/sys/kernel/random/boot_id", "r")) {
+    if (!fgets(boot, sizeof(boot), f)) boot[0] = 0;
+    fclose(f);
+  }
+  for (char* p = boot; *p; ++p)
+    if (*p == '\n') *p = 0;
+  snprintf(pi.host, sizeof(pi.host), "%s/%s", host, boot);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) memcpy(pi.uuid, &prop.uuid, 16);
+  pi.pid = (int)getpid();
+  return pi;
+}
+
+// Can this process map the memory of a peer described by `q` (CUDA IPC: same OS instance,
+// the peer's device visible here and either this device or peer-accessible from it)?
+bool reachable(const PeerInfo& me, const PeerInfo& q, int my_dev) {
+  if (strncmp(me.host, q.host, sizeof(me.host)) != 0) return false;
+  if (memcmp(me.uuid, q.uuid, 16) == 0) return true;  // ranks sharing one GPU (single-GPU emulation)
+  int n = 0;
+  cudaGetDeviceCount(&n);
+  for (int d = 0; d < n; ++d) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, d) != cudaSuccess) continue;
+    if (memcmp(&prop.uuid, q.uuid, 16) != 0) continue;
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, my_dev, d);
+    return can != 0;
+  }
+  return false;
+}
+
+// Collective: decide whether the P2P transport is usable by every rank, and
+// whether some ranks share a device.  Ranks sharing a GPU must never wait for one another in
+// a kernel (nothing guarantees that kernels of different processes run concurrently; a
+// spinning kernel can stall a context switch), so such a comm waits with stream memory
+// operations only.
+sdp4_status probe_p2p(sdp4_comm* c, bool* ok) {
+  const PeerInfo me = my_peer_info(c->device);
+  std::vector<PeerInfo> all(c->world);
+  sdp4_status s = host_allgather(c, &me, all.data(), sizeof(PeerInfo));
+  if (s != SDP4_OK) return s;
+  bool mine = c->write_value && c->wait_value && c->N <= sdp4::kMaxN && c->M <= sdp4::kMaxDests &&
+              c->world <= sdp4::kMaxDests;
+  for (int q = 0; q < c->world && mine; ++q)
+    if (q != c->rank && !reachable(me, all[q], c->device)) mine = false;
+  for (int q = 0; q < c->world; ++q)
+    for (int p = 0; p < q; ++p)
+      if (memcmp(all[p].uuid, all[q].uuid, 16) == 0) c->shared_gpu = true;
+  if (c->shared_gpu) c->timeout_ns = 0;
+  const int bad = host_agree(c, mine, &s);
+  if (s != SDP4_OK) return s;
+  *ok = bad < 0;
+  return SDP4_OK;
+}
+
+void sym_release(sdp4_comm* c, SymBuf& b) {
+  for (size_t q = 0; q < b.peer.size(); ++q)
+    if ((int)q != c->rank && b.peer[q]) cudaIpcCloseMemHandle(b.peer[q]);
+  if (b.local) cudaFree(b.local);
+  b = SymBuf();
+}
+
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+
+// Collectively (re)allocate a symmetric buffer whose region holds `region` bytes.  Every
+// failure is agreed on by all ranks (each reports its status through the bootstrap channel),
+// so either every rank returns with a complete mapping or every rank returns the error with
+// the buffer released -- never a partial mapping, never a rank left waiting in a barrier.
+sdp4_status sym_ensure(sdp4_comm* c, SymBuf& b, size_t region, cudaStream_t st) {
+  if (b.local && region <= b.region) return SDP4_OK;
+  if (capturing(st))
+    return fail(SDP4_ESTATE, "the symmetric buffer must grow to %zu bytes during stream capture: make one eager call "
+                             "of the same size before capturing", region);
+  region = round_up(region + region / 16, 1 << 21);
+  cudaError_t e = cudaDeviceSynchronize();  // no kernel of ours still touches the old buffers
+  sdp4_status s;
+  if (b.local) {  // every rank synchronized: the peers are done with the old buffers
+    int bad = host_agree(c, e == cudaSuccess, &s);
+    if (s != SDP4_OK) return s;
+    sym_release(c, b);
+    if (bad >= 0) return fail(SDP4_ECUDA, "rank %d failed to synchronize before reallocation", bad);
+  }
+  struct Rec {
+    cudaIpcMemHandle_t h;
+    int ok;
+  } mine;
+  memset(&mine, 0, sizeof(mine));
+  const size_t bytes = kFlagBytes + region;
+  std::string why;
+  if ((e = cudaMalloc(&b.local, bytes)) != cudaSuccess) {
+    b.local = nullptr;
+    why = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+  } else {
+    // data flags 0 (nothing published), free flags 1 (every receive slot initially free)
+    std::vector<uint32_t> init(kFlagBytes / 4, 0u);
+    for (size_t i = flag_off(kFree, 0, 0) / 4; i < init.size(); ++i) init[i] = 1u;
+    e = cudaMemcpy(b.local, init.data(), kFlagBytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&mine.h, b.local);
+    if (e != cudaSuccess) why = std::string("init/ipc handle: ") + cudaGetErrorString(e);
+  }
+  mine.ok = why.empty();
+  b.bytes = bytes;
+  b.region = region;
+  std::vector<Rec> all(c->world);
+  if ((s = host_allgather(c, &mine, all.data(), sizeof(Rec))) != SDP4_OK) {
+    sym_release(c, b);
+    return s;
+  }
+  int bad = -1;
+  for (int q = 0; q < c->world && bad < 0; ++q)
+    if (!all[q].ok) bad = q;
+  if (bad < 0) {
+    b.peer.assign(c->world, nullptr);
+    for (int q = 0; q < c->world; ++q) {
+      if (q == c->rank) {
+        b.peer[q] = b.local;
+        continue;
+      }
+      void* p = nullptr;
+      if ((e = cudaIpcOpenMemHandle(&p, all[q].h, cudaIpcMemLazyEnablePeerAccess)) != cudaSuccess) {
+        cudaGetLastError();
+        why = "open peer " + std::to_string(q) + " buffer: " + cudaGetErrorString(e);
+        break;
+      }
+      b.peer[q] = static_cast<uint8_t*>(p);
+    }
+    if (why.empty() && (e = cudaDeviceSynchronize()) != cudaSuccess)  // flags initialized before any peer signals
+      why = std::string("sync: ") + cudaGetErrorString(e);
+    bad = host_agree(c, why.empty(), &s);
+    if (s != SDP4_OK) {
+      sym_release(c, b);
+      return s;
+    }
+  }
+  if (bad >= 0) {
+    sym_release(c, b);
+    if (bad == c->rank) return fail(SDP4_ECUDA, "symmetric buffer of %zu bytes: %s", bytes, why.c_str());
+    return fail(SDP4_ECUDA, "symmetric buffer of %zu bytes failed on rank %d", bytes, bad);
   }
   return SDP4_OK;
 }
-// Before the consuming kernel on `st`: wait until every source rank raised its flag.
-// With profiling on, the time the stream spends in these waits is recorded as `name`.
-sdp4_status wait_peers(sdp4_comm* c, cudaStream_t st, const SymBuf& b, int stage, const std::vector<int>& srcs,
-                       uint32_t epoch, const char* name = "wait") {
+
+uint8_t* sym_region(const SymBuf& b, int rank) { return b.peer[rank] + kFlagBytes; }
+
+// ---- P2P sync protocol --------------------------------------------------------------
+// Binary flags, no epochs, so a captured graph replays correctly and the receive regions
+// need no double buffering.  For an exchange from producer p to consumer q (q's receive
+// region written by p, or p's own region read by q):
+//   p: wait free[stage][q] (in p's buffer) -> produce -> raise data[stage][p] in q's buffer;
+//   q: wait data[stage][p] (in q's buffer) -> consume -> raise free[stage][q] in p's buffer.
+// Each wait resets the flag it saw.  q's reset of data happens before q's consume, which is
+// before q raises free, which p waits for before it raises data again -- so a reset never
+// erases a newer raise (and symmetrically for free).  Initial state: data 0, free 1.
+struct Sig {
+  int owner, kind, stage;  // raise owner's flag[kind][stage][me]
+};
+struct Wt {
+  int kind, stage, src;  // wait for my flag[kind][stage][src]
+};
+
+sdp4_status raise_flags(sdp4_comm* c, cudaStream_t st, const SymBuf& b, const std::vector<Sig>& sigs) {
+  std::vector<CUstreamBatchMemOpParams> ops;
+  for (const Sig& g : sigs) {
+    if (g.owner == c->rank) continue;
+    const CUdeviceptr a = (CUdeviceptr)(b.peer[g.owner] + flag_off(g.kind, g.stage, c->rank));
+    if (!c->batch_memop) {
+      CUresult r = c->write_value((CUstream)st, a, 1u, CU_STREAM_WRITE_VALUE_DEFAULT);
+      if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+      continue;
+    }
+    CUstreamBatchMemOpParams op;
+    memset(&op, 0, sizeof(op));
+    op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+    op.writeValue.address = a;
+    op.writeValue.value = 1u;
+    op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;  // fenced after the stream's prior work
+    ops.push_back(op);
+  }
+  if (ops.empty()) return SDP4_OK;
+  CUresult r = c->batch_memop((CUstream)st, (unsigned)ops.size(), ops.data(), 0);
+  return r == CUDA_SUCCESS ? SDP4_OK : fail(SDP4_ECUDA, "cuStreamBatchMemOp (raise) failed (%d)", (int)r);
+}
+
+// Wait for (and reset) my flags.  timeout_ns > 0: one polling kernel with a deadline (a missing
+// peer sets the comm's error word instead of blocking the stream forever); 0: stream memory
+// operations (cuStreamWaitValue32, unbounded).  With profiling on, the wait is timed as `name`.
+sdp4_status wait_flags(sdp4_comm* c, cudaStream_t st, const SymBuf& b, const std::vector<Wt>& wts,
+                       const char* name = "wait") {
+  std::vector<Wt> w;
+  for (const Wt& x : wts)
+    if (x.src != c->rank) w.push_back(x);
+  if (w.empty()) return SDP4_OK;
   cudaEvent_t ea = nullptr, eb = nullptr;
   if (c->profiling) {
     ea = c->ev();
     eb = c->ev();
     cudaEventRecord(ea, st);
   }
-  if (c->batch_memop) {
-    CUstreamBatchMemOpParams ops[sdp4::kMaxDests];
-    unsigned n = 0;
-    for (int q : srcs) {
-      if (q == c->rank || n >= (unsigned)sdp4::kMaxDests) continue;
-      memset(&ops[n], 0, sizeof(ops[n]));
-      ops[n].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
-      ops[n].waitValue.address = flag_ptr(b, c->rank, stage, q);
-      ops[n].waitValue.value = epoch;
-      ops[n].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
-      ++n;
+  if (c->timeout_ns) {
+    if (w.size() > (size_t)sdp4::kMaxWait) return fail(SDP4_EINVAL, "too many flags to wait for");
+    sdp4::FlagWait fw;
+    memset(&fw, 0, sizeof(fw));
+    fw.n = (int)w.size();
+    fw.timeout_ns = c->timeout_ns;
+    fw.err = c->err_dev;
+    for (size_t i = 0; i < w.size(); ++i) {
+      fw.flag[i] = reinterpret_cast<uint32_t*>(b.local + flag_off(w[i].kind, w[i].stage, w[i].src));
+      fw.code[i] = 0x80000000u | ((uint32_t)w[i].kind << 24) | ((uint32_t)w[i].stage << 16) | (uint32_t)w[i].src;
     }
-    if (n) {
-      CUresult r = c->batch_memop((CUstream)st, n, ops, 0);
-      if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamBatchMemOp (wait) failed (%d)", (int)r);
-    }
+    cudaError_t e = sdp4::launch_wait_flags(fw, st);  // one of our kernels: counted as a launch
+    if (e != cudaSuccess) return fail(SDP4_ECUDA, "flag-wait launch failed: %s", cudaGetErrorString(e));
+    c->launches++;
   } else {
-    for (int q : srcs) {
-      if (q == c->rank) continue;
-      CUresult r = c->wait_value((CUstream)st, flag_ptr(b, c->rank, stage, q), epoch, CU_STREAM_WAIT_VALUE_GEQ);
-      if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+    std::vector<CUstreamBatchMemOpParams> waits, resets;
+    for (const Wt& x : w) {
+      const CUdeviceptr a = (CUdeviceptr)(b.local + flag_off(x.kind, x.stage, x.src));
+      if (!c->batch_memop) {
+        CUresult r = c->wait_value((CUstream)st, a, 1u, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r == CUDA_SUCCESS) r = c->write_value((CUstream)st, a, 0u, CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+        continue;
+      }
+      CUstreamBatchMemOpParams op;
+      memset(&op, 0, sizeof(op));
+      op.waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+      op.waitValue.address = a;
+      op.waitValue.value = 1u;
+      op.waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+      waits.push_back(op);
+      memset(&op, 0, sizeof(op));
+      op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+      op.writeValue.address = a;
+      op.writeValue.value = 0u;
+      op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+      resets.push_back(op);
+    }
+    if (!waits.empty()) {
+      CUresult r = c->batch_memop((CUstream)st, (unsigned)waits.size(), waits.data(), 0);
+      if (r == CUDA_SUCCESS) r = c->batch_memop((CUstream)st, (unsigned)resets.size(), resets.data(), 0);
+      if (r != CUDA_SUCCESS) return fail(SDP4_ECUDA, "cuStreamBatchMemOp (wait) failed (%d)", (int)r);
     }
   }
   if (c->profiling) {
@@ -454,6 +653,68 @@ bool valid_round(sdp4_round r) { return r == SDP4_RNE || r == SDP4_STOCHASTIC; }
 
 }  // namespace
 
+namespace {
+sdp4_status check_topology(sdp4_comm_t* out, int rank, int world, int groups_M, int group_size_N) {
+  if (!out) return fail(SDP4_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return fail(SDP4_EINVAL, "bad rank %d / world %d", rank, world);
+  if (groups_M < 1 || group_size_N < 1 || groups_M * group_size_N != world)
+    return fail(SDP4_EINVAL, "groups_M (%d) * group_size_N (%d) != world (%d)", groups_M, group_size_N, world);
+  return SDP4_OK;
+}
+
+sdp4_comm* comm_new(int rank, int world, int groups_M, int group_size_N, int nccl_ctas) {
+  sdp4_comm* c = new sdp4_comm();
+  c->rank = rank;
+  c->world = world;
+  c->M = groups_M;
+  c->N = group_size_N;
+  c->m = rank / group_size_N;
+  c->l = rank % group_size_N;
+  c->nccl_ctas = nccl_ctas ? nccl_ctas : kDefaultNcclCtas;
+  cudaGetDevice(&c->device);
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device);
+  if (c->nccl_ctas >= c->sm_count) c->nccl_ctas = c->sm_count / 2;
+  if (world > 1) {
+    void* fw = nullptr;
+    void* fwt = nullptr;
+    void* fb = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2, q3;
+    cudaGetDriverEntryPoint("cuStreamWriteValue32", &fw, cudaEnableDefault, &q1);
+    cudaGetDriverEntryPoint("cuStreamWaitValue32", &fwt, cudaEnableDefault, &q2);
+    cudaGetDriverEntryPoint("cuStreamBatchMemOp", &fb, cudaEnableDefault, &q3);
+    c->write_value = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(fw);
+    c->wait_value = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(fwt);
+    c->batch_memop = reinterpret_cast<PFN_cuStreamBatchMemOp_v11070>(fb);
+    if (getenv("SDP4_NO_BATCH_MEMOP")) c->batch_memop = nullptr;  // measurement switch
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi);
+    // the error word a timed-out flag wait writes (host-mapped: readable without a sync)
+    if (cudaHostAlloc(&c->err_host, sizeof(uint32_t), cudaHostAllocMapped) == cudaSuccess) {
+      *c->err_host = 0;
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0);
+    } else {
+      c->err_host = nullptr;
+      cudaGetLastError();
+    }
+    double sec = kDefaultTimeoutS;
+    if (const char* e = getenv("SDP4_WAIT_TIMEOUT_S")) sec = atof(e);
+    c->timeout_ns = (sec > 0 && c->err_dev) ? (unsigned long long)(sec * 1e9) : 0ull;
+  }
+  return c;
+}
+
+void comm_free(sdp4_comm* c) {
+  if (c->inter) ncclCommDestroy(c->inter);
+  if (c->intra) ncclCommDestroy(c->intra);
+  if (c->world_c) ncclCommDestroy(c->world_c);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->err_host) cudaFreeHost(c->err_host);
+  delete c;
+}
+}  // namespace
+
 extern "C" {
 
 int sdp4_version(void) { return 200; }
@@ -470,50 +731,20 @@ sdp4_status sdp4_get_unique_id(unsigned char id[SDP4_UNIQUE_ID_BYTES]) {
   return SDP4_OK;
 }
 
+
 sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, int world, int groups_M,
                            int group_size_N, int nccl_ctas) {
-  if (!out) return fail(SDP4_EINVAL, "out is NULL");
-  *out = nullptr;
-  if (world < 1 || rank < 0 || rank >= world) return fail(SDP4_EINVAL, "bad rank %d / world %d", rank, world);
-  if (groups_M < 1 || group_size_N < 1 || groups_M * group_size_N != world)
-    return fail(SDP4_EINVAL, "groups_M (%d) * group_size_N (%d) != world (%d)", groups_M, group_size_N, world);
+  sdp4_status s = check_topology(out, rank, world, groups_M, group_size_N);
+  if (s != SDP4_OK) return s;
   if (world > 1 && !id) return fail(SDP4_EINVAL, "id is NULL with world > 1");
   if (nccl_ctas < 0) return fail(SDP4_EINVAL, "nccl_ctas must be >= 0");
-  sdp4_comm* c = new sdp4_comm();
-  c->rank = rank;
-  c->world = world;
-  c->M = groups_M;
-  c->N = group_size_N;
-  c->m = rank / group_size_N;
-  c->l = rank % group_size_N;
-  c->nccl_ctas = nccl_ctas ? nccl_ctas : kDefaultNcclCtas;
-  cudaGetDevice(&c->device);
-  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device);
-  if (c->nccl_ctas >= c->sm_count) c->nccl_ctas = c->sm_count / 2;
+  sdp4_comm* c = comm_new(rank, world, groups_M, group_size_N, nccl_ctas);
   if (world > 1) {
-    void* fw = nullptr;
-    void* fwt = nullptr;
-    cudaDriverEntryPointQueryResult q1, q2;
-    cudaGetDriverEntryPoint("cuStreamWriteValue32", &fw, cudaEnableDefault, &q1);
-    cudaGetDriverEntryPoint("cuStreamWaitValue32", &fwt, cudaEnableDefault, &q2);
-    c->write_value = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(fw);
-    c->wait_value = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(fwt);
-    void* fb = nullptr;
-    cudaDriverEntryPointQueryResult q3;
-    cudaGetDriverEntryPoint("cuStreamBatchMemOp", &fb, cudaEnableDefault, &q3);
-    c->batch_memop = reinterpret_cast<PFN_cuStreamBatchMemOp_v11070>(fb);
-    if (getenv("SDP4_NO_BATCH_MEMOP")) c->batch_memop = nullptr;  // measurement switch
-    const bool p2p_ok = c->write_value && c->wait_value && group_size_N <= sdp4::kMaxN &&
-                        groups_M <= sdp4::kMaxDests && world <= sdp4::kMaxDests;
-    c->transport = p2p_ok ? kTransportP2P : kTransportNccl;
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi);
     ncclUniqueId u;
     memcpy(&u, id, sizeof(u));
     ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
     cfg.maxCTAs = c->nccl_ctas;
-    sdp4_status s = nccl_check(ncclCommInitRankConfig(&c->world_c, world, u, rank, &cfg), "ncclCommInitRankConfig");
+    s = nccl_check(ncclCommInitRankConfig(&c->world_c, world, u, rank, &cfg), "ncclCommInitRankConfig");
     if (s == SDP4_OK && group_size_N > 1) {
       ncclConfig_t cfg2 = NCCL_CONFIG_INITIALIZER;
       cfg2.maxCTAs = c->nccl_ctas;
@@ -524,14 +755,36 @@ sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, 
       cfg3.maxCTAs = c->nccl_ctas;
       s = nccl_check(ncclCommSplit(c->world_c, c->l, c->m, &c->inter, &cfg3), "ncclCommSplit(inter)");
     }
+    // P2P (the default) only if every rank reaches every other through CUDA IPC
+    if (s == SDP4_OK) s = probe_p2p(c, &c->p2p_ok);
     if (s != SDP4_OK) {
-      if (c->inter) ncclCommDestroy(c->inter);
-      if (c->intra) ncclCommDestroy(c->intra);
-      if (c->world_c) ncclCommDestroy(c->world_c);
-      if (c->side) cudaStreamDestroy(c->side);
-      delete c;
+      comm_free(c);
       return s;
     }
+    c->transport = c->p2p_ok ? kTransportP2P : kTransportNccl;
+  }
+  *out = c;
+  return SDP4_OK;
+}
+
+sdp4_status sdp4_comm_init_p2p(sdp4_comm_t* out, int rank, int world, int groups_M, int group_size_N,
+                               sdp4_host_allgather_fn allgather, void* ctx) {
+  sdp4_status s = check_topology(out, rank, world, groups_M, group_size_N);
+  if (s != SDP4_OK) return s;
+  if (world > 1 && !allgather) return fail(SDP4_EINVAL, "allgather callback is NULL with world > 1");
+  sdp4_comm* c = comm_new(rank, world, groups_M, group_size_N, 0);
+  c->ag_fn = allgather;
+  c->ag_ctx = ctx;
+  if (world > 1) {
+    s = probe_p2p(c, &c->p2p_ok);
+    if (s == SDP4_OK && !c->p2p_ok)
+      s = fail(SDP4_ESTATE, "P2P transport unavailable: some rank cannot map another's memory with CUDA IPC "
+                            "(different hosts, or no peer access); use sdp4_comm_init (NCCL)");
+    if (s != SDP4_OK) {
+      comm_free(c);
+      return s;
+    }
+    c->transport = kTransportP2P;
   }
   *out = c;
   return SDP4_OK;
@@ -546,31 +799,33 @@ sdp4_status sdp4_comm_destroy(sdp4_comm_t c) {
   }
   for (auto e : c->pool) cudaEventDestroy(e);
   for (auto e : c->deps) cudaEventDestroy(e);
-  const bool any_sym = c->sym_qwd.local || c->sym_tlq.local || c->sym_ring.local;
-  if (any_sym && c->world_c) {
+  sdp4_status s = SDP4_OK;
+  if (c->sym_qwd.local || c->sym_tlq.local || c->sym_ring.local) {
     // peers may still be reading this rank's symmetric buffers (K2 / K4 pulls): every rank
     // finishes its own work, then a barrier, then the mappings are closed and freed
-    cudaDeviceSynchronize();
-    int* tok = nullptr;
-    if (cudaMalloc(&tok, sizeof(int)) == cudaSuccess) {
-      ncclAllReduce(tok, tok, 1, ncclInt32, ncclSum, c->world_c, c->side);
-      cudaStreamSynchronize(c->side);
-      cudaFree(tok);
-    }
+    const cudaError_t e = cudaDeviceSynchronize();
+    host_agree(c, e == cudaSuccess, &s);
+    for (SymBuf* b : {&c->sym_qwd, &c->sym_tlq, &c->sym_ring}) sym_release(c, *b);
   }
-  for (SymBuf* b : {&c->sym_qwd, &c->sym_tlq, &c->sym_ring}) {
-    if (!b->local) continue;
-    cudaDeviceSynchronize();
-    for (int q = 0; q < c->world; ++q)
-      if (q != c->rank && b->peer[q]) cudaIpcCloseMemHandle(b->peer[q]);
-    cudaFree(b->local);
-  }
-  if (c->inter) ncclCommDestroy(c->inter);
-  if (c->intra) ncclCommDestroy(c->intra);
-  if (c->world_c) ncclCommDestroy(c->world_c);
-  if (c->side) cudaStreamDestroy(c->side);
-  delete c;
+  comm_free(c);
+  return s;
+}
+
+sdp4_status sdp4_comm_set_timeout(sdp4_comm_t c, double seconds) {
+  if (!c) return fail(SDP4_EINVAL, "comm is NULL");
+  if (!(seconds >= 0)) return fail(SDP4_EINVAL, "timeout must be >= 0");
+  if (seconds > 0 && c->world > 1 && !c->err_dev) return fail(SDP4_ESTATE, "no host-mapped error word");
+  if (seconds > 0 && c->shared_gpu)
+    return fail(SDP4_EINVAL, "ranks share a GPU: flag waits must be stream memory operations (timeout 0), never "
+                             "polling kernels");
+  c->timeout_ns = (unsigned long long)(seconds * 1e9);
   return SDP4_OK;
+}
+
+sdp4_status sdp4_comm_check(sdp4_comm_t c) {
+  if (!c) return fail(SDP4_EINVAL, "comm is NULL");
+  g_err.clear();
+  return async_check(c);
 }
 
 sdp4_status sdp4_comm_set_chunks(sdp4_comm_t c, int chunks) {
@@ -591,9 +846,10 @@ sdp4_status sdp4_comm_set_intra_pull(sdp4_comm_t c, int num, int den) {
 sdp4_status sdp4_comm_set_transport(sdp4_comm_t c, int transport) {
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (transport != kTransportNccl && transport != kTransportP2P) return fail(SDP4_EINVAL, "bad transport %d", transport);
-  if (transport == kTransportP2P && (c->world == 1 || !c->write_value || c->N > sdp4::kMaxN ||
-                                     c->M > sdp4::kMaxDests || c->world > sdp4::kMaxDests))
-    return fail(SDP4_EINVAL, "P2P transport unavailable for this comm");
+  if (transport == kTransportP2P && (c->world == 1 || !c->p2p_ok))
+    return fail(SDP4_EINVAL, "P2P transport unavailable for this comm (world 1, or CUDA IPC does not reach every rank)");
+  if (transport == kTransportNccl && c->world > 1 && !c->world_c)
+    return fail(SDP4_EINVAL, "this comm has no NCCL communicators (sdp4_comm_init_p2p)");
   c->transport = transport;
   return SDP4_OK;
 }
@@ -662,22 +918,35 @@ sdp4_status weight_quantize(sdp4_comm_t c, bool diff, const float* w_main_shard,
   };
   if (c->transport == kTransportP2P) {
     // Alg. 2 l.2-3: K1 writes unit `rank` into this rank's own symmetric buffer and raises
-    // flag[0][rank] on every peer; the all-gather (l.4) is the pull inside each rank's K2.
+    // data[0][rank] on every peer; the all-gather (l.4) is the pull inside each rank's K2.
+    // Before overwriting the unit, wait until every peer's K2 of the previous call has read it.
+    if (c->qwd_pending.valid)
+      return fail(SDP4_ESTATE, "P2P: the unit of the previous quantize has not been applied yet (one outstanding "
+                               "quantize per comm: call the matching allgather_apply first)");
     const size_t W = unit_bytes(S, bits, group);
-    if ((s = sym_ensure(c, c->sym_qwd, W, &c->epoch_qwd)) != SDP4_OK) return s;
-    const uint32_t ep = ++c->epoch_qwd;
+    if ((s = sym_ensure(c, c->sym_qwd, W, st)) != SDP4_OK) return s;
+    std::vector<Wt> frees;
+    std::vector<Sig> datas;
+    for (int q = 0; q < c->world; ++q) {
+      frees.push_back({kFree, 0, q});
+      datas.push_back({q, kData, 0});
+    }
+    if ((s = wait_flags(c, st, c->sym_qwd, frees, "wait_qwd_free")) != SDP4_OK) return s;
     sdp4::Dests d;
     d.n = 1;
     d.remote = 0;
-    d.p[0] = sym_region(c->sym_qwd, c->rank, ep);
-    std::vector<int> all(c->world);
-    for (int q = 0; q < c->world; ++q) all[q] = q;
+    d.p[0] = sym_region(c->sym_qwd, c->rank);
     s = launch(c, kname, st, [&] {
       return sdp4::launch_qwd_quantize(w_main_shard, shard_of(0), model_dtype, S, bits, group, d, sr, key,
                                        (uint64_t)c->rank * S, c->sm_count, st, apply_own);
     });
     if (s != SDP4_OK) return s;
-    return signal_peers(c, st, c->sym_qwd, 0, all, ep);
+    if ((s = raise_flags(c, st, c->sym_qwd, datas)) != SDP4_OK) return s;
+    c->qwd_pending.valid = true;
+    c->qwd_pending.numel = numel;
+    c->qwd_pending.bits = bits;
+    c->qwd_pending.group = group;
+    return SDP4_OK;
   }
   uint8_t* region = static_cast<uint8_t*>(workspace);
   for (const Chunk& ch : chunks) {  // Alg. 2 l.2-3 per chunk: unit (chunk, rank)
@@ -720,18 +989,30 @@ sdp4_status weight_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes,
   if (P > sdp4::kMaxDests) return fail(SDP4_EINVAL, "world %d > %d", P, sdp4::kMaxDests);
   if (skip_own && P == 1) return SDP4_OK;  // the only unit was applied by K1 (flags are >= waits)
   if (c->transport == kTransportP2P) {  // wait for every rank's unit; K2 pulls unit j from rank j
-    const uint32_t ep = c->epoch_qwd;
-    std::vector<int> all(P);
-    for (int q = 0; q < P; ++q) all[q] = q;
-    if ((s = wait_peers(c, st, c->sym_qwd, 0, all, ep, "wait_qwd_allgather")) != SDP4_OK) return s;
+    const auto& pd = c->qwd_pending;
+    if (!pd.valid || !c->sym_qwd.local)
+      return fail(SDP4_ESTATE, "P2P: no quantized unit is pending (call qwd_quantize / qw_quantize first)");
+    if (pd.numel != numel || pd.bits != bits || pd.group != group)
+      return fail(SDP4_ESTATE, "P2P: apply (numel %zu, bits %d, G %d) does not match the pending quantize (numel %zu, "
+                               "bits %d, G %d)", numel, bits, group, pd.numel, pd.bits, pd.group);
+    std::vector<Wt> datas;
+    std::vector<Sig> frees;
+    for (int q = 0; q < P; ++q) {
+      datas.push_back({kData, 0, q});
+      frees.push_back({q, kFree, 0});
+    }
+    if ((s = wait_flags(c, st, c->sym_qwd, datas, "wait_qwd_allgather")) != SDP4_OK) return s;
     sdp4::Dests u;
     u.n = P;
-    u.remote = P > 1 ? (uint32_t)(((uint64_t)1 << std::min(P, 32)) - 1) & ~(1u << (c->rank & 31)) : 0u;  // peers
-    for (int q = 0; q < P; ++q) u.p[q] = sym_region(c->sym_qwd, q, ep);
-    return launch(c, kname, st, [&] {
+    u.remote = ~0ull >> (64 - P) & ~(1ull << c->rank);  // peers' units (P <= 64)
+    for (int q = 0; q < P; ++q) u.p[q] = sym_region(c->sym_qwd, q);
+    s = launch(c, kname, st, [&] {
       return sdp4::launch_qwd_apply(u, P, S, S, bits, group, w_model_full, model_dtype, add, c->sm_count, st,
                                     c->rank, skip_own);
     });
+    if (s != SDP4_OK) return s;
+    c->qwd_pending.valid = false;
+    return raise_flags(c, st, c->sym_qwd, frees);  // K2 is done reading every peer's unit
   }
   if (P > 1) c->link(st, c->side);  // the units of every chunk were written on st (K1)
   uint8_t* region = static_cast<uint8_t*>(workspace);
@@ -841,8 +1122,7 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
       const size_t w8 = unit_bytes(chunks[k].len, bits_intra, group), w4 = unit_bytes(chunks[k].len, bits_inter, group);
       base[k + 1] = base[k] + (size_t)N * M * w8 * (pulling ? 2 : 1) + (size_t)M * w4;
     }
-    if ((s = sym_ensure(c, c->sym_tlq, base[C], &c->epoch_tlq)) != SDP4_OK) return s;
-    const uint32_t ep = ++c->epoch_tlq;
+    if ((s = sym_ensure(c, c->sym_tlq, base[C], st)) != SDP4_OK) return s;
     const int m = c->m, l = c->l;
     std::vector<int> group_ranks(N), node_ranks(M);
     for (int q = 0; q < N; ++q) group_ranks[q] = m * N + q;
@@ -854,7 +1134,7 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
       cudaStream_t sk = (k & 1) ? c->side : st;
       const size_t w8 = unit_bytes(ch.len, bits_intra, group), w4 = unit_bytes(ch.len, bits_inter, group);
       const size_t intra_bytes = (size_t)N * M * w8, outbox_off = intra_bytes + (size_t)M * w4;
-      auto region = [&](int rank) { return sym_region(c->sym_tlq, rank, ep) + base[k]; };
+      auto region = [&](int rank) { return sym_region(c->sym_tlq, rank) + base[k]; };
       // K3: shard m'N + l' -> unit m' of block l (this rank) in rank (m, l')'s intra receive region
       uint8_t* blocks[sdp4::kMaxN];
       for (int lp = 0; lp < N; ++lp) blocks[lp] = region(m * N + lp) + (size_t)l * M * w8;
@@ -867,19 +1147,36 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
         pull.outbox[lp] = region(c->rank) + outbox_off + (size_t)lp * M * w8;  // mine, for l'
         pull.src[lp] = region(m * N + lp) + outbox_off + (size_t)l * M * w8;   // l''s, for me
       }
+      // flag stages of chunk k; sync protocol: K3 writes the group peers' receive blocks and this
+      // rank's outbox (read by their K4), K4 the node peers' inter slots (read by their K5)
+      const int st_intra = 1 + 2 * k, st_inter = 2 + 2 * k;
+      std::vector<Wt> wq3, wq4, wq5;
+      std::vector<Sig> g3, g4, g5;
+      for (int q : group_ranks) {
+        wq3.push_back({kFree, st_intra, q});  // q's K4 of the previous call is done with my pushes / outbox
+        g3.push_back({q, kData, st_intra});
+        wq4.push_back({kData, st_intra, q});
+        g4.push_back({q, kFree, st_intra});
+      }
+      for (int q : node_ranks) {
+        wq4.push_back({kFree, st_inter, q});  // q's K5 of the previous call is done with my pushes
+        g4.push_back({q, kData, st_inter});
+        wq5.push_back({kData, st_inter, q});
+        g5.push_back({q, kFree, st_inter});
+      }
+      if ((s = wait_flags(c, sk, c->sym_tlq, wq3, "wait_tlq_free")) != SDP4_OK) return s;
       s = launch(c, "K3_tlq_had_quant", sk, [&] {
         return sdp4::launch_tlq_had_quant(static_cast<const uint8_t*>(grad) + ch.off * es, S, grad_dtype, ch.len, M, N,
                                           group, b, cb, bits_intra, blocks, remote, w8, sr, key8, ch.off, c->sm_count,
                                           sk, &pull);
       });
       if (s != SDP4_OK) return s;
-      const int st_intra = 1 + 2 * k, st_inter = 2 + 2 * k;  // flag slots of chunk k
-      if ((s = signal_peers(c, sk, c->sym_tlq, st_intra, group_ranks, ep)) != SDP4_OK) return s;
-      if ((s = wait_peers(c, sk, c->sym_tlq, st_intra, group_ranks, ep, "wait_tlq_intra")) != SDP4_OK) return s;
+      if ((s = raise_flags(c, sk, c->sym_tlq, g3)) != SDP4_OK) return s;
+      if ((s = wait_flags(c, sk, c->sym_tlq, wq4, "wait_tlq_intra")) != SDP4_OK) return s;
       // K4: unit m' -> slot m (this node) of rank (m', l)'s inter receive region
       sdp4::Dests d4;
       d4.n = M;
-      d4.remote = ((1u << M) - 1u) & ~(1u << m);
+      d4.remote = ~0ull >> (64 - M) & ~(1ull << m);
       for (int mp = 0; mp < M; ++mp) d4.p[mp] = region(mp * N + l) + intra_bytes + (size_t)m * w4;
       uint8_t* my = region(c->rank);
       s = launch(c, "K4_tlq_dq_reduce_q", sk, [&] {
@@ -887,13 +1184,14 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
                                             ch.off, c->sm_count, sk, &pull);
       });
       if (s != SDP4_OK) return s;
-      if ((s = signal_peers(c, sk, c->sym_tlq, st_inter, node_ranks, ep)) != SDP4_OK) return s;
-      if ((s = wait_peers(c, sk, c->sym_tlq, st_inter, node_ranks, ep, "wait_tlq_inter")) != SDP4_OK) return s;
+      if ((s = raise_flags(c, sk, c->sym_tlq, g4)) != SDP4_OK) return s;
+      if ((s = wait_flags(c, sk, c->sym_tlq, wq5, "wait_tlq_inter")) != SDP4_OK) return s;
       s = launch(c, "K5_tlq_dq_reduce_had", sk, [&] {
         return sdp4::launch_tlq_dq_reduce_had(my + intra_bytes, w4, bits_inter, M, ch.len, group, b, kappa,
                                               out_shard + ch.off, c->sm_count, sk);
       });
       if (s != SDP4_OK) return s;
+      if ((s = raise_flags(c, sk, c->sym_tlq, g5)) != SDP4_OK) return s;
     }
     if (C > 1) c->link(c->side, st);
     return SDP4_OK;
@@ -969,8 +1267,8 @@ size_t sdp4_ring_workspace_bytes(int world, size_t numel, int bits, int group) {
 // Ring reduce-scatter with per-hop quantization (sec. 2.3) -- the ablation baseline.
 // Hop t on rank r: chunk (r - t - 1) mod P; K6 folds the received partial sum into this rank's
 // gradient chunk and quantizes it into the next rank's receive slot; the last hop writes the
-// fp32 output shard r.  P2P: slot t of hop t in the library's symmetric buffer, one flag per
-// hop raised with cuStreamWriteValue32 (value (epoch << 6) + t + 1).  NCCL: ncclSend/ncclRecv.
+// fp32 output shard r.  P2P: slot t of hop t in the library's symmetric buffer, one data flag
+// per hop (binary flags, sync protocol above).  NCCL: ncclSend/ncclRecv.
 sdp4_status sdp4_ring_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dtype grad_dtype, size_t numel, int bits,
                                      int group, int average, float* out_shard, void* workspace,
                                      size_t workspace_bytes, void* stream) {
@@ -1001,22 +1299,24 @@ sdp4_status sdp4_ring_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dtype
   const int next = (r + 1) % P, prev = (r + P - 1) % P;
   if (c->transport == kTransportP2P) {
     // region: P-1 receive slots + one local send slot; K6 writes the hop's unit locally and
-    // the copy engine moves it into the next rank's slot (large NVLink writes)
-    if ((s = sym_ensure(c, c->sym_ring, (size_t)P * W, &c->epoch_ring)) != SDP4_OK) return s;
-    const uint32_t ep = ++c->epoch_ring;
-    auto slot = [&](int owner, int t) { return sym_region(c->sym_ring, owner, ep) + (size_t)t * W; };
-    auto val = [&](int t) { return (ep << 6) + (uint32_t)t + 1; };
+    // the copy engine moves it into the next rank's slot (large NVLink writes).  Sync: hop t
+    // raises data[t] on next; the final hop consumed every slot, so it raises free[0] on prev,
+    // which prev waits for before its first push of the following call.
+    if ((s = sym_ensure(c, c->sym_ring, (size_t)P * W, st)) != SDP4_OK) return s;
+    auto slot = [&](int owner, int t) { return sym_region(c->sym_ring, owner) + (size_t)t * W; };
     uint8_t* send_local = slot(r, P - 1);
+    if ((s = wait_flags(c, st, c->sym_ring, {{kFree, 0, next}}, "wait_ring_free")) != SDP4_OK) return s;
     for (int t = 0; t < P - 1; ++t) {
-      if (t > 0 && (s = wait_peers(c, st, c->sym_ring, 0, {prev}, val(t - 1), "wait_ring")) != SDP4_OK) return s;
+      if (t > 0 && (s = wait_flags(c, st, c->sym_ring, {{kData, t - 1, prev}}, "wait_ring")) != SDP4_OK) return s;
       if ((s = hop((r - t - 1 + 2 * P) % P, t ? slot(r, t - 1) : nullptr, send_local, nullptr)) != SDP4_OK)
         return s;
       cudaError_t e = cudaMemcpyAsync(slot(next, t), send_local, W, cudaMemcpyDeviceToDevice, st);
       if (e != cudaSuccess) return fail(SDP4_ECUDA, "ring hop copy: %s", cudaGetErrorString(e));
-      if ((s = signal_peers(c, st, c->sym_ring, 0, {next}, val(t))) != SDP4_OK) return s;
+      if ((s = raise_flags(c, st, c->sym_ring, {{next, kData, t}})) != SDP4_OK) return s;
     }
-    if ((s = wait_peers(c, st, c->sym_ring, 0, {prev}, val(P - 2), "wait_ring")) != SDP4_OK) return s;
-    return hop(r, slot(r, P - 2), nullptr, out_shard);
+    if ((s = wait_flags(c, st, c->sym_ring, {{kData, P - 2, prev}}, "wait_ring")) != SDP4_OK) return s;
+    if ((s = hop(r, slot(r, P - 2), nullptr, out_shard)) != SDP4_OK) return s;
+    return raise_flags(c, st, c->sym_ring, {{prev, kFree, 0}});
   }
   uint8_t* send = static_cast<uint8_t*>(workspace);
   uint8_t* recv = send + W;
@@ -1144,6 +1444,7 @@ sdp4_status sdp4_profile_read(sdp4_comm_t c, const char** names, double* ms, uin
 sdp4_status sdp4_nccl_reduce_scatter(sdp4_comm_t c, const void* send, void* recv, size_t numel, sdp4_dtype dtype,
                                      int average, void* stream) {
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
+  if (c->world > 1 && !c->world_c) return fail(SDP4_ESTATE, "this comm has no NCCL communicators");
   if (numel % (size_t)c->world) return fail(SDP4_EALIGN, "numel not divisible by world");
   const ncclDataType_t dt = dtype == SDP4_BF16 ? ncclBfloat16 : ncclFloat32;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1158,6 +1459,7 @@ sdp4_status sdp4_nccl_reduce_scatter(sdp4_comm_t c, const void* send, void* recv
 sdp4_status sdp4_nccl_all_gather(sdp4_comm_t c, const void* send, void* recv, size_t numel, sdp4_dtype dtype,
                                  void* stream) {
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
+  if (c->world > 1 && !c->world_c) return fail(SDP4_ESTATE, "this comm has no NCCL communicators");
   if (numel % (size_t)c->world) return fail(SDP4_EALIGN, "numel not divisible by world");
   const ncclDataType_t dt = dtype == SDP4_BF16 ? ncclBfloat16 : ncclFloat32;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

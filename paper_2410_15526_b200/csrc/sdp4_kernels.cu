@@ -1269,7 +1269,7 @@ __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const 
     // in slot order, written at their element positions (undoing the slot permutation)
     // local destination: write global memory directly (L2 merges the partial sectors);
     // peer destination: stage the tile in smem and bulk-store it (contiguous NVLink writes)
-    const bool remote = (dst.remote >> mp) & 1u;  // CTA-uniform
+    const bool remote = (dst.remote >> mp) & 1ull;  // CTA-uniform
     uint8_t* gout = dst.p[mp];
     uint8_t* ot = remote ? out_buf + (i % C::OUTB) * C::OUT_TILE : gout + e0 * BOUT / 8;
     float* osc = remote ? reinterpret_cast<float*>(ot + kK4Tile * BOUT / 8)
@@ -1494,6 +1494,36 @@ __global__ void __launch_bounds__(kK5Rows, kK5Ctas)
     }
   }
   if (t == 0) bulk_wait<0>();
+}
+
+// =====================================================================================
+// P2P completion-flag wait (the sync protocol of sdp4_api.cu): one warp, lane i polls flags
+// i, i + 32, ... of this rank's own symmetric buffer with system-scope acquire loads until each
+// is non-zero (raised by a peer's stream memory operation after its producing kernel), then
+// resets it to 0.  With a timeout, a flag still missing at the deadline writes its code into a
+// host-mapped error word and the lane gives up, so a dead peer cannot hang the stream.
+// =====================================================================================
+__global__ void __launch_bounds__(32, 1) k_wait_flags(const FlagWait w) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int i = threadIdx.x; i < w.n; i += 32) {
+    uint32_t* f = w.flag[i];
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (v) break;
+      if (w.timeout_ns) {
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (now - t0 > w.timeout_ns) {
+          if (w.err) *reinterpret_cast<volatile uint32_t*>(w.err) = w.code[i];
+          return;
+        }
+      }
+      __nanosleep(32);
+    }
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(f), "r"(0u) : "memory");
+  }
 }
 
 inline int grid_for(size_t ntiles, int cap) {
@@ -1795,6 +1825,13 @@ cudaError_t launch_tlq_dq_reduce_had(const uint8_t* inter_recv, size_t in_unit_b
   if (in_r == 32) { K5(32); } else if (in_r == 64) { K5(64); } else { K5(256); }
 #undef K5
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_wait_flags(const FlagWait& w, cudaStream_t st) {
+  if (w.n <= 0) return cudaSuccess;
+  if (w.n > kMaxWait) return cudaErrorInvalidValue;
+  k_wait_flags<<<1, 32, 0, st>>>(w);
+  return cudaGetLastError();
 }
 
 }  // namespace sdp4

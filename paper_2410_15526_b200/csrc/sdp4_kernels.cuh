@@ -24,8 +24,22 @@ constexpr int kMaxN = 8;  // max local ranks per group (K3 keeps one tensor map 
 struct Dests {
   uint8_t* p[kMaxDests];
   int n;
-  uint32_t remote;  // bit k: p[k] is peer memory (store via staged 1-D bulk copies)
+  uint64_t remote;  // bit k: p[k] is peer memory (store via staged 1-D bulk copies)
 };
+
+// P2P completion flags (sdp4_api.cu): wait until every listed flag word of this rank's own
+// symmetric buffer is non-zero, then reset it to 0 (binary flags, so a captured CUDA graph
+// replays correctly).  timeout_ns > 0: give up after that long, write `code` | the index of the
+// first missing flag into *err (host-mapped) and return -- the stream is never blocked forever.
+constexpr int kMaxWait = 128;
+struct FlagWait {
+  uint32_t* flag[kMaxWait];
+  int n;
+  unsigned long long timeout_ns;
+  uint32_t* err;  // device view of a host-mapped word
+  uint32_t code[kMaxWait];
+};
+cudaError_t launch_wait_flags(const FlagWait& w, cudaStream_t st);
 
 // K1: Alg. 2 l.2-3 -- d = w_main - w_model (this shard), k-bit group quantization
 // into the wire unit at every destination dst.p[0..n) (n = 1: local; n = P: all-gather push).

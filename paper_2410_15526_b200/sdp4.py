@@ -16,7 +16,7 @@ import torch
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libsdp4.so")
 
-OK, EINVAL, EALIGN, ECUDA, ENCCL, ESTATE = range(6)
+OK, EINVAL, EALIGN, ECUDA, ENCCL, ESTATE, ETIMEOUT = range(7)
 F32, BF16 = 0, 1
 RNE, STOCHASTIC = 0, 1
 UNIQUE_ID_BYTES = 128
@@ -28,6 +28,8 @@ _c_size = ctypes.c_size_t
 _vp = ctypes.c_void_p
 _ci = ctypes.c_int
 _u64 = ctypes.c_uint64
+# sdp4_host_allgather_fn: int (*)(const void* send, void* recv, size_t bytes, void* ctx)
+HOST_ALLGATHER_FN = ctypes.CFUNCTYPE(_ci, _vp, _vp, _c_size, _vp)
 
 # name -> (restype, argtypes): exactly the entry points of include/sdp4.h
 SIGNATURES = {
@@ -35,7 +37,10 @@ SIGNATURES = {
     "sdp4_last_error": (ctypes.c_char_p, []),
     "sdp4_get_unique_id": (_ci, [ctypes.c_char_p]),
     "sdp4_comm_init": (_ci, [ctypes.POINTER(_vp), ctypes.c_char_p, _ci, _ci, _ci, _ci, _ci]),
+    "sdp4_comm_init_p2p": (_ci, [ctypes.POINTER(_vp), _ci, _ci, _ci, _ci, HOST_ALLGATHER_FN, _vp]),
     "sdp4_comm_destroy": (_ci, [_vp]),
+    "sdp4_comm_set_timeout": (_ci, [_vp, ctypes.c_double]),
+    "sdp4_comm_check": (_ci, [_vp]),
     "sdp4_comm_set_chunks": (_ci, [_vp, _ci]),
     "sdp4_comm_chunks": (_ci, [_vp, _c_size, _ci]),
     "sdp4_comm_set_transport": (_ci, [_vp, _ci]),
@@ -164,17 +169,67 @@ def get_unique_id() -> bytes:
     return buf.raw
 
 
+def _gloo_allgather(group):
+    """A sdp4_host_allgather_fn over a torch.distributed process group (the host bootstrap of
+    sdp4_comm_init_p2p): byte buffers gathered rank-major.  Argument marshalling only."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else None
+
+    def cb(send, recv, nbytes, ctx):
+        try:
+            src = torch.frombuffer(bytearray(ctypes.string_at(send, nbytes)), dtype=torch.uint8) if nbytes \
+                else torch.zeros(0, dtype=torch.uint8)
+            if dev is not None:
+                src = src.to(dev)
+            outs = [torch.empty_like(src) for _ in range(world)]
+            dist.all_gather(outs, src, group=group)
+            for r, o in enumerate(outs):
+                if nbytes:
+                    b = bytes(o.cpu().numpy().tobytes())
+                    ctypes.memmove(recv + r * nbytes, b, nbytes)
+            return 0
+        except Exception as ex:  # noqa: BLE001 -- reported as a nonzero status to the library
+            import sys
+            print(f"libsdp4 host allgather failed: {ex!r}", file=sys.stderr)
+            return 1
+    return HOST_ALLGATHER_FN(cb)
+
+
 class Comm:
-    """sdp4_comm_t: world + intra (N) + inter (M) NCCL communicators."""
+    """sdp4_comm_t: world + intra (N) + inter (M) NCCL communicators, or a P2P-only comm
+    bootstrapped over a host channel (sdp4_comm_init_p2p).  Destroy it with close() on every
+    rank (collective); a Comm that is garbage-collected unclosed is leaked, never destroyed,
+    because destruction is a collective."""
 
     def __init__(self, rank: int = 0, world: int = 1, groups: int = 1, group_size: int = 1,
-                 unique_id: Optional[bytes] = None, nccl_ctas: int = 0, chunks: int = 0):
+                 unique_id: Optional[bytes] = None, nccl_ctas: int = 0, chunks: int = 0,
+                 host_allgather=None):
         self.rank, self.world, self.M, self.N = rank, world, groups, group_size
         self._h = ctypes.c_void_p()
-        uid = None if unique_id is None else ctypes.create_string_buffer(unique_id, UNIQUE_ID_BYTES)
-        _check(lib().sdp4_comm_init(ctypes.byref(self._h), uid, rank, world, groups, group_size, nccl_ctas))
+        self._ag = host_allgather          # keeps the ctypes callback alive
+        if host_allgather is not None:
+            _check(lib().sdp4_comm_init_p2p(ctypes.byref(self._h), rank, world, groups, group_size, host_allgather,
+                                            None))
+        else:
+            uid = None if unique_id is None else ctypes.create_string_buffer(unique_id, UNIQUE_ID_BYTES)
+            _check(lib().sdp4_comm_init(ctypes.byref(self._h), uid, rank, world, groups, group_size, nccl_ctas))
         if chunks:
             self.set_chunks(chunks)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_timeout(self, seconds: float):
+        """Deadline of the P2P flag waits (0 = unbounded stream-memop waits); see sdp4_comm_set_timeout."""
+        _check(lib().sdp4_comm_set_timeout(self._h, float(seconds)))
+
+    def check(self):
+        """Raise SDP4Error if an earlier call failed asynchronously (P2P wait timeout, NCCL)."""
+        _check(lib().sdp4_comm_check(self._h))
 
     def set_chunks(self, chunks: int):
         """Pipeline chunk count (0 = automatic, 1 = off); see sdp4_comm_set_chunks."""
@@ -200,21 +255,25 @@ class Comm:
 
     @classmethod
     def from_process_group(cls, groups: Optional[int] = None, device=None, nccl_ctas: int = 0,
-                           chunks: int = 0) -> "Comm":
-        """Bootstrap from torch.distributed: rank 0 draws an NCCL unique id and broadcasts
-        it; groups defaults to the topology of topology.default_split."""
+                           chunks: int = 0, bootstrap: str = "nccl", group=None) -> "Comm":
+        """Bootstrap from torch.distributed; groups defaults to the topology of
+        topology.default_split.  bootstrap="nccl": rank 0 draws an NCCL unique id and broadcasts
+        it (sdp4_comm_init).  bootstrap="host": a P2P-only comm whose CUDA-IPC handles travel over
+        the process group (sdp4_comm_init_p2p) -- no NCCL, so several ranks may share one GPU."""
         import torch.distributed as dist
         from .topology import default_split
-        rank, world = dist.get_rank(), dist.get_world_size()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
         M, N = default_split(world, groups)
+        if bootstrap == "host":
+            return cls(rank, world, M, N, chunks=chunks, host_allgather=_gloo_allgather(group))
         uid = None
         if world > 1:
             t = torch.zeros(UNIQUE_ID_BYTES, dtype=torch.uint8)
             if rank == 0:
                 t = torch.frombuffer(bytearray(get_unique_id()), dtype=torch.uint8)
-            if dist.get_backend() == "nccl":
+            if dist.get_backend(group) == "nccl":
                 t = t.to(device or torch.device("cuda", torch.cuda.current_device()))
-            dist.broadcast(t, 0)
+            dist.broadcast(t, dist.get_global_rank(group, 0) if group is not None else 0, group=group)
             uid = bytes(t.cpu().tolist())
         return cls(rank, world, M, N, uid, nccl_ctas, chunks)
 
@@ -224,8 +283,12 @@ class Comm:
             self._h = ctypes.c_void_p()
 
     def __del__(self):
+        # sdp4_comm_destroy is collective (a barrier with the peers when symmetric buffers
+        # exist): running it from a garbage collector on one rank could hang, so an unclosed
+        # multi-rank comm is leaked; a single-rank one is destroyed (nothing collective).
         try:
-            self.close()
+            if self._h and self.world == 1:
+                self.close()
         except Exception:
             pass
 

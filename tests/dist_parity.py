@@ -1,6 +1,13 @@
-"""Distributed parity of the full NCCL path (run with torchrun, one process per GPU).
+"""Distributed parity of the full path (run with torchrun, one process per rank).
 
     torchrun --nproc-per-node P --master-addr 127.0.0.1 tests/dist_parity.py [--groups M]
+    torchrun --nproc-per-node P ... tests/dist_parity.py --shared-gpu [--splits all]
+
+Default: one process per GPU, NCCL bootstrap, both transports.  --shared-gpu: every rank on
+cuda:0, bootstrapped over a gloo process group (sdp4_comm_init_p2p, no NCCL), so the product
+P2P transport -- K1/K2 all-gather pull, K3/K4 all-to-all pushes and pulls, the flag protocol --
+runs for any M x N on a single GPU; --splits all checks every M dividing P.  Ranks sharing a
+GPU wait with stream memory operations only (no kernel ever waits for another rank).
 
 Every rank draws all P ranks' synthetic inputs (seeded, CPU), runs
   qWD:    sdp4_qwd_quantize + sdp4_qwd_allgather_apply  (ncclAllGather), and sdp4_qwd_step
@@ -22,27 +29,63 @@ sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402
 import synth  # noqa: E402
-from paper_2410_15526_b200 import Comm, default_split  # noqa: E402
+from paper_2410_15526_b200 import Comm, SDP4Error, default_split  # noqa: E402
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--groups", type=int, default=None)
+    ap.add_argument("--splits", type=str, default=None, help="'all' or comma-separated M values (virtual mode)")
     ap.add_argument("--G", type=int, default=128)
     ap.add_argument("--b", type=int, default=64)
     ap.add_argument("--chunks", type=str, default="1,3,0", help="NCCL pipeline chunk counts to check (0 = auto)")
     ap.add_argument("--transports", type=str, default="p2p,nccl")
     ap.add_argument("--full", action="store_true", help="GPT-1.3B-sized buffer, sampled windows (bench config)")
+    ap.add_argument("--shared-gpu", dest="virtual", action="store_true", help="all ranks on cuda:0, host (gloo) bootstrap, P2P only")
+    ap.add_argument("--timeout-test", action="store_true", help="rank 1 skips a call; rank 0 must time out")
+    ap.add_argument("--graph", action="store_true", help="also replay CUDA-graph-captured P2P calls")
+    ap.add_argument("--wait", type=str, default="kernel", help="P2P waits: kernel (timeout) or memop (unbounded)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    local = 0 if a.virtual else int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if a.virtual:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if a.timeout_test:
+        ok, msg = run_timeout_test(rank, world)
+        print(f"rank {rank}/{world} {'PASS' if ok else 'FAIL'} timeout test: {msg}", flush=True)
+        dist.barrier()
+        dist.destroy_process_group()
+        sys.exit(0 if ok else 1)
+    if a.virtual:
+        splits = [m for m in range(1, world + 1) if world % m == 0] if a.splits in (None, "all") \
+            else [int(x) for x in a.splits.split(",")]
+        ok, out = True, []
+        for M in splits:
+            comm = Comm.from_process_group(M, bootstrap="host")
+            try:   # ranks sharing a GPU never wait in a kernel: polling waits are refused
+                comm.set_timeout(5.0)
+                ok, out = False, out + [f"{M}: set_timeout accepted with ranks sharing a GPU"]
+            except SDP4Error:
+                pass
+            N = world // M
+            runs = [("p2p", 0, None), ("p2p", 0, 2 ** 34 + 2410), ("p2p", -1, None), ("p2p", -3, 2410),
+                    ("p2p", 2, None), ("p2p", 3, 2411)]
+            ok_m, msgs = run_matrix(comm, rank, world, M, N, a.G, a.b, runs, graph=a.graph)
+            comm.close()
+            ok &= ok_m
+            out.append(f"{M}x{N} {'PASS' if ok_m else 'FAIL'} {'; '.join(msgs)}")
+        print(f"rank {rank}/{world} virtual {'PASS' if ok else 'FAIL'} " + " | ".join(out), flush=True)
+        dist.barrier()
+        dist.destroy_process_group()
+        sys.exit(0 if ok else 1)
     M, N = default_split(world, a.groups)
     comm = Comm.from_process_group(a.groups)
+    if a.wait == "memop":
+        comm.set_timeout(0)
     P, G, b = world, a.G, a.b
-    ok = True
-    msgs = []
     if a.full:
         ok, msgs = run_full(comm, rank, P, M, N)
         comm.close()
@@ -57,21 +100,127 @@ def main():
         runs.append((tr, 3 if tr == "nccl" else 0, 2 ** 34 + 2410))     # stochastic rounding (R14)
     if "p2p" in a.transports:   # intra all-to-all split between K3 pushes and K4 pulls; chunked P2P
         runs += [("p2p", -1, None), ("p2p", -3, 2410), ("p2p", 2, None), ("p2p", 3, 2411)]
-    for tr, chunks, seed in runs:
-        comm.set_transport(tr)
-        comm.set_chunks(max(chunks, 0))
-        if tr == "p2p":      # chunks -1: push only; -3: pull 2 of 3 tiles; else the default 1/2
-            comm.set_intra_pull(*{-1: (0, 1), -3: (2, 3)}.get(chunks, (1, 2)))
-        for S in (16384 * 2 + 64 * 5 * max(1, G // 64), 16384 * 12 + 640):
-            S -= S % max(G, 64)
-            ok_c, m_c = run_checks(comm, rank, P, M, N, G, b, S, seed)
-            ok &= ok_c
-            msgs += [f"{tr} chunks={chunks} seed={seed} S={S} ({comm.chunks(P * S, G)} used): {m}" for m in m_c]
+    ok, msgs = run_matrix(comm, rank, P, M, N, G, b, runs, graph=a.graph)
     comm.close()
     print(f"rank {rank}/{world} ({M}x{N}) {'PASS' if ok else 'FAIL'} runs={runs} {'; '.join(msgs)}", flush=True)
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
+
+
+def run_matrix(comm, rank, P, M, N, G, b, runs, graph=False):
+    """Every (transport, chunks / push-pull split, seed) run at two shard sizes (several K3
+    tiles and a ragged tail), then optionally the CUDA-graph replays."""
+    ok, msgs = True, []
+    for tr, chunks, seed in runs:
+        comm.set_transport(tr)
+        comm.set_chunks(max(chunks, 0))
+        if tr == "p2p":      # chunks -1: push only; -3: pull 2 of 3 tiles; else the default split
+            if chunks in (-1, -3):
+                comm.set_intra_pull(*{-1: (0, 1), -3: (2, 3)}[chunks])
+            else:
+                comm.set_intra_pull(1, 2) if N > 2 else comm.set_intra_pull(0, 1)
+        for S in (16384 * 2 + 64 * 5 * max(1, G // 64), 16384 * 12 + 640):
+            S -= S % max(G, 64)
+            ok_c, m_c = run_checks(comm, rank, P, M, N, G, b, S, seed)
+            ok &= ok_c
+            msgs += [f"{tr} chunks={chunks} seed={seed} S={S} ({comm.chunks(P * S, G)} used): {m}" for m in m_c]
+    if graph and comm.transport == "p2p":
+        ok_g, m_g = run_graph(comm, rank, P, M, N, G, b)
+        ok &= ok_g
+        msgs += m_g
+    msgs.append(f"{len(runs)} runs x 2 sizes{' + graph replays' if graph else ''}")
+    return ok, msgs
+
+
+def run_graph(comm, rank, P, M, N, G, b, S=16384 * 2 + 640, replays=3):
+    """P2P calls captured in CUDA graphs replay correctly (binary flags, no host epoch): the
+    TLq-HS reduce-scatter and the qWD step, each replayed on new inputs copied into the
+    captured buffers, every replay checked against the oracle."""
+    S -= S % max(G, 64)
+    D = P * S
+    comm.set_chunks(0)
+    ok, msgs = True, []
+    g_in = torch.empty(D, dtype=torch.bfloat16, device="cuda")
+    out = torch.empty(S, dtype=torch.float32, device="cuda")
+    w_model = torch.empty(D, dtype=torch.bfloat16, device="cuda")
+    w_main = torch.empty(S, dtype=torch.float32, device="cuda")
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):   # eager warm-up of the same sizes: no buffer grows in capture
+        comm.tlq_hs_reduce_scatter(g_in.zero_(), out, None, 8, 4, G, b, True)
+        comm.qwd_step(w_main.zero_(), w_model.zero_(), None, 4, G)
+    side.synchronize()
+    g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g1, stream=side):
+        comm.tlq_hs_reduce_scatter(g_in, out, None, 8, 4, G, b, True)
+    with torch.cuda.graph(g2, stream=side):
+        comm.qwd_step(w_main, w_model, None, 4, G)
+    for it in range(replays):
+        grads = [synth.gradient(D, seed=synth.seed_for(r, 50 + it), dtype=torch.bfloat16) for r in range(P)]
+        g_in.copy_(grads[rank])
+        torch.cuda.synchronize()
+        g1.replay()
+        torch.cuda.synchronize()
+        want = oracle.tlq_hs_reduce_scatter([g.float().numpy() for g in grads], oracle.Topology(M, N), G, b, 8, 4,
+                                            True).out[rank]
+        if not np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32)):
+            ok = False
+            msgs.append(f"graph replay {it}: TLq-HS differs")
+        wm0 = synth.model_weights(D, seed=70 + it)
+        mains = [synth.main_weights(wm0[r * S:(r + 1) * S], seed=synth.seed_for(r, 80 + it)) for r in range(P)]
+        w_model.copy_(wm0)
+        w_main.copy_(mains[rank])
+        torch.cuda.synchronize()
+        g2.replay()
+        torch.cuda.synchronize()
+        _, want = oracle.qwd_step([m.numpy() for m in mains], synth.bf16_bits(wm0), 4, G, model_bf16=True)
+        if not np.array_equal(synth.bf16_bits(w_model.cpu()), want):
+            ok = False
+            msgs.append(f"graph replay {it}: qWD replica differs")
+    del g1, g2
+    comm.check()
+    msgs.append(f"{replays} graph replays (TLq-HS, qWD step)")
+    return ok, msgs
+
+
+def run_timeout_test(rank, world, timeout_s=1.0):
+    """Bounded waits: after one good call on both ranks, rank 1 skips the next collective call.
+    Rank 0's flag waits must give up at the deadline (the stream drains, no hang) and the
+    following call must return SDP4_ETIMEOUT; rank 1 is unaffected."""
+    import time
+    from paper_2410_15526_b200 import sdp4
+    comm = Comm.from_process_group(1 if world == 2 else None)
+    P = world
+    S = 16384 * 2
+    D = P * S
+    g = synth.gradient(D, seed=synth.seed_for(rank, 3), dtype=torch.bfloat16).cuda()
+    out = torch.empty(S, dtype=torch.float32, device="cuda")
+    comm.tlq_hs_reduce_scatter(g, out, None, 8, 4, 128, 64, True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ok, msg = True, ""
+    if rank == 0:
+        comm.set_timeout(timeout_s)
+        t0 = time.time()
+        comm.tlq_hs_reduce_scatter(g, out, None, 8, 4, 128, 64, True)   # rank 1 never joins
+        torch.cuda.synchronize()
+        el = time.time() - t0
+        try:
+            comm.tlq_hs_reduce_scatter(g, out, None, 8, 4, 128, 64, True)
+            ok, msg = False, "the call after the timed-out one succeeded"
+        except SDP4Error as ex:
+            ok = ex.status == sdp4.ETIMEOUT
+            msg = f"drained in {el:.1f} s (timeout {timeout_s} s per wait); next call: {ex}"
+        try:
+            comm.check()
+            ok = False
+        except SDP4Error:
+            pass
+    else:
+        msg = "skipped the call"
+    dist.barrier()
+    comm.close()
+    return ok, msg
 
 
 def run_full(comm, rank, P, M, N, G=128, b=64, win=16384, nwin=6):
@@ -146,7 +295,7 @@ def run_checks(comm, rank, P, M, N, G, b, S, seed=None):
         ok = False
         msgs.append(f"qWD replica differs from oracle in {int(np.sum(got != want))} elements")
     h = torch.tensor([int(np.uint64(np.sum(got.astype(np.uint64) * np.arange(1, D + 1, dtype=np.uint64))) & 0x7FFFFFFF)],
-                     device="cuda")
+                     device="cuda" if dist.get_backend() == "nccl" else "cpu")
     hs = [torch.zeros_like(h) for _ in range(P)]
     dist.all_gather(hs, h)
     if len({int(x.item()) for x in hs}) != 1:

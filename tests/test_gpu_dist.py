@@ -16,7 +16,7 @@ def test_dist_parity(nproc, groups):
         pytest.skip(f"needs {nproc} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", f"--master-port={29500 + nproc * 10 + groups}",
-           os.path.join(ROOT, "tests", "dist_parity.py"), "--groups", str(groups)]
+           os.path.join(ROOT, "tests", "dist_parity.py"), "--groups", str(groups), "--graph"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("PASS") == nproc, r.stdout
@@ -34,3 +34,30 @@ def test_dist_parity_fullsize(groups):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("PASS") == nproc, r.stdout
+
+
+@pytest.mark.parametrize("nproc,groups", [(2, 1), (4, 2)])
+def test_dist_parity_memop_waits(nproc, groups):
+    """The unbounded stream-memop flag waits (timeout 0) give the same results as the default
+    polling-kernel waits."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={29560 + nproc}", os.path.join(ROOT, "tests", "dist_parity.py"),
+           "--groups", str(groups), "--transports", "p2p", "--wait", "memop", "--graph"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("PASS") == nproc, r.stdout
+
+
+def test_dist_wait_timeout():
+    """Bounded waits on two GPUs: rank 1 skips a collective call; rank 0's polling waits give
+    up at the deadline (its stream drains, no hang) and its next call returns SDP4_ETIMEOUT."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29590", os.path.join(ROOT, "tests", "dist_parity.py"),
+           "--timeout-test"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("PASS") == 2, r.stdout
