@@ -12,8 +12,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsdp4.so")
-SOURCES = ["sdp4_api.cu", "sdp4_kernels.cu"]
-HEADERS = ["sdp4_kernels.cuh"]
+SOURCES = ["sdp4_api.cu", "k_weights.cu", "k_had_quant.cu", "k_reduce.cu", "k_final.cu"]
+HEADERS = ["sdp4_kernels.cuh", "sdp4_device.cuh"]
 
 
 def nccl_dirs():
@@ -52,8 +52,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
 
+    hdr_t = max(os.path.getmtime(d) for d in [os.path.join(CSRC, f) for f in HEADERS] +
+                [os.path.join(ROOT, "include", "sdp4.h"), os.path.abspath(__file__)])
+
     def compile_one(src):
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(
+                os.path.join(CSRC, src))):
+            return obj     # incremental: object newer than its source and every header
         cmd = flags + ["-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -74,4 +80,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="--verbose" in sys.argv))
+    print(build(force="--incremental" not in sys.argv, verbose="--verbose" in sys.argv))

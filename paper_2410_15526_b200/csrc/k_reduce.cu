@@ -1,0 +1,353 @@
+// k_reduce.cu -- K4 tlq_dq_reduce_q: dequantize + fp32 reduce + requantize (Alg. 3 l.5, 7, 9).
+#include "sdp4_device.cuh"
+
+namespace sdp4 {
+namespace {
+
+// =====================================================================================
+// K4  TLq dequantize + reduce + requantize (Alg. 3 l.5, 7, 9, FP32 reduce P:344).
+// Vector layout: a tile is 8192 elements of sub-block m'; thread t owns the 64 contiguous
+// elements [64t, 64t+64), read from smem as 16-byte chunks in XOR-permuted order
+// (slot c <- chunk c ^ f(t): conflict-free; the permutation is undone by the store
+// addresses).  Thread 0 streams (tile, source l'') items through a STAGES-deep ring of 1-D
+// bulk copies (codes + scales); sources are summed in order l'' = 0..N-1 (R8); the sum is
+// requantized (one division per group) into a staged smem tile that thread 0 bulk-stores to
+// unit m' (P2P transport: the receive slot of node m' itself -- the inter all-to-all).
+// =====================================================================================
+constexpr int kK4Threads = 128;
+constexpr int kK4Ctas = 4;
+constexpr int kK4Tile = kK4Threads * 64;
+
+template <int BIN, int BOUT>
+struct K4Cfg {
+  static constexpr int CODE_BYTES = kK4Tile * BIN / 8;
+  static constexpr int SC_BYTES = BIN == 32 ? 0 : kK4Tile / 32 * 4;
+  static constexpr int STAGE = CODE_BYTES + SC_BYTES;
+  static constexpr int OUT_TILE = kK4Tile * BOUT / 8 + kK4Tile / 32 * 4;  // staged output: codes + scales
+  static constexpr int OUTB = OUT_TILE <= 8 * 1024 ? 4 : 2;  // staged remote output tiles in flight
+  static constexpr int S0 = (54 * 1024 - OUTB * OUT_TILE) / STAGE;  // ~54 KB per CTA: kK4Ctas per SM
+  static constexpr int STAGES = S0 > 8 ? 8 : (S0 < 1 ? 1 : S0);
+  static constexpr int SMEM = STAGES * STAGE + OUTB * OUT_TILE + 64 + 128;
+  static_assert(SMEM <= 227 * 1024, "K4 tile configuration exceeds the per-CTA shared memory");
+  static constexpr int CPT = 64 * BIN / 8 / 16;   // 16-byte chunks per thread
+  static constexpr int EPC = 64 / CPT;            // elements per chunk
+};
+
+// Producer cursor over (tile, source) items of this CTA, advanced without divisions.
+struct ItemCursor {
+  uint32_t l;
+  TileIter it;
+  __device__ explicit ItemCursor(uint32_t units) : l(0), it(units) {}
+  __device__ void next(uint32_t n_src) {
+    if (++l == n_src) {
+      l = 0;
+      it.next();
+    }
+  }
+};
+
+// K4 helper: decode + dequantize the thread's 64 codes of one source (slot order; chunk c holds
+// elements of half ((c ^ f) * EPC) >> 5) and fold them into acc.  FIRST: acc = x (for quantized
+// inputs 0 + x_0 == x_0 since a dequantized code is never -0; the identity codec keeps the add
+// so that -0 becomes +0 as in R8's acc = 0; acc += x); else acc += x.
+template <int BIN, int CPT, int EPC, bool FIRST>
+__device__ __forceinline__ void k4_item(const uint8_t* codes, float ds0, float ds1, int f, float z, float2* acc) {
+  constexpr float kDec = BIN == 8 ? kDec8 : kDec4;
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const uint4 u = *reinterpret_cast<const uint4*>(codes + 16 * (c ^ f));
+    float2* ac = acc + c * (EPC / 2);
+    if constexpr (BIN == 32) {
+      const float2 x0 = make_float2(__uint_as_float(u.x), __uint_as_float(u.y));
+      const float2 x1 = make_float2(__uint_as_float(u.z), __uint_as_float(u.w));
+      ac[0] = f2add(FIRST ? make_float2(0.f, 0.f) : ac[0], x0);
+      ac[1] = f2add(FIRST ? make_float2(0.f, 0.f) : ac[1], x1);
+    } else {
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+      const float2 dec = make_float2(-kDec, -kDec);
+      const float d = (((c ^ f) * EPC) >> 5) ? ds1 : ds0;
+      const float2 dd = make_float2(d, d);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float2 v[BIN == 8 ? 2 : 4];
+        if constexpr (BIN == 8) {  // 4 codes
+          const uint32_t xw = w[q] ^ 0x80808080u;
+          v[0] = f2add(make_float2(__uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7540)),
+                                   __uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7541))), dec);
+          v[1] = f2add(make_float2(__uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7542)),
+                                   __uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7543))), dec);
+        } else {  // 8 codes
+          const uint32_t xw = w[q] ^ 0x88888888u;
+          const uint32_t lo = xw & 0x0F0F0F0Fu, hi = (xw >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            v[b] = f2add(make_float2(__uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7540 + b)),
+                                     __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7540 + b))), dec);
+        }
+        constexpr int NV = BIN == 8 ? 2 : 4;
+#pragma unroll
+        for (int b = 0; b < NV; ++b) {
+          const float2 x = f2mulz(v[b], dd, z);  // rn(code * ds) (R5); added next: fusion barrier
+          if constexpr (FIRST) ac[NV * q + b] = x;
+          else ac[NV * q + b] = f2add(ac[NV * q + b], x);
+        }
+      }
+    }
+  }
+}
+
+struct K4Pull {  // IntraPull, K4 side: tiles of source l with ts % den < num come from src[l]
+  const uint8_t* src[kMaxN];
+  uint32_t mask, num, den;
+};
+
+template <int BIN, int BOUT, bool STOCH>
+__global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
+                                                          int N, int M, size_t S, int lg, const Dests dst,
+                                                          uint32_t tpu, uint32_t ntiles, float z, const SR sr,
+                                                          int l_self, size_t sr_stride, size_t sr_off,
+                                                          const K4Pull pull) {
+  using C = K4Cfg<BIN, BOUT>;
+  constexpr int STAGES = C::STAGES, CPT = C::CPT, EPC = C::EPC;
+  constexpr float qin = float((1 << (BIN == 32 ? 1 : BIN - 1)) - 1);
+  constexpr float qout = float((1 << (BOUT == 32 ? 1 : BOUT - 1)) - 1);
+  constexpr float kDec = BIN == 8 ? kDec8 : kDec4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint8_t* out_buf = smem + STAGES * C::STAGE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(out_buf + C::OUTB * C::OUT_TILE);
+  const int t = threadIdx.x;
+  if (t == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  ItemCursor pc((uint32_t)M);
+  uint32_t pk = 0;
+  auto issue = [&]() {  // thread 0: next item of the producer cursor into its ring slot
+    if (pc.it.ts < tpu) {
+      const int s = pk % STAGES;
+      const size_t e0 = (size_t)pc.it.ts * kK4Tile;
+      const uint32_t n = (uint32_t)min((size_t)kK4Tile, S - e0);
+      // K3 tile (kTileElems) holding these elements: pulled from the source's outbox or pushed
+      const bool pulled = ((pull.mask >> pc.l) & 1u) && (uint32_t)(e0 / kTileElems) % pull.den < pull.num;
+      const uint8_t* unit = pulled ? pull.src[pc.l] + (size_t)pc.it.unit * in_unit_bytes
+                                   : recv + ((size_t)pc.l * M + pc.it.unit) * in_unit_bytes;
+      const uint32_t cb = n * BIN / 8;
+      uint32_t sb = 0;
+      if constexpr (BIN != 32) sb = (((n >> lg) * 4) + 15) & ~15u;
+      mbar_arrive_tx(&bar[s], cb + sb);
+      bulk_load(smem + s * C::STAGE, unit + e0 * BIN / 8, cb, &bar[s]);
+      if constexpr (BIN != 32)
+        bulk_load(smem + s * C::STAGE + C::CODE_BYTES, unit + S * BIN / 8 + (e0 >> lg) * 4, sb, &bar[s]);
+    }
+    ++pk;
+    pc.next(N);
+  };
+  if (t == 0)
+    for (int k = 0; k < STAGES; ++k) issue();
+
+  // slot c of this thread holds chunk c ^ f (f = 0 for the fp32 identity path)
+  const int f = BIN == 32 ? 0 : (CPT >= 8 ? (t & 7) : ((t / (8 / CPT)) & (CPT - 1)));
+  const int tpg = lg >= 6 ? (1 << (lg - 6)) : 1;  // threads per group
+  TileIter it((uint32_t)M);
+  uint32_t k = 0;
+  for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i, it.next()) {
+    const uint32_t mp = it.unit;
+    const size_t e0 = (size_t)it.ts * kK4Tile;
+    const bool act = e0 + 64 * t < S;
+    float2 acc[32];  // slot order: acc[i] = elements (2i, 2i+1) of the slot-ordered 64
+    // one (tile, source) item: wait for its ring slot, dequantize, fold into acc (R8), release
+    auto consume = [&](auto first) {
+      const int s = k % STAGES;
+      mbar_wait(&bar[s], (k / STAGES) & 1);
+      const uint8_t* codes = smem + s * C::STAGE + t * (64 * BIN / 8);
+      float ds0 = 1.f, ds1 = 1.f;
+      if constexpr (BIN != 32) {
+        const float* sc = reinterpret_cast<const float*>(smem + s * C::STAGE + C::CODE_BYTES);
+        if (lg >= 6) {
+          ds0 = ds1 = __fdiv_rn(sc[(64 * t) >> lg], qin);
+        } else {
+          ds0 = __fdiv_rn(sc[2 * t], qin);
+          ds1 = __fdiv_rn(sc[2 * t + 1], qin);
+        }
+      }
+      k4_item<BIN, CPT, EPC, decltype(first)::value>(codes, ds0, ds1, f, z, acc);
+      __syncthreads();
+      if (t == 0) issue();
+      ++k;
+    };
+    // the first source is dequantized straight into acc (no copies); the rest are added in
+    // source order l'' = 1..N-1
+    consume(std::true_type{});
+    for (int l = 1; l < N; ++l) consume(std::false_type{});
+
+    // ---- requantize at BOUT bits into the staged output tile; 16-element vectors v = 0..3
+    // in slot order, written at their element positions (undoing the slot permutation)
+    // local destination: write global memory directly (L2 merges the partial sectors);
+    // peer destination: stage the tile in smem and bulk-store it (contiguous NVLink writes)
+    const bool remote = (dst.remote >> mp) & 1ull;  // CTA-uniform
+    uint8_t* gout = dst.p[mp];
+    uint8_t* ot = remote ? out_buf + (i % C::OUTB) * C::OUT_TILE : gout + e0 * BOUT / 8;
+    float* osc = remote ? reinterpret_cast<float*>(ot + kK4Tile * BOUT / 8)
+                        : reinterpret_cast<float*>(gout + S * BOUT / 8) + (e0 >> lg);
+    if (remote) {
+      if (t == 0) bulk_wait_read<C::OUTB - 1>();  // the stores of tile i - OUTB have left out_buf[i % OUTB]
+      __syncthreads();
+    }
+    auto vbase = [&](int v) {  // element offset (within the thread's 64) of slot-order vector v
+      if constexpr (EPC >= 16) return (((16 * v) / EPC) ^ f) * EPC + (16 * v) % EPC;
+      else return 16 * v;
+    };
+    if constexpr (BOUT == 32) {
+      if (act) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          float4* o = reinterpret_cast<float4*>(ot + (64 * t + vbase(v)) * 4);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            o[q] = make_float4(acc[8 * v + 2 * q].x, acc[8 * v + 2 * q].y, acc[8 * v + 2 * q + 1].x,
+                               acc[8 * v + 2 * q + 1].y);
+        }
+      }
+    } else {
+      float am[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        float a = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a = max3_abs_nan(a, acc[8 * v + q].x, acc[8 * v + q].y);
+        am[v] = a;
+      }
+      QP p0, p1;
+      float a0, a1;
+      if (lg >= 6) {
+        a0 = max_nan(max_nan(am[0], am[1]), max_nan(am[2], am[3]));
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1)
+          if (off < tpg) a0 = max_nan(a0, __shfl_xor_sync(0xffffffffu, a0, off));
+        a1 = a0;
+        p0 = qparam(a0, qout);
+        p1 = p0;
+      } else {  // G == 32: two groups per thread (element halves)
+        a0 = 0.f;
+        a1 = 0.f;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          if (vbase(v) >> 5) a1 = max_nan(a1, am[v]);
+          else a0 = max_nan(a0, am[v]);
+        }
+        p0 = qparam(a0, qout);
+        p1 = qparam(a1, qout);
+      }
+      if (act) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const bool h = (vbase(v) >> 5) != 0;
+          const float iv = h ? p1.inv : p0.inv;
+          uint32_t r[16];
+          const int e = 64 * t + vbase(v);
+          if constexpr (STOCH) {  // global index of the shard element (mp*N + l)*S_full + off + e0 + e (R14)
+            const uint64_t i0 = (uint64_t)(mp * N + l_self) * sr_stride + sr_off + e0 + e;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              r[2 * q] = rq_sr(acc[8 * v + q].x, iv, sr_u(i0 + 2 * q, sr.key), qout);
+              r[2 * q + 1] = rq_sr(acc[8 * v + q].y, iv, sr_u(i0 + 2 * q + 1, sr.key), qout);
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float2 y = f2rq(acc[8 * v + q], make_float2(iv, iv));
+              r[2 * q] = __float_as_uint(y.x);
+              r[2 * q + 1] = __float_as_uint(y.y);
+            }
+          }
+          const bool okv = h ? p1.ok : p0.ok;
+          if constexpr (BOUT == 4) {
+            uint2 w = make_uint2(pack4x8(r), pack4x8(r + 8));
+            if (!okv) w = make_uint2(0u, 0u);
+            *reinterpret_cast<uint2*>(ot + e / 2) = w;
+          } else {
+            uint4 w = make_uint4(pack8x4(r[0], r[1], r[2], r[3]), pack8x4(r[4], r[5], r[6], r[7]),
+                                 pack8x4(r[8], r[9], r[10], r[11]), pack8x4(r[12], r[13], r[14], r[15]));
+            if (!okv) w = make_uint4(0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(ot + e) = w;
+          }
+        }
+        if (lg >= 6) {
+          if ((t & (tpg - 1)) == 0) osc[(64 * t) >> lg] = stored_scale(a0, 1.f);
+        } else {
+          *reinterpret_cast<float2*>(osc + 2 * t) = make_float2(stored_scale(a0, 1.f), stored_scale(a1, 1.f));
+        }
+      }
+    }
+    if (remote) {  // unit m' -> node m' (P2P: the peer's receive slot -- Alg. 3 l.10)
+      fence_proxy_async();
+      __syncthreads();
+      const uint32_t n = (uint32_t)min((size_t)kK4Tile, S - e0);
+      store_tile(ot, n * BOUT / 8, osc, BOUT == 32 ? 0u : (n >> lg), gout + e0 * BOUT / 8,
+                 reinterpret_cast<float*>(gout + S * BOUT / 8) + (e0 >> lg));
+      if (t == 0) bulk_commit();
+    }
+  }
+  if (t == 0) bulk_wait<0>();
+}
+
+
+template <int BIN, int BOUT, bool STOCH>
+cudaError_t k4_launch_t(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
+                        const SR& sr, int l_self, size_t sr_stride, size_t sr_off, int sms, cudaStream_t st,
+                        const K4Pull& pull) {
+  constexpr int SMEM = K4Cfg<BIN, BOUT>::SMEM;
+  cudaError_t e = set_smem(k4_tlq_dq_reduce_q<BIN, BOUT, STOCH>, SMEM);
+  if (e != cudaSuccess) return e;
+  const uint32_t tpu = (uint32_t)((S + kK4Tile - 1) / kK4Tile);
+  const uint32_t ntiles = tpu * (uint32_t)M;
+  const int grid = grid_for(ntiles, sms * kK4Ctas);
+  k4_tlq_dq_reduce_q<BIN, BOUT, STOCH><<<grid, kK4Threads, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G),
+                                                                dst, tpu, ntiles, -0.0f, sr, l_self, sr_stride, sr_off,
+                                                                pull);
+  return cudaGetLastError();
+}
+template <int BIN, int BOUT>
+cudaError_t k4_launch(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
+                      const SR& sr, int l_self, size_t sr_stride, size_t sr_off, int sms, cudaStream_t st,
+                      const K4Pull& pull) {
+  if constexpr (BOUT != 32) {
+    if (sr.on)
+      return k4_launch_t<BIN, BOUT, true>(recv, in_unit_bytes, N, M, S, G, dst, sr, l_self, sr_stride, sr_off, sms, st,
+                                          pull);
+  }
+  return k4_launch_t<BIN, BOUT, false>(recv, in_unit_bytes, N, M, S, G, dst, sr, l_self, sr_stride, sr_off, sms, st,
+                                       pull);
+}
+
+
+}  // namespace
+
+cudaError_t launch_tlq_dq_reduce_q(const uint8_t* intra_recv, size_t in_unit_bytes, int bits_in,
+                                   int N, int M, size_t S, int G, const Dests& dst, int bits_out, int sr_on,
+                                   uint32_t sr_key, int l_self, size_t sr_stride, size_t sr_off, int sms,
+                                   cudaStream_t st, const IntraPull* pull) {
+  if (M > kMaxDests || N > kMaxN) return cudaErrorInvalidValue;
+  const SR sr{sr_on, sr_key};
+  K4Pull kp;
+  memset(&kp, 0, sizeof(kp));
+  kp.den = 1;
+  if (pull && pull->num > 0) {
+    kp.mask = pull->mask;
+    kp.num = (uint32_t)pull->num;
+    kp.den = (uint32_t)pull->den;
+    for (int l = 0; l < N; ++l) kp.src[l] = pull->src[l];
+  }
+#define K4(BI, BO) return k4_launch<BI, BO>(intra_recv, in_unit_bytes, N, M, S, G, dst, sr, l_self, sr_stride, sr_off, \
+                                            sms, st, kp)
+#define K4O(BI) \
+  if (bits_out == 4) { K4(BI, 4); } else if (bits_out == 8) { K4(BI, 8); } else { K4(BI, 32); }
+  if (bits_in == 4) { K4O(4); } else if (bits_in == 8) { K4O(8); } else { K4O(32); }
+#undef K4O
+#undef K4
+}
+
+
+}  // namespace sdp4
