@@ -6,16 +6,22 @@ namespace {
 
 // =====================================================================================
 // K4  TLq dequantize + reduce + requantize (Alg. 3 l.5, 7, 9, FP32 reduce P:344).
-// Vector layout: a tile is 8192 elements of sub-block m'; thread t owns the 64 contiguous
-// elements [64t, 64t+64), read from smem as 16-byte chunks in XOR-permuted order
+// Vector layout: a tile is 8192 elements of sub-block m'; consumer thread t owns the 64
+// contiguous elements [64t, 64t+64), read from smem as 16-byte chunks in XOR-permuted order
 // (slot c <- chunk c ^ f(t): conflict-free; the permutation is undone by the store
-// addresses).  Thread 0 streams (tile, source l'') items through a STAGES-deep ring of 1-D
-// bulk copies (codes + scales); sources are summed in order l'' = 0..N-1 (R8); the sum is
-// requantized (one division per group) into a staged smem tile that thread 0 bulk-stores to
-// unit m' (P2P transport: the receive slot of node m' itself -- the inter all-to-all).
+// addresses).  Warp-specialized: a dedicated producer warp streams (tile, source l'') items
+// through a STAGES-deep ring of 1-D bulk copies (codes + scales), each slot guarded by a
+// "full" mbarrier (transaction bytes) and an "empty" mbarrier that each of the four consumer
+// warps arrives on when it is done with its quarter -- no CTA-wide barrier per item, so warps
+// drift within the ring depth.  Sources are summed in order l'' = 0..N-1 (R8); the sum is
+// requantized (one division per group; a group spans at most one warp) and stored straight to
+// global memory (local unit), or staged in smem and bulk-stored by consumer thread 0 to unit m'
+// (P2P transport: the receive slot of node m' itself -- the inter all-to-all), with named
+// barriers over the consumer warps only.
 // =====================================================================================
-constexpr int kK4Threads = 128;
-constexpr int kK4Ctas = 4;
+constexpr int kK4Threads = 128;                   // consumer threads (four warps)
+constexpr int kK4Block = kK4Threads + 32;         // + one producer warp
+constexpr int kK4Ctas = 3;
 constexpr int kK4Tile = kK4Threads * 64;
 
 template <int BIN, int BOUT>
@@ -25,9 +31,9 @@ struct K4Cfg {
   static constexpr int STAGE = CODE_BYTES + SC_BYTES;
   static constexpr int OUT_TILE = kK4Tile * BOUT / 8 + kK4Tile / 32 * 4;  // staged output: codes + scales
   static constexpr int OUTB = OUT_TILE <= 8 * 1024 ? 4 : 2;  // staged remote output tiles in flight
-  static constexpr int S0 = (54 * 1024 - OUTB * OUT_TILE) / STAGE;  // ~54 KB per CTA: kK4Ctas per SM
-  static constexpr int STAGES = S0 > 8 ? 8 : (S0 < 1 ? 1 : S0);
-  static constexpr int SMEM = STAGES * STAGE + OUTB * OUT_TILE + 64 + 128;
+  static constexpr int S0 = (74 * 1024 - OUTB * OUT_TILE) / STAGE;  // ~74 KB per CTA: kK4Ctas per SM
+  static constexpr int STAGES = S0 > 8 ? 8 : (S0 < 2 ? 2 : S0);
+  static constexpr int SMEM = STAGES * STAGE + OUTB * OUT_TILE + 2 * 8 * STAGES + 128;
   static_assert(SMEM <= 227 * 1024, "K4 tile configuration exceeds the per-CTA shared memory");
   static constexpr int CPT = 64 * BIN / 8 / 16;   // 16-byte chunks per thread
   static constexpr int EPC = 64 / CPT;            // elements per chunk
@@ -102,50 +108,53 @@ struct K4Pull {  // IntraPull, K4 side: tiles of source l with ts % den < num co
 };
 
 template <int BIN, int BOUT, bool STOCH>
-__global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
+__global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
                                                           int N, int M, size_t S, int lg, const Dests dst,
                                                           uint32_t tpu, uint32_t ntiles, float z, const SR sr,
                                                           int l_self, size_t sr_stride, size_t sr_off,
-                                                          const K4Pull pull) {
+                                                          const K4Pull pull, uint32_t m16) {
   using C = K4Cfg<BIN, BOUT>;
   constexpr int STAGES = C::STAGES, CPT = C::CPT, EPC = C::EPC;
   constexpr float qin = float((1 << (BIN == 32 ? 1 : BIN - 1)) - 1);
   constexpr float qout = float((1 << (BOUT == 32 ? 1 : BOUT - 1)) - 1);
-  constexpr float kDec = BIN == 8 ? kDec8 : kDec4;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint8_t* smem = align_smem<128>(smem_raw);
   uint8_t* out_buf = smem + STAGES * C::STAGE;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(out_buf + C::OUTB * C::OUT_TILE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(out_buf + C::OUTB * C::OUT_TILE);
+  uint64_t* empty = full + STAGES;
   const int t = threadIdx.x;
   if (t == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kK4Threads / 32);
+    }
     fence_mbar_init();
   }
-  __syncthreads();
-  ItemCursor pc((uint32_t)M);
-  uint32_t pk = 0;
-  auto issue = [&]() {  // thread 0: next item of the producer cursor into its ring slot
-    if (pc.it.ts < tpu) {
-      const int s = pk % STAGES;
-      const size_t e0 = (size_t)pc.it.ts * kK4Tile;
-      const uint32_t n = (uint32_t)min((size_t)kK4Tile, S - e0);
-      // K3 tile (kTileElems) holding these elements: pulled from the source's outbox or pushed
-      const bool pulled = ((pull.mask >> pc.l) & 1u) && (uint32_t)(e0 / kTileElems) % pull.den < pull.num;
-      const uint8_t* unit = pulled ? pull.src[pc.l] + (size_t)pc.it.unit * in_unit_bytes
-                                   : recv + ((size_t)pc.l * M + pc.it.unit) * in_unit_bytes;
-      const uint32_t cb = n * BIN / 8;
-      uint32_t sb = 0;
-      if constexpr (BIN != 32) sb = (((n >> lg) * 4) + 15) & ~15u;
-      mbar_arrive_tx(&bar[s], cb + sb);
-      bulk_load(smem + s * C::STAGE, unit + e0 * BIN / 8, cb, &bar[s]);
-      if constexpr (BIN != 32)
-        bulk_load(smem + s * C::STAGE + C::CODE_BYTES, unit + S * BIN / 8 + (e0 >> lg) * 4, sb, &bar[s]);
+  __syncthreads();  // the only CTA-wide barrier
+  if (t >= kK4Threads) {  // ---- producer warp: one lane streams every (tile, source) item
+    if (t == kK4Threads) {
+      ItemCursor pc((uint32_t)M);
+      for (uint32_t pk = 0; pc.it.ts < tpu; ++pk) {  // tile < ntiles <=> ts < tpu
+        const int s = pk % STAGES;
+        mbar_wait(&empty[s], ((pk / STAGES) & 1) ^ 1);  // the consumers released this slot
+        const size_t e0 = (size_t)pc.it.ts * kK4Tile;
+        const uint32_t n = (uint32_t)min((size_t)kK4Tile, S - e0);
+        // K3 tile (kTileElems) holding these elements: pulled from the source's outbox or pushed
+        const bool pulled = ((pull.mask >> pc.l) & 1u) && (uint32_t)(e0 / kTileElems) % pull.den < pull.num;
+        const uint8_t* unit = pulled ? pull.src[pc.l] + (size_t)pc.it.unit * in_unit_bytes
+                                     : recv + ((size_t)pc.l * M + pc.it.unit) * in_unit_bytes;
+        const uint32_t cb = n * BIN / 8;
+        uint32_t sb = 0;
+        if constexpr (BIN != 32) sb = (((n >> lg) * 4) + 15) & ~15u;
+        mbar_arrive_tx(&full[s], cb + sb);
+        bulk_load(smem + s * C::STAGE, unit + e0 * BIN / 8, cb, &full[s]);
+        if constexpr (BIN != 32)
+          bulk_load(smem + s * C::STAGE + C::CODE_BYTES, unit + S * BIN / 8 + (e0 >> lg) * 4, sb, &full[s]);
+        pc.next(N);
+      }
     }
-    ++pk;
-    pc.next(N);
-  };
-  if (t == 0)
-    for (int k = 0; k < STAGES; ++k) issue();
+    return;
+  }
 
   // slot c of this thread holds chunk c ^ f (f = 0 for the fp32 identity path)
   const int f = BIN == 32 ? 0 : (CPT >= 8 ? (t & 7) : ((t / (8 / CPT)) & (CPT - 1)));
@@ -160,7 +169,7 @@ __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const 
     // one (tile, source) item: wait for its ring slot, dequantize, fold into acc (R8), release
     auto consume = [&](auto first) {
       const int s = k % STAGES;
-      mbar_wait(&bar[s], (k / STAGES) & 1);
+      mbar_wait(&full[s], (k / STAGES) & 1);
       const uint8_t* codes = smem + s * C::STAGE + t * (64 * BIN / 8);
       float ds0 = 1.f, ds1 = 1.f;
       if constexpr (BIN != 32) {
@@ -173,8 +182,8 @@ __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const 
         }
       }
       k4_item<BIN, CPT, EPC, decltype(first)::value>(codes, ds0, ds1, f, z, acc);
-      __syncthreads();
-      if (t == 0) issue();
+      __syncwarp();
+      if ((t & 31) == 0) mbar_arrive(&empty[s]);  // this warp is done with its quarter of slot s
       ++k;
     };
     // the first source is dequantized straight into acc (no copies); the rest are added in
@@ -188,12 +197,15 @@ __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const 
     // peer destination: stage the tile in smem and bulk-store it (contiguous NVLink writes)
     const bool remote = (dst.remote >> mp) & 1ull;  // CTA-uniform
     uint8_t* gout = dst.p[mp];
-    uint8_t* ot = remote ? out_buf + (i % C::OUTB) * C::OUT_TILE : gout + e0 * BOUT / 8;
-    float* osc = remote ? reinterpret_cast<float*>(ot + kK4Tile * BOUT / 8)
-                        : reinterpret_cast<float*>(gout + S * BOUT / 8) + (e0 >> lg);
+    // output codes / scales: the staged smem tile (remote) or the unit in global memory (local);
+    // two explicit address spaces, so stores are STS / STG rather than generic
+    uint8_t* ot_s = out_buf + (i % C::OUTB) * C::OUT_TILE;
+    uint8_t* ot_g = gout + e0 * BOUT / 8;
+    float* osc_s = reinterpret_cast<float*>(ot_s + kK4Tile * BOUT / 8);
+    float* osc_g = reinterpret_cast<float*>(gout + S * BOUT / 8) + (e0 >> lg);
     if (remote) {
       if (t == 0) bulk_wait_read<C::OUTB - 1>();  // the stores of tile i - OUTB have left out_buf[i % OUTB]
-      __syncthreads();
+      named_sync(1, kK4Threads);
     }
     auto vbase = [&](int v) {  // element offset (within the thread's 64) of slot-order vector v
       if constexpr (EPC >= 16) return (((16 * v) / EPC) ^ f) * EPC + (16 * v) % EPC;
@@ -203,14 +215,19 @@ __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const 
       if (act) {
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-          float4* o = reinterpret_cast<float4*>(ot + (64 * t + vbase(v)) * 4);
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            o[q] = make_float4(acc[8 * v + 2 * q].x, acc[8 * v + 2 * q].y, acc[8 * v + 2 * q + 1].x,
-                               acc[8 * v + 2 * q + 1].y);
+          for (int q = 0; q < 4; ++q) {
+            const float4 w = make_float4(acc[8 * v + 2 * q].x, acc[8 * v + 2 * q].y, acc[8 * v + 2 * q + 1].x,
+                                         acc[8 * v + 2 * q + 1].y);
+            const int off = (64 * t + vbase(v)) * 4 + 16 * q;
+            if (remote) *reinterpret_cast<float4*>(ot_s + off) = w;
+            else *reinterpret_cast<float4*>(ot_g + off) = w;
+          }
         }
       }
     } else {
+      // 4-bit output codes come out of the quantizer biased by 8 (pack4x8_b)
+      constexpr float magic = BOUT == 4 ? kMagicB4 : kMagic;
       float am[4];
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
@@ -251,42 +268,48 @@ __global__ void __launch_bounds__(kK4Threads, kK4Ctas) k4_tlq_dq_reduce_q(const 
             const uint64_t i0 = (uint64_t)(mp * N + l_self) * sr_stride + sr_off + e0 + e;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              r[2 * q] = rq_sr(acc[8 * v + q].x, iv, sr_u(i0 + 2 * q, sr.key), qout);
-              r[2 * q + 1] = rq_sr(acc[8 * v + q].y, iv, sr_u(i0 + 2 * q + 1, sr.key), qout);
+              r[2 * q] = rq_sr(acc[8 * v + q].x, iv, sr_u(i0 + 2 * q, sr.key), qout, magic);
+              r[2 * q + 1] = rq_sr(acc[8 * v + q].y, iv, sr_u(i0 + 2 * q + 1, sr.key), qout, magic);
             }
           } else {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              const float2 y = f2rq(acc[8 * v + q], make_float2(iv, iv));
+              const float2 y = f2rq(acc[8 * v + q], make_float2(iv, iv), magic);
               r[2 * q] = __float_as_uint(y.x);
               r[2 * q + 1] = __float_as_uint(y.y);
             }
           }
           const bool okv = h ? p1.ok : p0.ok;
           if constexpr (BOUT == 4) {
-            uint2 w = make_uint2(pack4x8(r), pack4x8(r + 8));
+            uint2 w = make_uint2(pack4x8_b(r, m16), pack4x8_b(r + 8, m16));
             if (!okv) w = make_uint2(0u, 0u);
-            *reinterpret_cast<uint2*>(ot + e / 2) = w;
+            if (remote) *reinterpret_cast<uint2*>(ot_s + e / 2) = w;
+            else *reinterpret_cast<uint2*>(ot_g + e / 2) = w;
           } else {
             uint4 w = make_uint4(pack8x4(r[0], r[1], r[2], r[3]), pack8x4(r[4], r[5], r[6], r[7]),
                                  pack8x4(r[8], r[9], r[10], r[11]), pack8x4(r[12], r[13], r[14], r[15]));
             if (!okv) w = make_uint4(0u, 0u, 0u, 0u);
-            *reinterpret_cast<uint4*>(ot + e) = w;
+            if (remote) *reinterpret_cast<uint4*>(ot_s + e) = w;
+            else *reinterpret_cast<uint4*>(ot_g + e) = w;
           }
         }
         if (lg >= 6) {
-          if ((t & (tpg - 1)) == 0) osc[(64 * t) >> lg] = stored_scale(a0, 1.f);
+          if ((t & (tpg - 1)) == 0) {
+            if (remote) osc_s[(64 * t) >> lg] = stored_scale(a0, 1.f);
+            else osc_g[(64 * t) >> lg] = stored_scale(a0, 1.f);
+          }
         } else {
-          *reinterpret_cast<float2*>(osc + 2 * t) = make_float2(stored_scale(a0, 1.f), stored_scale(a1, 1.f));
+          const float2 w = make_float2(stored_scale(a0, 1.f), stored_scale(a1, 1.f));
+          if (remote) *reinterpret_cast<float2*>(osc_s + 2 * t) = w;
+          else *reinterpret_cast<float2*>(osc_g + 2 * t) = w;
         }
       }
     }
     if (remote) {  // unit m' -> node m' (P2P: the peer's receive slot -- Alg. 3 l.10)
       fence_proxy_async();
-      __syncthreads();
+      named_sync(1, kK4Threads);
       const uint32_t n = (uint32_t)min((size_t)kK4Tile, S - e0);
-      store_tile(ot, n * BOUT / 8, osc, BOUT == 32 ? 0u : (n >> lg), gout + e0 * BOUT / 8,
-                 reinterpret_cast<float*>(gout + S * BOUT / 8) + (e0 >> lg));
+      store_tile(ot_s, n * BOUT / 8, osc_s, BOUT == 32 ? 0u : (n >> lg), ot_g, osc_g);
       if (t == 0) bulk_commit();
     }
   }
@@ -304,9 +327,9 @@ cudaError_t k4_launch_t(const uint8_t* recv, size_t in_unit_bytes, int N, int M,
   const uint32_t tpu = (uint32_t)((S + kK4Tile - 1) / kK4Tile);
   const uint32_t ntiles = tpu * (uint32_t)M;
   const int grid = grid_for(ntiles, sms * kK4Ctas);
-  k4_tlq_dq_reduce_q<BIN, BOUT, STOCH><<<grid, kK4Threads, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G),
+  k4_tlq_dq_reduce_q<BIN, BOUT, STOCH><<<grid, kK4Block, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G),
                                                                 dst, tpu, ntiles, -0.0f, sr, l_self, sr_stride, sr_off,
-                                                                pull);
+                                                                pull, 16u);
   return cudaGetLastError();
 }
 template <int BIN, int BOUT>

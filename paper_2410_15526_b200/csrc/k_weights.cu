@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply_ring(const Dests uni
   constexpr int ROUNDS = kK2rTile / (kVecThreads * 8);
   constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint8_t* smem = align_smem<128>(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kK2rStages * C::STAGE);
   const int t = threadIdx.x;
   // U units (U = P, or P - 1 when the owner applied its own in K1), unit fastest, starting at rot
