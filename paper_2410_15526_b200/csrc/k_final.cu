@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(kK5Block, kK5Ctas)
   }
 
   constexpr float qin = float((1 << (BIN == 32 ? 1 : BIN - 1)) - 1);
+  const float rqin = __fdiv_rn(1.f, qin);  // rn(1/q): div_by_q's reciprocal (constant-folded)
   const int lane = t & 31, warp = t >> 5;
   uint8_t* ob = out_buf + warp * C::OUT_WARP;  // this warp's transpose tile
   uint32_t k = 0;
@@ -118,11 +119,11 @@ __global__ void __launch_bounds__(kK5Block, kK5Ctas)
       if constexpr (BIN != 32) {
         const float* sc = reinterpret_cast<const float*>(st + C::IN_TILE);
         if (lg >= 6) {
-          ds0 = ds1 = __fdiv_rn(sc[t >> (lg - 6)], qin);
+          ds0 = ds1 = div_by_q(sc[t >> (lg - 6)], qin, rqin);
         } else {
           const float2 s2 = *reinterpret_cast<const float2*>(sc + 2 * t);
-          ds0 = __fdiv_rn(s2.x, qin);
-          ds1 = __fdiv_rn(s2.y, qin);
+          ds0 = div_by_q(s2.x, qin, rqin);
+          ds1 = div_by_q(s2.y, qin, rqin);
         }
       }
       // R8 order; the first add 0 + x_0 is exact for quantized inputs (x_0 != -0), so source 0

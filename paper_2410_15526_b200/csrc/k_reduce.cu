@@ -23,6 +23,8 @@ constexpr int kK4Threads = 128;                   // consumer threads (four warp
 constexpr int kK4Block = kK4Threads + 32;         // + one producer warp
 constexpr int kK4Ctas = 3;
 constexpr int kK4Tile = kK4Threads * 64;
+constexpr int kK4Chunk = 8;  // tiles per scheduler claim
+constexpr uint32_t kNoTile = 0xffffffffu;
 
 template <int BIN, int BOUT>
 struct K4Cfg {
@@ -33,23 +35,10 @@ struct K4Cfg {
   static constexpr int OUTB = OUT_TILE <= 8 * 1024 ? 4 : 2;  // staged remote output tiles in flight
   static constexpr int S0 = (74 * 1024 - OUTB * OUT_TILE) / STAGE;  // ~74 KB per CTA: kK4Ctas per SM
   static constexpr int STAGES = S0 > 8 ? 8 : (S0 < 2 ? 2 : S0);
-  static constexpr int SMEM = STAGES * STAGE + OUTB * OUT_TILE + 2 * 8 * STAGES + 128;
+  static constexpr int SMEM = STAGES * STAGE + OUTB * OUT_TILE + 2 * 8 * STAGES + 4 * STAGES + 128;
   static_assert(SMEM <= 227 * 1024, "K4 tile configuration exceeds the per-CTA shared memory");
   static constexpr int CPT = 64 * BIN / 8 / 16;   // 16-byte chunks per thread
   static constexpr int EPC = 64 / CPT;            // elements per chunk
-};
-
-// Producer cursor over (tile, source) items of this CTA, advanced without divisions.
-struct ItemCursor {
-  uint32_t l;
-  TileIter it;
-  __device__ explicit ItemCursor(uint32_t units) : l(0), it(units) {}
-  __device__ void next(uint32_t n_src) {
-    if (++l == n_src) {
-      l = 0;
-      it.next();
-    }
-  }
 };
 
 // K4 helper: decode + dequantize the thread's 64 codes of one source (slot order; chunk c holds
@@ -112,16 +101,18 @@ __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const ui
                                                           int N, int M, size_t S, int lg, const Dests dst,
                                                           uint32_t tpu, uint32_t ntiles, float z, const SR sr,
                                                           int l_self, size_t sr_stride, size_t sr_off,
-                                                          const K4Pull pull, uint32_t m16) {
+                                                          const K4Pull pull, uint32_t m16, uint32_t* sched) {
   using C = K4Cfg<BIN, BOUT>;
   constexpr int STAGES = C::STAGES, CPT = C::CPT, EPC = C::EPC;
   constexpr float qin = float((1 << (BIN == 32 ? 1 : BIN - 1)) - 1);
+  const float rqin = __fdiv_rn(1.f, qin);  // rn(1/q): div_by_q's reciprocal (constant-folded)
   constexpr float qout = float((1 << (BOUT == 32 ? 1 : BOUT - 1)) - 1);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem<128>(smem_raw);
   uint8_t* out_buf = smem + STAGES * C::STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(out_buf + C::OUTB * C::OUT_TILE);
   uint64_t* empty = full + STAGES;
+  uint32_t* tile_of = reinterpret_cast<uint32_t*>(empty + STAGES);  // tile id carried by each slot
   const int t = threadIdx.x;
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -131,27 +122,40 @@ __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const ui
     fence_mbar_init();
   }
   __syncthreads();  // the only CTA-wide barrier
-  if (t >= kK4Threads) {  // ---- producer warp: one lane streams every (tile, source) item
+  if (t >= kK4Threads) {  // ---- producer warp: one lane claims tiles and streams their (tile, source) items
     if (t == kK4Threads) {
-      ItemCursor pc((uint32_t)M);
-      for (uint32_t pk = 0; pc.it.ts < tpu; ++pk) {  // tile < ntiles <=> ts < tpu
-        const int s = pk % STAGES;
-        mbar_wait(&empty[s], ((pk / STAGES) & 1) ^ 1);  // the consumers released this slot
-        const size_t e0 = (size_t)pc.it.ts * kK4Tile;
-        const uint32_t n = (uint32_t)min((size_t)kK4Tile, S - e0);
-        // K3 tile (kTileElems) holding these elements: pulled from the source's outbox or pushed
-        const bool pulled = ((pull.mask >> pc.l) & 1u) && (uint32_t)(e0 / kTileElems) % pull.den < pull.num;
-        const uint8_t* unit = pulled ? pull.src[pc.l] + (size_t)pc.it.unit * in_unit_bytes
-                                     : recv + ((size_t)pc.l * M + pc.it.unit) * in_unit_bytes;
-        const uint32_t cb = n * BIN / 8;
-        uint32_t sb = 0;
-        if constexpr (BIN != 32) sb = (((n >> lg) * 4) + 15) & ~15u;
-        mbar_arrive_tx(&full[s], cb + sb);
-        bulk_load(smem + s * C::STAGE, unit + e0 * BIN / 8, cb, &full[s]);
-        if constexpr (BIN != 32)
-          bulk_load(smem + s * C::STAGE + C::CODE_BYTES, unit + S * BIN / 8 + (e0 >> lg) * 4, sb, &full[s]);
-        pc.next(N);
+      uint32_t pk = 0;
+      for (;;) {
+        const uint32_t t0 = sched_claim(sched, kK4Chunk);
+        if (t0 >= ntiles) break;
+        const uint32_t t1 = min(t0 + kK4Chunk, ntiles);
+        for (uint32_t tile = t0; tile < t1; ++tile) {
+          const uint32_t ts = tile / (uint32_t)M, mp = tile - ts * (uint32_t)M;  // unit fastest
+          const size_t e0 = (size_t)ts * kK4Tile;
+          const uint32_t n = (uint32_t)min((size_t)kK4Tile, S - e0);
+          const uint32_t cb = n * BIN / 8;
+          uint32_t sb = 0;
+          if constexpr (BIN != 32) sb = (((n >> lg) * 4) + 15) & ~15u;
+          for (int l = 0; l < N; ++l, ++pk) {  // sources l'' = 0..N-1 (R8)
+            const int s = pk % STAGES;
+            mbar_wait(&empty[s], ((pk / STAGES) & 1) ^ 1);  // the consumers released this slot
+            tile_of[s] = (ts << 6) | mp;  // (tile-in-unit, unit): M <= 64
+            // K3 tile (kTileElems) holding these elements: pulled from the source's outbox or pushed
+            const bool pulled = ((pull.mask >> l) & 1u) && (uint32_t)(e0 / kTileElems) % pull.den < pull.num;
+            const uint8_t* unit = pulled ? pull.src[l] + (size_t)mp * in_unit_bytes
+                                         : recv + ((size_t)l * M + mp) * in_unit_bytes;
+            mbar_arrive_tx(&full[s], cb + sb);  // release: tile_of[s] is visible with the data
+            bulk_load(smem + s * C::STAGE, unit + e0 * BIN / 8, cb, &full[s]);
+            if constexpr (BIN != 32)
+              bulk_load(smem + s * C::STAGE + C::CODE_BYTES, unit + S * BIN / 8 + (e0 >> lg) * 4, sb, &full[s]);
+          }
+        }
       }
+      const int s = pk % STAGES;  // end of work: a slot carrying no data, tile id kNoTile
+      mbar_wait(&empty[s], ((pk / STAGES) & 1) ^ 1);
+      tile_of[s] = kNoTile;
+      mbar_arrive(&full[s]);
+      sched_done(sched);
     }
     return;
   }
@@ -159,11 +163,16 @@ __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const ui
   // slot c of this thread holds chunk c ^ f (f = 0 for the fp32 identity path)
   const int f = BIN == 32 ? 0 : (CPT >= 8 ? (t & 7) : ((t / (8 / CPT)) & (CPT - 1)));
   const int tpg = lg >= 6 ? (1 << (lg - 6)) : 1;  // threads per group
-  TileIter it((uint32_t)M);
   uint32_t k = 0;
-  for (uint32_t i = 0; blockIdx.x + i * gridDim.x < ntiles; ++i, it.next()) {
-    const uint32_t mp = it.unit;
-    const size_t e0 = (size_t)it.ts * kK4Tile;
+  for (uint32_t i = 0;; ++i) {
+    {  // the tile of the next item (kNoTile: no more work)
+      const int s = k % STAGES;
+      mbar_wait(&full[s], (k / STAGES) & 1);
+    }
+    const uint32_t tile = tile_of[k % STAGES];
+    if (tile == kNoTile) break;
+    const uint32_t ts = tile >> 6, mp = tile & 63u;
+    const size_t e0 = (size_t)ts * kK4Tile;
     const bool act = e0 + 64 * t < S;
     float2 acc[32];  // slot order: acc[i] = elements (2i, 2i+1) of the slot-ordered 64
     // one (tile, source) item: wait for its ring slot, dequantize, fold into acc (R8), release
@@ -175,10 +184,10 @@ __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const ui
       if constexpr (BIN != 32) {
         const float* sc = reinterpret_cast<const float*>(smem + s * C::STAGE + C::CODE_BYTES);
         if (lg >= 6) {
-          ds0 = ds1 = __fdiv_rn(sc[(64 * t) >> lg], qin);
+          ds0 = ds1 = div_by_q(sc[(64 * t) >> lg], qin, rqin);
         } else {
-          ds0 = __fdiv_rn(sc[2 * t], qin);
-          ds1 = __fdiv_rn(sc[2 * t + 1], qin);
+          ds0 = div_by_q(sc[2 * t], qin, rqin);
+          ds1 = div_by_q(sc[2 * t + 1], qin, rqin);
         }
       }
       k4_item<BIN, CPT, EPC, decltype(first)::value>(codes, ds0, ds1, f, z, acc);
@@ -241,8 +250,13 @@ __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const ui
       if (lg >= 6) {
         a0 = max_nan(max_nan(am[0], am[1]), max_nan(am[2], am[3]));
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1)
-          if (off < tpg) a0 = max_nan(a0, __shfl_xor_sync(0xffffffffu, a0, off));
+        if (tpg == 2) {  // G = 128 (the common case): one exchange
+          a0 = max_nan(a0, __shfl_xor_sync(0xffffffffu, a0, 1));
+        } else {
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1)
+            if (off < tpg) a0 = max_nan(a0, __shfl_xor_sync(0xffffffffu, a0, off));
+        }
         a1 = a0;
         p0 = qparam(a0, qout);
         p1 = p0;
@@ -324,12 +338,14 @@ cudaError_t k4_launch_t(const uint8_t* recv, size_t in_unit_bytes, int N, int M,
   constexpr int SMEM = K4Cfg<BIN, BOUT>::SMEM;
   cudaError_t e = set_smem(k4_tlq_dq_reduce_q<BIN, BOUT, STOCH>, SMEM);
   if (e != cudaSuccess) return e;
+  uint32_t* sched = sched_counter();
+  if (!sched) return cudaErrorMemoryAllocation;
   const uint32_t tpu = (uint32_t)((S + kK4Tile - 1) / kK4Tile);
   const uint32_t ntiles = tpu * (uint32_t)M;
   const int grid = grid_for(ntiles, sms * kK4Ctas);
   k4_tlq_dq_reduce_q<BIN, BOUT, STOCH><<<grid, kK4Block, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G),
                                                                 dst, tpu, ntiles, -0.0f, sr, l_self, sr_stride, sr_off,
-                                                                pull, 16u);
+                                                                pull, 16u, sched);
   return cudaGetLastError();
 }
 template <int BIN, int BOUT>

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
         if constexpr (APPLY) {  // K2's update from the codes just packed: x = mulz(code, rn(s/q)), w += x
           // r[i] holds code + 1.5*2^23 exactly (|code| <= q when p.ok), so code = r - 1.5*2^23:
           // the value K2 decodes from the packed word; !p.ok packs zero codes
-          const float ds = __fdiv_rn(stored_scale(a, 1.f), q);
+          const float ds = div_by_q(stored_scale(a, 1.f), q, __fdiv_rn(1.f, q));
           float f[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) f[i] = mulz(p.ok ? __fsub_rn(__uint_as_float(r[i]), kMagic) : 0.f, ds, z);
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply_ring(const Dests uni
 #pragma unroll
           for (int i = 0; i < 8; ++i) f[i] = float((int)(((w >> (2 * i)) & 3u) ^ 2u) - 2);
         }
-        const float ds = __fdiv_rn(reinterpret_cast<const float*>(st + C::CODE_BYTES)[el >> lg], q);
+        const float ds = div_by_q(reinterpret_cast<const float*>(st + C::CODE_BYTES)[el >> lg], q, __fdiv_rn(1.f, q));
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] = ADD ? mulz(f[i], ds, z) : __fmul_rn(f[i], ds);  // added next: barrier
       }
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kVecThreads) k6_ring_hop(const TG* __restrict_
           x[0] = r0.x; x[1] = r0.y; x[2] = r0.z; x[3] = r0.w;
           x[4] = r1.x; x[5] = r1.y; x[6] = r1.z; x[7] = r1.w;
         } else {
-          const float ds = __fdiv_rn(reinterpret_cast<const float*>(recv + sc_off)[e0 >> lg], q);
+          const float ds = div_by_q(reinterpret_cast<const float*>(recv + sc_off)[e0 >> lg], q, __fdiv_rn(1.f, q));
           float f[8];
           if constexpr (BITS == 4) {
             dec4x8(*reinterpret_cast<const uint32_t*>(recv + e0 / 2), f);
