@@ -96,7 +96,10 @@ struct K4Pull {  // IntraPull, K4 side: tiles of source l with ts % den < num co
   uint32_t mask, num, den;
 };
 
-template <int BIN, int BOUT, bool STOCH>
+// REMOTE: some destination unit is peer memory (P2P inter all-to-all); G64: G >= 64 (a group
+// is whole threads).  Both are compile-time so the common local / G >= 64 path carries none
+// of the other paths' branches and selects (K4 is issue- and ALU-bound: ~1.56 B per element).
+template <int BIN, int BOUT, bool STOCH, bool REMOTE, bool G64>
 __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
                                                           int N, int M, size_t S, int lg, const Dests dst,
                                                           uint32_t tpu, uint32_t ntiles, float z, const SR sr,
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const ui
 
   // slot c of this thread holds chunk c ^ f (f = 0 for the fp32 identity path)
   const int f = BIN == 32 ? 0 : (CPT >= 8 ? (t & 7) : ((t / (8 / CPT)) & (CPT - 1)));
-  const int tpg = lg >= 6 ? (1 << (lg - 6)) : 1;  // threads per group
+  const int tpg = G64 ? (1 << (lg - 6)) : 1;  // threads per group
   uint32_t k = 0;
   for (uint32_t i = 0;; ++i) {
     {  // the tile of the next item (kNoTile: no more work)
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const ui
       float ds0 = 1.f, ds1 = 1.f;
       if constexpr (BIN != 32) {
         const float* sc = reinterpret_cast<const float*>(smem + s * C::STAGE + C::CODE_BYTES);
-        if (lg >= 6) {
+        if constexpr (G64) {
           ds0 = ds1 = div_by_q(sc[(64 * t) >> lg], qin, rqin);
         } else {
           ds0 = div_by_q(sc[2 * t], qin, rqin);
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const ui
     // in slot order, written at their element positions (undoing the slot permutation)
     // local destination: write global memory directly (L2 merges the partial sectors);
     // peer destination: stage the tile in smem and bulk-store it (contiguous NVLink writes)
-    const bool remote = (dst.remote >> mp) & 1ull;  // CTA-uniform
+    const bool remote = REMOTE && ((dst.remote >> mp) & 1ull);  // CTA-uniform
     uint8_t* gout = dst.p[mp];
     // output codes / scales: the staged smem tile (remote) or the unit in global memory (local);
     // two explicit address spaces, so stores are STS / STG rather than generic
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const ui
       }
       QP p0, p1;
       float a0, a1;
-      if (lg >= 6) {
+      if constexpr (G64) {
         a0 = max_nan(max_nan(am[0], am[1]), max_nan(am[2], am[3]));
 #pragma unroll
         if (tpg == 2) {  // G = 128 (the common case): one exchange
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const ui
             else *reinterpret_cast<uint4*>(ot_g + e) = w;
           }
         }
-        if (lg >= 6) {
+        if constexpr (G64) {
           if ((t & (tpg - 1)) == 0) {
             if (remote) osc_s[(64 * t) >> lg] = stored_scale(a0, 1.f);
             else osc_g[(64 * t) >> lg] = stored_scale(a0, 1.f);
@@ -331,22 +334,35 @@ __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const ui
 }
 
 
-template <int BIN, int BOUT, bool STOCH>
-cudaError_t k4_launch_t(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
+template <int BIN, int BOUT, bool STOCH, bool REMOTE, bool G64>
+cudaError_t k4_launch_v(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
                         const SR& sr, int l_self, size_t sr_stride, size_t sr_off, int sms, cudaStream_t st,
                         const K4Pull& pull) {
   constexpr int SMEM = K4Cfg<BIN, BOUT>::SMEM;
-  cudaError_t e = set_smem(k4_tlq_dq_reduce_q<BIN, BOUT, STOCH>, SMEM);
+  cudaError_t e = set_smem(k4_tlq_dq_reduce_q<BIN, BOUT, STOCH, REMOTE, G64>, SMEM);
   if (e != cudaSuccess) return e;
   uint32_t* sched = sched_counter();
   if (!sched) return cudaErrorMemoryAllocation;
   const uint32_t tpu = (uint32_t)((S + kK4Tile - 1) / kK4Tile);
   const uint32_t ntiles = tpu * (uint32_t)M;
   const int grid = grid_for(ntiles, sms * kK4Ctas);
-  k4_tlq_dq_reduce_q<BIN, BOUT, STOCH><<<grid, kK4Block, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G),
+  k4_tlq_dq_reduce_q<BIN, BOUT, STOCH, REMOTE, G64><<<grid, kK4Block, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G),
                                                                 dst, tpu, ntiles, -0.0f, sr, l_self, sr_stride, sr_off,
                                                                 pull, 16u, sched);
   return cudaGetLastError();
+}
+template <int BIN, int BOUT, bool STOCH>
+cudaError_t k4_launch_t(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
+                        const SR& sr, int l_self, size_t sr_stride, size_t sr_off, int sms, cudaStream_t st,
+                        const K4Pull& pull) {
+#define K4V(RM, GB) return k4_launch_v<BIN, BOUT, STOCH, RM, GB>(recv, in_unit_bytes, N, M, S, G, dst, sr, l_self, \
+                                                               sr_stride, sr_off, sms, st, pull)
+  if (dst.remote) {
+    if (G >= 64) K4V(true, true); else K4V(true, false);
+  } else {
+    if (G >= 64) K4V(false, true); else K4V(false, false);
+  }
+#undef K4V
 }
 template <int BIN, int BOUT>
 cudaError_t k4_launch(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
