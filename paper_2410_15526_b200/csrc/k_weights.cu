@@ -38,7 +38,7 @@ template <typename TM, int BITS, bool DIFF, bool APPLY>
 __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __restrict__ w_main,
                                                                    TM* __restrict__ w_model, size_t S,
                                                                    int lg, const Dests dst, const SR sr,
-                                                                   uint64_t idx0, float z) {
+                                                                   uint64_t idx0, float z, uint32_t tpb) {
   static_assert(!APPLY || DIFF, "the owner's apply is the qWD update");
   constexpr int TILE = kVecThreads * 8;
   __shared__ float red[kVecThreads / 32];
@@ -50,9 +50,15 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
   // the next tile's inputs are loaded before this tile's arithmetic (one tile of prefetch)
   float4 na0, na1;
   uint4 nu0, nu1;
+  // tpb > 0: block b streams its own tpb consecutive tiles (a non-persistent grid: the
+  // hardware hands blocks to SMs as they free up -- a static persistent split measured 10-20%
+  // slower on B200 streams); tpb == 0: persistent grid-stride
+  const size_t t_end = tpb ? min(ntiles, ((size_t)blockIdx.x + 1) * tpb) : ntiles;
+  const size_t t_begin = tpb ? (size_t)blockIdx.x * tpb : blockIdx.x;
+  const size_t t_step = tpb ? 1 : gridDim.x;
   auto load = [&](size_t tile) {
     const size_t e = tile * TILE + t * 8;
-    if (tile < ntiles && e < S) {
+    if (tile < t_end && e < S) {
       na0 = *reinterpret_cast<const float4*>(w_main + e);
       na1 = *reinterpret_cast<const float4*>(w_main + e + 4);
       if constexpr (DIFF) {
@@ -61,13 +67,13 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
       }
     }
   };
-  load(blockIdx.x);
-  for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  load(t_begin);
+  for (size_t tile = t_begin; tile < t_end; tile += t_step) {
     const size_t e0 = tile * TILE + t * 8;
     const bool act = e0 < S;
     const float4 a0 = na0, a1 = na1;
     const uint4 u0 = nu0, u1 = nu1;
-    load(tile + gridDim.x);
+    load(tile + t_step);
     float d[8], m[8];
     if (act) {
       if constexpr (!DIFF) {
@@ -167,29 +173,32 @@ __global__ void __launch_bounds__(kVecThreads) k1_qwd_quantize(const float* __re
 // locally (0.94 vs 0.98 ms at P = 1) and over NVLink (0.95 vs 1.11 ms at P = 4).
 constexpr int kK2rTile = 8192;
 constexpr int kK2rStages = 6;
+constexpr int kK2Chunk = 4;  // tiles per scheduler claim
+constexpr uint32_t kNoTileW = 0xffffffffu;
 template <int BITS>
 struct K2rCfg {
   static constexpr int CODE_BYTES = kK2rTile * (BITS == 32 ? 32 : BITS) / 8;
   static constexpr int SC_BYTES = BITS == 32 ? 0 : kK2rTile / 32 * 4;  // G >= 32
   static constexpr int STAGE = CODE_BYTES + SC_BYTES;
-  static constexpr int SMEM = kK2rStages * STAGE + kK2rStages * 8 + 128;
+  static constexpr int SMEM = kK2rStages * STAGE + kK2rStages * 12 + 128;
 };
 
 template <typename TM, int BITS, bool ADD>
 __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply_ring(const Dests units, size_t S, size_t stride, int P,
                                                                     int rot, int U, int lg, TM* __restrict__ w_model,
-                                                                    float z) {
+                                                                    float z, uint32_t* sched) {
   using C = K2rCfg<BITS>;
   constexpr int ROUNDS = kK2rTile / (kVecThreads * 8);
   constexpr float q = float((1 << (BITS == 32 ? 1 : BITS - 1)) - 1);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem<128>(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kK2rStages * C::STAGE);
+  uint32_t* tile_of = reinterpret_cast<uint32_t*>(bar + kK2rStages);  // tile carried by each stage
   const int t = threadIdx.x;
   // U units (U = P, or P - 1 when the owner applied its own in K1), unit fastest, starting at rot
   const size_t tpu = (S + kK2rTile - 1) / kK2rTile, ntiles = tpu * U;
   const size_t sc_off = S * (BITS == 32 ? 4 : BITS) / 8;
-  auto tile_of = [&](size_t tile, size_t& ts, size_t& j) {
+  auto tile_of_fn = [&](size_t tile, size_t& ts, size_t& j) {
     ts = tile / U;
     j = tile - ts * U + rot;
     if (j >= (size_t)P) j -= P;
@@ -199,17 +208,33 @@ __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply_ring(const Dests uni
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue = [&](uint32_t k) {  // thread 0: tile k of this CTA into stage k % STAGES
-    const size_t tile = blockIdx.x + (size_t)k * gridDim.x;
-    if (tile >= ntiles) return;
+  // thread 0 claims tiles from the dynamic scheduler, kK2Chunk at a time (sched_counter)
+  uint32_t c_next = 0, c_end = 0;
+  bool done = false;
+  auto issue = [&](uint32_t k) {  // thread 0: the next claimed tile into stage k % STAGES
+    const int s = k % kK2rStages;
+    if (c_next == c_end && !done) {
+      c_next = sched_claim(sched, kK2Chunk);
+      c_end = (uint32_t)min((size_t)c_next + kK2Chunk, ntiles);
+      if (c_next >= ntiles) {
+        done = true;
+        sched_done(sched);
+      }
+    }
+    if (done) {  // no more work: complete the stage's phase with no data
+      tile_of[s] = kNoTileW;
+      mbar_arrive(&bar[s]);
+      return;
+    }
+    const size_t tile = c_next++;
+    tile_of[s] = (uint32_t)tile;
     size_t ts, j;
-    tile_of(tile, ts, j);
+    tile_of_fn(tile, ts, j);
     const size_t e0 = ts * kK2rTile;
     const uint32_t n = (uint32_t)min((size_t)kK2rTile, S - e0);
     const uint32_t cb = n * (BITS == 32 ? 32 : BITS) / 8;
     uint32_t sb = 0;
     if constexpr (BITS != 32) sb = ((((n >> lg) * 4) + 15) & ~15u);
-    const int s = k % kK2rStages;
     mbar_arrive_tx(&bar[s], cb + sb);
     const uint8_t* unit = units.p[j];
     bulk_load(smem + s * C::STAGE, unit + e0 * (BITS == 32 ? 32 : BITS) / 8, cb, &bar[s]);
@@ -218,11 +243,12 @@ __global__ void __launch_bounds__(kVecThreads) k2_qwd_apply_ring(const Dests uni
   };
   if (t == 0)
     for (int k = 0; k < kK2rStages; ++k) issue(k);
+  __syncthreads();  // tile_of[] of the first stages is visible (later ones: after the per-tile barrier)
   for (uint32_t k = 0;; ++k) {
-    const size_t tile = blockIdx.x + (size_t)k * gridDim.x;
-    if (tile >= ntiles) break;
+    const uint32_t tid = tile_of[k % kK2rStages];  // written by thread 0 before an earlier barrier
+    if (tid == kNoTileW) break;
     size_t ts, j;
-    tile_of(tile, ts, j);
+    tile_of_fn(tid, ts, j);
     TM* wm = w_model + j * stride;
     const size_t e0 = ts * kK2rTile;
     // replica loads first (local HBM), then wait for the pulled codes
@@ -401,12 +427,17 @@ cudaError_t launch_qwd_quantize(const float* w_main, const void* w_model_shard, 
   if (apply_own && !w_model_shard) return cudaErrorInvalidValue;
   void* wm = const_cast<void*>(w_model_shard);  // written only by the APPLY variants
   const size_t ntiles = (S + kVecThreads * 8 - 1) / (kVecThreads * 8);
+  static const uint32_t tpb = [] {  // tiles per block (measurement override: SDP4_K1_TPB, 0 = persistent)
+    const char* e = getenv("SDP4_K1_TPB");
+    return e ? (uint32_t)atoi(e) : 8u;
+  }();
   // persistent grid: as many CTAs per SM as the variant's registers allow (at most kVecCtas)
 #define K1(TM, B, DF, AP)                                                                                    \
   do {                                                                                                       \
     static const int nb = std::min(kVecCtas, occ_blocks(k1_qwd_quantize<TM, B, DF, AP>, kVecThreads));      \
-    k1_qwd_quantize<TM, B, DF, AP><<<grid_for(ntiles, sms * nb), kVecThreads, 0, st>>>(                      \
-        w_main, static_cast<TM*>(wm), S, __builtin_ctz(G), dst, sr, idx0, -0.0f);                            \
+    const int grid = tpb ? (int)((ntiles + tpb - 1) / tpb) : grid_for(ntiles, sms * nb);                     \
+    k1_qwd_quantize<TM, B, DF, AP><<<grid, kVecThreads, 0, st>>>(                                            \
+        w_main, static_cast<TM*>(wm), S, __builtin_ctz(G), dst, sr, idx0, -0.0f, tpb);                       \
   } while (0)
 #define K1B(TM, DF, AP)                 \
   if (bits == 2) K1(TM, 2, DF, AP);     \
@@ -431,11 +462,13 @@ cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride,
   if (skip_rot) rot = (rot + 1) % P;
   if (U <= 0 || S == 0) return cudaSuccess;
   const int grid_r = grid_for((S + kK2rTile - 1) / kK2rTile * U, sms * 4);
+  uint32_t* sched = sched_counter();
+  if (!sched) return cudaErrorMemoryAllocation;
 #define K2(TM, B, AD)                                                                          \
   do {                                                                                                 \
     set_smem(k2_qwd_apply_ring<TM, B, AD>, K2rCfg<B>::SMEM);                                           \
     k2_qwd_apply_ring<TM, B, AD><<<grid_r, kVecThreads, K2rCfg<B>::SMEM, st>>>(                         \
-        units, S, stride, P, rot % P, U, __builtin_ctz(G), static_cast<TM*>(w_model), -0.0f);          \
+        units, S, stride, P, rot % P, U, __builtin_ctz(G), static_cast<TM*>(w_model), -0.0f, sched);   \
   } while (0)
 #define K2B(TM, AD) \
   if (bits == 2) K2(TM, 2, AD); else if (bits == 4) K2(TM, 4, AD); else if (bits == 8) K2(TM, 8, AD); else K2(TM, 32, AD)
