@@ -60,6 +60,9 @@ def parse_args():
     p.add_argument("--intra-pull", type=str, default=None,
                    help="P2P: num/den of the intra all-to-all pulled by K4 (default: the library's auto split)")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle timing")
+    p.add_argument("--steps-only", action="store_true",
+                   help="only the warm-up and the K timed steps (for an ncu launch list of exactly those)")
+    p.add_argument("--no-variants", action="store_true", help="skip the fp32-gradient step variant")
     return p.parse_args()
 
 
@@ -174,38 +177,65 @@ def ncu_traffic(kernel, workload):
 
 
 # ------------------------------------------------------------------- oracle (CPU) legs
-def oracle_sample_rate(a, seconds: float, D_full: int):
+def _oracle_window(args):
+    """Worker: one oracle step (qWD + TLq-HS at P=1) on a window of the workload, repeated for
+    `seconds`; returns (elements processed, seconds).  Imports only numpy and the oracle."""
+    w_main, wm, grad, cfg, seconds = args
+    import oracle
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.qwd_step([w_main], wm, cfg["bits_w"], cfg["qwd_group"], model_bf16=cfg["model_bf16"])
+        oracle.tlq_hs_reduce_scatter([grad], oracle.Topology(1, 1), cfg["group"], cfg["hadamard"], cfg["bits_intra"],
+                                     cfg["bits_inter"], True)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return reps * grad.size, el
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sample_rate(a, seconds: float, D_full: int, cores: int = 1):
     """Time the oracle (as it stands) on a bounded sample of the workload: the full step
-    (qWD at P=1 + TLq-HS at P=1) on a contiguous window of `n` elements, repeated until
-    `seconds` elapse.  Returns (GB/s of pre-quant bytes, description, cores)."""
-    import numpy as np
+    (qWD at P=1 + TLq-HS at P=1) on `cores` independent 2M-element windows of the workload,
+    one per worker process (numpy is single-threaded per process), each repeated for
+    `seconds`.  Returns (GB/s of pre-quant bytes summed over the workers, description, cores)."""
     import torch
 
-    import oracle
     import synth
     n = min(D_full, 1 << 21)
     n -= n % max(a.group, a.qwd_group, 64)
+    g = 2 if a.grad_dtype == "bf16" else 4
     gdt = torch.bfloat16 if a.grad_dtype == "bf16" else torch.float32
     mdt = torch.bfloat16 if a.model_dtype == "bf16" else torch.float32
     w_model = synth.model_weights(n, seed=synth.seed_for(0, 1), dtype=mdt)
     w_main = synth.main_weights(w_model, seed=synth.seed_for(0, 2), lr=synth.GPT_LR.get(a.model, 2e-4)).numpy()
     grad = synth.gradient(n, seed=synth.seed_for(0, 3), dtype=gdt).float().numpy()
     wm = synth.bf16_bits(w_model) if mdt == torch.bfloat16 else w_model.numpy()
-    g = 2 if a.grad_dtype == "bf16" else 4
-    reps, t0 = 0, time.perf_counter()
-    while True:
-        oracle.qwd_step([w_main], wm, a.bits_w, a.qwd_group, model_bf16=(mdt == torch.bfloat16))
-        oracle.tlq_hs_reduce_scatter([grad], oracle.Topology(1, 1), a.group, a.hadamard, a.bits_intra,
-                                     a.bits_inter, True)
-        reps += 1
-        el = time.perf_counter() - t0
-        if el >= seconds:
-            break
-    rate = reps * n * (4 + g) / el / 1e9
-    desc = (f"{reps} oracle steps (qWD + TLq-HS, P=1) on a {n}-element window of the workload, "
-            f"{el:.1f} s, single-threaded numpy fp32")
-    del np
-    return rate, desc, 1
+    cfg = {"bits_w": a.bits_w, "qwd_group": a.qwd_group, "model_bf16": mdt == torch.bfloat16, "group": a.group,
+           "hadamard": a.hadamard, "bits_intra": a.bits_intra, "bits_inter": a.bits_inter}
+    jobs = [(w_main, wm, grad, cfg, seconds)] * cores
+    if cores == 1:
+        res = [_oracle_window(jobs[0])]
+    else:
+        import multiprocessing as mp
+        with mp.get_context("spawn").Pool(cores) as pool:
+            res = pool.map(_oracle_window, jobs)
+    elems = sum(r[0] for r in res)
+    el = max(r[1] for r in res)
+    rate = elems * (4 + g) / el / 1e9
+    desc = (f"{elems // n} oracle steps (qWD + TLq-HS, P=1) on {cores} x {n}-element windows of the workload "
+            f"({cores} worker process{'es' if cores > 1 else ''}, single-threaded numpy fp32 each), {el:.1f} s")
+    return rate, desc, cores
 
 
 def run_reference(a, rank, world):
@@ -215,19 +245,21 @@ def run_reference(a, rank, world):
     import synth
     D = a.numel or synth.gpt_numel(a.model)
     per = max(1.0, a.cpu_seconds / max(1, a.steps))
+    cores = min(os.cpu_count() or 1, 64)
     rates = []
     for _ in range(a.warmup):
         oracle_sample_rate(a, 0.1, D)
     desc = ""
     for _ in range(a.steps):
-        r, desc, cores = oracle_sample_rate(a, per, D)
+        r, desc, cores = oracle_sample_rate(a, per, D, cores)
         rates.append(r)
     v = statistics.median(rates)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"GPT-{a.model}-shaped flat buffer (bounded CPU sample)", "D": D},
-            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "cpu_model": cpu_model(),
+                             "kind": "oracle", "sample": desc},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     emit(line)
@@ -313,6 +345,17 @@ def run_sdp4(a, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         ms = timed(step, a.steps)
     launches = comm.launch_count(reset=True)
+    pre_bytes_rank = D * (4 + g_bytes)
+    value = P * pre_bytes_rank / (ms * 1e-3) / 1e9
+    if a.steps_only:   # the launch list of exactly the warm-up + timed steps (ncu), nothing else
+        if rank == 0:
+            emit({"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": a.steps,
+                  "warmup": max(3, a.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True,
+                  "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                  "config": {"workload": f"GPT-{a.model} D={D} P={P} ({M}x{N})", "steps_only": True},
+                  "gpu_launches": int(launches), "clocks": clk.summary()})
+        comm.close()
+        return
     # per-kernel device times: the same K steps again with every launch bracketed by events
     comm.profile_enable(True)
     comm.profile_read()
@@ -322,9 +365,6 @@ def run_sdp4(a, rank, world, local_rank):
     if os.environ.get("SDP4_BENCH_RANKS"):   # diagnostics: every rank's per-kernel / wait times
         print(f"rank {rank}: " + ", ".join(f"{n} {t / a.steps:.3f}" for n, (t, c) in sorted(prof.items())),
               file=sys.stderr, flush=True)
-
-    pre_bytes_rank = D * (4 + g_bytes)
-    value = P * pre_bytes_rank / (ms * 1e-3) / 1e9
 
     # roofline for the dominant kernel (largest summed device time in the timed region)
     workload = f"GPT-{a.model} D={D} P={P} ({M}x{N}) G={a.group} Gw={a.qwd_group} b={a.hadamard} " \
@@ -386,6 +426,36 @@ def run_sdp4(a, rank, world, local_rank):
                              "nvlink_GBps": round(nv / (t * 1e-3) / 1e9, 1) if nv else None,
                              "nvlink_frac_of_900": round(nv / (t * 1e-3) / 900e9, 4) if nv else None}
 
+    # the paper's FP32-gradient setting: the same step with fp32 gradients
+    variants, t_tlq32 = None, None
+    if not a.no_variants and gdt == torch.bfloat16:
+        g32 = grad.float()
+
+        def step32():
+            qwd(w_main)
+            comm.tlq_hs_reduce_scatter(g32, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
+        for _ in range(2):
+            step32()
+        ms32 = timed(step32, a.steps)
+        comm.profile_enable(True)
+        comm.profile_read()
+        timed(step32, a.steps)
+        prof32 = comm.profile_read()
+        comm.profile_enable(False)
+        t_tlq32 = timed(lambda: comm.tlq_hs_reduce_scatter(g32, out, ws_t, a.bits_intra, a.bits_inter, a.group,
+                                                           a.hadamard, True), a.steps)
+        a32 = argparse.Namespace(**dict(vars(a), grad_dtype="fp32"))
+        k3 = {n: v for n, v in prof32.items() if n.startswith("K3")}
+        k3_ms = sum(v[0] for v in k3.values()) / max(1, sum(v[1] for v in k3.values()))
+        k3_bytes = kernel_bytes("K3", D, S, P, M, N, a32)
+        variants = {"fp32_grad": {"ms_per_step": round(ms32, 4),
+                                  "value": round(P * D * (4 + 4) / (ms32 * 1e-3) / 1e9, 2), "unit": "GB/s",
+                                  "tlq_hs_reduce_scatter_ms": round(t_tlq32, 4),
+                                  "K3_avg_ms": round(k3_ms, 4),
+                                  "K3_gbs": round(k3_bytes / (k3_ms * 1e-3) / 1e9, 1) if k3_ms else None,
+                                  "K3_frac_of_peak": round(k3_bytes / (k3_ms * 1e-3) / 1e9 / peak, 4) if k3_ms else None}}
+        del g32
+
     # ablation (NEXT-3): TLq-HS with the Hadamard transforms as separate passes ("SDP4Bit (HS
     # w/o fused)") -- K3 identity codec forward pass, the b = 0 reduce-scatter, K5
     # identity codec inverse pass -- against the fused path
@@ -412,43 +482,52 @@ def run_sdp4(a, rank, world, local_rank):
                         qwd_own_fusion_speedup=round(t_two / t_qwd, 3))
         del hbuf, red, out2
 
-    # unquantized NCCL comparators on the same buffers (sec. 2.1), N > 1 only
+    # unquantized NCCL comparators (sec. 2.1), N > 1 only, torch.distributed's own NCCL
+    # communicator (default configuration).  Like for like: qWD against the bf16 all-gather of
+    # the model weights it replaces, TLq-HS against a reduce-scatter of the SAME gradient dtype
+    # (bf16 and, for the paper's FP32-gradient setting P:502, fp32); plus the "same buffers"
+    # pair SURVEY sec. 8(d) names (fp32 weight-difference all-gather + gradient reduce-scatter).
     comparators = None
     if world > 1 and not a.no_comparators:
-        # torch.distributed's own NCCL communicator (default configuration, not the
-        # CTA-capped one libsdp4 pipelines with)
+        reps = max(3, a.steps // 2)
         big = torch.empty(D, dtype=torch.float32, device=dev)
         d_shard = torch.empty(S, dtype=torch.float32, device=dev)
-        rs_out = torch.empty(S, dtype=gdt, device=dev)
-        t_ag = timed(lambda: dist.all_gather_into_tensor(big, d_shard), max(3, a.steps // 2), 2)
-        t_rs = timed(lambda: dist.reduce_scatter_tensor(rs_out, grad, op=dist.ReduceOp.AVG), max(3, a.steps // 2), 2)
-        # Megatron-realistic pair: bf16 model-weight all-gather and
-        # fp32 gradient reduce-scatter
+        t_ag32 = timed(lambda: dist.all_gather_into_tensor(big, d_shard), reps, 2)
         w_shard16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
         big16 = big.view(torch.bfloat16)[:D]
-        t_ag16 = timed(lambda: dist.all_gather_into_tensor(big16, w_shard16), max(3, a.steps // 2), 2)
-        del big16
+        t_ag16 = timed(lambda: dist.all_gather_into_tensor(big16, w_shard16), reps, 2)
+        del big16, w_shard16, big, d_shard
+        g16 = grad if gdt == torch.bfloat16 else grad.bfloat16()
+        rs16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
+        t_rs16 = timed(lambda: dist.reduce_scatter_tensor(rs16, g16, op=dist.ReduceOp.AVG), reps, 2)
+        del g16, rs16
         g32 = grad.float() if gdt != torch.float32 else grad
         rs32 = torch.empty(S, dtype=torch.float32, device=dev)
-        t_rs32 = timed(lambda: dist.reduce_scatter_tensor(rs32, g32, op=dist.ReduceOp.AVG), max(3, a.steps // 2), 2)
-        del g32, rs32, w_shard16
-        del big
+        t_rs32 = timed(lambda: dist.reduce_scatter_tensor(rs32, g32, op=dist.ReduceOp.AVG), reps, 2)
+        del g32, rs32
+        t_rs_grad = t_rs16 if gdt == torch.bfloat16 else t_rs32
         # ablation baselines through libsdp4 (NEXT-3): 4-bit ring reduce-scatter with per-hop
-        # quantization and the qW direct-weight all-gather (Alg. 1)
+        # quantization
         ws_r = None if comm.transport == "p2p" else torch.empty(comm.ring_workspace_bytes(D, a.bits_inter, a.group),
                                                                  dtype=torch.uint8, device=dev)
-        t_ring = timed(lambda: comm.ring_reduce_scatter(grad, out, ws_r, a.bits_inter, a.group, True),
-                       max(3, a.steps // 2), 2)
+        t_ring = timed(lambda: comm.ring_reduce_scatter(grad, out, ws_r, a.bits_inter, a.group, True), reps, 2)
         del ws_r
-        comparators = {"nccl_all_gather_fp32_ms": round(t_ag, 3), "nccl_reduce_scatter_grad_ms": round(t_rs, 3),
-                       "unquantized_ms_per_step": round(t_ag + t_rs, 3),
-                       "unquantized_GBps": round(P * pre_bytes_rank / ((t_ag + t_rs) * 1e-3) / 1e9, 2),
-                       "speedup_vs_unquantized": round((t_ag + t_rs) / ms, 3),
-                       "speedup_all_gather": round(t_ag / t_qwd, 3), "speedup_reduce_scatter": round(t_rs / t_tlq, 3),
-                       f"ring_q{a.bits_inter}_reduce_scatter_ms": round(t_ring, 3),
-                       "megatron_pair": {"nccl_all_gather_bf16_ms": round(t_ag16, 3),
-                                         "nccl_reduce_scatter_fp32_ms": round(t_rs32, 3),
-                                         "speedup_vs_pair": round((t_ag16 + t_rs32) / ms, 3)}}
+        ms32 = variants["fp32_grad"]["ms_per_step"] if variants else None
+        comparators = {
+            "nccl_ms": {"all_gather_bf16_weights": round(t_ag16, 3), "all_gather_fp32_weight_diff": round(t_ag32, 3),
+                        "reduce_scatter_bf16": round(t_rs16, 3), "reduce_scatter_fp32": round(t_rs32, 3)},
+            "like_for_like": {
+                "qwd_vs_all_gather_bf16_weights": round(t_ag16 / t_qwd, 3),
+                f"tlq_hs_vs_reduce_scatter_{a.grad_dtype}": round(t_rs_grad / t_tlq, 3),
+                "tlq_hs_vs_reduce_scatter_fp32": round(t_rs32 / t_tlq32, 3) if t_tlq32 else None,
+                f"step_vs_pair_bf16_weights_{a.grad_dtype}_grads": round((t_ag16 + t_rs_grad) / ms, 3),
+                "step_vs_pair_bf16_weights_fp32_grads (Megatron, P:502)":
+                    round((t_ag16 + t_rs32) / ms32, 3) if ms32 else None},
+            "same_buffers (SURVEY 8(d): fp32 weight-difference all-gather + gradient reduce-scatter)": {
+                "unquantized_ms_per_step": round(t_ag32 + t_rs_grad, 3),
+                "unquantized_GBps": round(P * pre_bytes_rank / ((t_ag32 + t_rs_grad) * 1e-3) / 1e9, 2),
+                "speedup": round((t_ag32 + t_rs_grad) / ms, 3)},
+            f"ring_q{a.bits_inter}_reduce_scatter_ms": round(t_ring, 3)}
 
     # end to end through the public API with host buffers (pinned), copies inside the region.
     # Pipelined like a data loader: step i+1's inputs are copied host->device on one stream
@@ -511,8 +590,13 @@ def run_sdp4(a, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:   # host-only and single-rank: a failure here must not cost the GPU line
-            v, desc, cores = oracle_sample_rate(a, a.cpu_seconds, D)
-            cpu = {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc}
+            # all host cores (one worker process per core, the oracle as it stands) and one core
+            ncores = min(os.cpu_count() or 1, 64)
+            v, desc, cores = oracle_sample_rate(a, a.cpu_seconds / 2, D, ncores)
+            v1, desc1, _ = oracle_sample_rate(a, a.cpu_seconds / 2, D, 1)
+            cpu = {"value": round(v, 4), "unit": "GB/s", "cores": cores, "cpu_model": cpu_model(),
+                   "nproc": os.cpu_count(), "kind": "oracle", "sample": desc,
+                   "single_thread": {"value": round(v1, 4), "cores": 1, "sample": desc1}}
         except Exception as ex:  # noqa: BLE001
             cpu = {"error": f"{type(ex).__name__}: {ex}"[:300], "kind": "oracle"}
 
@@ -534,6 +618,7 @@ def run_sdp4(a, rank, world, local_rank):
                 "clocks": clk.summary(), "gpu_launches": int(launches), "kernels": kern, "comm_ops": comm_ops,
                 "ms_per_step_profiled": round(ms_prof, 4), "roofline": roofline,
                 "collectives": collectives, "e2e": e2e, "comparators": comparators, "ablation": ablation,
+                "variants": variants,
                 "cpu_baseline": cpu}
         emit(line)
     comm.close()
