@@ -39,7 +39,7 @@ def main():
     out = torch.empty(D, dtype=torch.float32, device=dev)
     for dt in (torch.bfloat16, torch.float32):
         grad = synth.gradient(D, seed=3, dtype=dt).to(dev)
-        for (bi, be, b, seed) in ((8, 4, 64, None), (8, 4, 0, None), (4, 4, 256, None), (8, 4, 64, 11),
+        for (bi, be, b, seed) in ((8, 4, 64, None), (8, 4, 0, None), (4, 4, 128, None), (8, 4, 64, 11),
                                   (32, 32, 64, None)):
             tws = torch.zeros(comm.tlq_workspace_bytes(D, bi, be, G), dtype=torch.uint8, device=dev)
             comm.tlq_hs_reduce_scatter(grad, out, tws, bi, be, G, b, True, seed=seed)
