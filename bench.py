@@ -63,6 +63,8 @@ def parse_args():
     p.add_argument("--steps-only", action="store_true",
                    help="only the warm-up and the K timed steps (for an ncu launch list of exactly those)")
     p.add_argument("--no-variants", action="store_true", help="skip the fp32-gradient step variant")
+    p.add_argument("--overlap", action="store_true",
+                   help="issue the qWD step on a second stream, concurrent with TLq-HS (experiment)")
     return p.parse_args()
 
 
@@ -309,9 +311,22 @@ def run_sdp4(a, rank, world, local_rank):
         else:
             comm.qwd_step(wmain, w_model, ws_q, a.bits_w, a.qwd_group)
 
+    s_q = torch.cuda.Stream() if a.overlap else None
+    ev_fork, ev_join = torch.cuda.Event(), torch.cuda.Event()
+
     def step():
-        qwd(w_main)
+        if s_q is None:
+            qwd(w_main)
+            comm.tlq_hs_reduce_scatter(grad, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
+            return
+        # the two collectives are independent: qWD on a second stream, joined at the end
+        ev_fork.record()
+        with torch.cuda.stream(s_q):
+            s_q.wait_event(ev_fork)
+            qwd(w_main)
+            ev_join.record()
         comm.tlq_hs_reduce_scatter(grad, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
+        torch.cuda.current_stream().wait_event(ev_join)
 
     def barrier():
         if world > 1:
