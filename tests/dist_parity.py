@@ -59,6 +59,16 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
         sys.exit(0 if ok else 1)
+    if a.virtual and a.full:   # the bench workload at full size on ranks sharing one GPU
+        M = int(a.splits or 2)
+        comm = Comm.from_process_group(M, bootstrap="host")
+        ok, msgs = run_full(comm, rank, world, M, world // M)
+        comm.close()
+        print(f"rank {rank}/{world} ({M}x{world // M}) {'PASS' if ok else 'FAIL'} full-size shared-GPU "
+              f"{'; '.join(msgs)}", flush=True)
+        dist.barrier()
+        dist.destroy_process_group()
+        sys.exit(0 if ok else 1)
     if a.virtual:
         splits = [m for m in range(1, world + 1) if world % m == 0] if a.splits in (None, "all") \
             else [int(x) for x in a.splits.split(",")]
@@ -74,6 +84,12 @@ def main():
             runs = [("p2p", 0, None), ("p2p", 0, 2 ** 34 + 2410), ("p2p", -1, None), ("p2p", -3, 2410),
                     ("p2p", 2, None), ("p2p", 3, 2411)]
             ok_m, msgs = run_matrix(comm, rank, world, M, N, a.G, a.b, runs, graph=a.graph)
+            if world == 8 and M == 2:   # BASELINE.json config 1: 2^20 elements, G 128, b 64, 2 x 4
+                comm.set_chunks(0)
+                comm.set_intra_pull(1, 2)
+                ok_c, m_c = run_checks(comm, rank, world, M, N, 128, 64, (1 << 20) // world, None)
+                ok_m &= ok_c
+                msgs += [f"config 1 (D = 2^20, 2x4): {m}" for m in m_c] + ["config 1 (D = 2^20, 2x4) checked"]
             comm.close()
             ok &= ok_m
             out.append(f"{M}x{N} {'PASS' if ok_m else 'FAIL'} {'; '.join(msgs)}")
@@ -231,12 +247,28 @@ def run_full(comm, rank, P, M, N, G=128, b=64, win=16384, nwin=6):
     D = pad_numel(synth.gpt_numel("1.3B"), P, G)
     S = D // P
     lr = synth.GPT_LR["1.3B"]
-    w_model = synth.model_weights(D, seed=synth.seed_for(0, 1), device=dev)
-    w_model0 = w_model.clone()
-    w_main = synth.main_weights(w_model[rank * S:(rank + 1) * S], seed=synth.seed_for(rank, 2), lr=lr)
-    grad = synth.gradient(D, seed=synth.seed_for(rank, 3), device=dev, dtype=torch.bfloat16)
-    ws_q = torch.empty(comm.qwd_workspace_bytes(D, 4, G), dtype=torch.uint8, device=dev)
-    ws_t = torch.empty(comm.tlq_workspace_bytes(D, 8, 4, G), dtype=torch.uint8, device=dev)
+
+    def one_at_a_time(fn):
+        """Generate full-size inputs rank by rank: ranks sharing one GPU must not hold their
+        generators' fp32 temporaries (~16 GB each) at the same time."""
+        res = None
+        for turn in range(P):
+            if turn == rank:
+                res = fn()
+                torch.cuda.synchronize()
+                torch.cuda.empty_cache()
+            dist.barrier()
+        return res
+
+    def inputs():
+        wm = synth.model_weights(D, seed=synth.seed_for(0, 1), device=dev)
+        wmain = synth.main_weights(wm[rank * S:(rank + 1) * S], seed=synth.seed_for(rank, 2), lr=lr)
+        g = synth.gradient(D, seed=synth.seed_for(rank, 3), device=dev, dtype=torch.bfloat16)
+        return wm, wm.clone(), wmain, g
+    w_model, w_model0, w_main, grad = one_at_a_time(inputs)
+    p2p = comm.transport == "p2p"   # exchanges through libsdp4's own buffers: no workspace
+    ws_q = None if p2p else torch.empty(comm.qwd_workspace_bytes(D, 4, G), dtype=torch.uint8, device=dev)
+    ws_t = None if p2p else torch.empty(comm.tlq_workspace_bytes(D, 8, 4, G), dtype=torch.uint8, device=dev)
     out = torch.empty(S, dtype=torch.float32, device=dev)
     comm.qwd_step(w_main, w_model, ws_q, 4, G)   # the call bench.py times
     comm.tlq_hs_reduce_scatter(grad, out, ws_t, 8, 4, G, b, True)
@@ -247,7 +279,7 @@ def run_full(comm, rank, P, M, N, G=128, b=64, win=16384, nwin=6):
     ok, msgs = True, []
     # qWD: replica windows inside every shard j need rank j's main weights
     for j in range(P):
-        mj = synth.main_weights(w_model0[j * S:(j + 1) * S], seed=synth.seed_for(j, 2), lr=lr)
+        mj = one_at_a_time(lambda: synth.main_weights(w_model0[j * S:(j + 1) * S], seed=synth.seed_for(j, 2), lr=lr))
         for o in offs[:3] + offs[-1:]:
             e = j * S + o
             _, want = oracle.qwd_step([mj[o:o + win].cpu().numpy()], synth.bf16_bits(w_model0[e:e + win]), 4, G,
@@ -259,12 +291,15 @@ def run_full(comm, rank, P, M, N, G=128, b=64, win=16384, nwin=6):
     # TLq-HS: windows of this rank's output shard need every rank's gradient at shard `rank`
     pieces = {o: [] for o in offs}
     for q in range(P):
-        gq = synth.gradient(D, seed=synth.seed_for(q, 3), device=dev, dtype=torch.bfloat16)
-        for o in offs:
+        def windows():
+            gq = synth.gradient(D, seed=synth.seed_for(q, 3), device=dev, dtype=torch.bfloat16)
             # a P-shard mini problem whose shard j holds the window of shard j (all shards are
             # needed only for the layout; the oracle's output shard `rank` uses column `rank`)
-            pieces[o].append(torch.cat([gq[j * S + o:j * S + o + win] for j in range(P)]).float().cpu().numpy())
-        del gq
+            return {o: torch.cat([gq[j * S + o:j * S + o + win] for j in range(P)]).float().cpu().numpy()
+                    for o in offs}
+        got_w = one_at_a_time(windows)
+        for o in offs:
+            pieces[o].append(got_w[o])
     for o in offs:
         tr = oracle.tlq_hs_reduce_scatter(pieces[o], oracle.Topology(M, N), G, b, 8, 4, True)
         got = out[o:o + win].cpu().numpy()

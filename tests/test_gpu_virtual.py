@@ -38,3 +38,11 @@ def test_virtual_all_splits(nproc):
     qWD calls, TLq-HS (bf16 and fp32 gradients), qW and the ring; plus CUDA-graph replays."""
     out = _run(nproc, ["--splits", "all", "--graph"], 29600 + nproc)
     assert "FAIL" not in out, out
+
+
+def test_virtual_fullsize_2x4():
+    """BASELINE config 2 as the paper splits it -- GPT-1.3B-shaped buffer, 8 ranks as 2 x 4
+     -- at FULL size on one GPU, bench.py's calls (qwd_step, TLq-HS 8/4 bits,
+    G = 128, b = 64), sampled windows of every shard bit-exact against the oracle."""
+    out = _run(8, ["--full", "--splits", "2"], 29640, timeout=1800)
+    assert "FAIL" not in out, out
