@@ -21,19 +21,21 @@ namespace {
 // =====================================================================================
 constexpr int kK4Threads = 128;                   // consumer threads (four warps)
 constexpr int kK4Block = kK4Threads + 32;         // + one producer warp
-constexpr int kK4Ctas = 3;
+constexpr int kK4Ctas = 3;        // CTAs per SM with remote output staging
+constexpr int kK4CtasLocal = 4;   // without it (every destination local: P = 1, NCCL transport)
 constexpr int kK4Tile = kK4Threads * 64;
 constexpr int kK4Chunk = 8;  // tiles per scheduler claim
 constexpr uint32_t kNoTile = 0xffffffffu;
 
-template <int BIN, int BOUT>
+template <int BIN, int BOUT, bool REMOTE = true>
 struct K4Cfg {
+  static constexpr int CTAS = REMOTE ? kK4Ctas : kK4CtasLocal;
   static constexpr int CODE_BYTES = kK4Tile * BIN / 8;
   static constexpr int SC_BYTES = BIN == 32 ? 0 : kK4Tile / 32 * 4;
   static constexpr int STAGE = CODE_BYTES + SC_BYTES;
   static constexpr int OUT_TILE = kK4Tile * BOUT / 8 + kK4Tile / 32 * 4;  // staged output: codes + scales
-  static constexpr int OUTB = OUT_TILE <= 8 * 1024 ? 4 : 2;  // staged remote output tiles in flight
-  static constexpr int S0 = (74 * 1024 - OUTB * OUT_TILE) / STAGE;  // ~74 KB per CTA: kK4Ctas per SM
+  static constexpr int OUTB = !REMOTE ? 0 : (OUT_TILE <= 8 * 1024 ? 4 : 2);  // staged remote output tiles in flight
+  static constexpr int S0 = ((REMOTE ? 74 : 55) * 1024 - OUTB * OUT_TILE) / STAGE;  // per-CTA budget: CTAS per SM
   static constexpr int STAGES = S0 > 8 ? 8 : (S0 < 2 ? 2 : S0);
   static constexpr int SMEM = STAGES * STAGE + OUTB * OUT_TILE + 2 * 8 * STAGES + 4 * STAGES + 128;
   static_assert(SMEM <= 227 * 1024, "K4 tile configuration exceeds the per-CTA shared memory");
@@ -100,12 +102,12 @@ struct K4Pull {  // IntraPull, K4 side: tiles of source l with ts % den < num co
 // is whole threads).  Both are compile-time so the common local / G >= 64 path carries none
 // of the other paths' branches and selects (K4 is issue- and ALU-bound: ~1.56 B per element).
 template <int BIN, int BOUT, bool STOCH, bool REMOTE, bool G64>
-__global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
+__global__ void __launch_bounds__(kK4Block, K4Cfg<BIN, BOUT, REMOTE>::CTAS) k4_tlq_dq_reduce_q(const uint8_t* __restrict__ recv, size_t in_unit_bytes,
                                                           int N, int M, size_t S, int lg, const Dests dst,
                                                           uint32_t tpu, uint32_t ntiles, float z, const SR sr,
                                                           int l_self, size_t sr_stride, size_t sr_off,
                                                           const K4Pull pull, uint32_t m16, uint32_t* sched) {
-  using C = K4Cfg<BIN, BOUT>;
+  using C = K4Cfg<BIN, BOUT, REMOTE>;
   constexpr int STAGES = C::STAGES, CPT = C::CPT, EPC = C::EPC;
   constexpr float qin = float((1 << (BIN == 32 ? 1 : BIN - 1)) - 1);
   const float rqin = __fdiv_rn(1.f, qin);  // rn(1/q): div_by_q's reciprocal (constant-folded)
@@ -211,12 +213,13 @@ __global__ void __launch_bounds__(kK4Block, kK4Ctas) k4_tlq_dq_reduce_q(const ui
     uint8_t* gout = dst.p[mp];
     // output codes / scales: the staged smem tile (remote) or the unit in global memory (local);
     // two explicit address spaces, so stores are STS / STG rather than generic
-    uint8_t* ot_s = out_buf + (i % C::OUTB) * C::OUT_TILE;
+    constexpr int OB = C::OUTB > 0 ? C::OUTB : 1;  // (no staging in the local-only variant)
+    uint8_t* ot_s = out_buf + (i % OB) * C::OUT_TILE;
     uint8_t* ot_g = gout + e0 * BOUT / 8;
     float* osc_s = reinterpret_cast<float*>(ot_s + kK4Tile * BOUT / 8);
     float* osc_g = reinterpret_cast<float*>(gout + S * BOUT / 8) + (e0 >> lg);
     if (remote) {
-      if (t == 0) bulk_wait_read<C::OUTB - 1>();  // the stores of tile i - OUTB have left out_buf[i % OUTB]
+      if (t == 0) bulk_wait_read<OB - 1>();  // the stores of tile i - OUTB have left out_buf[i % OUTB]
       named_sync(1, kK4Threads);
     }
     auto vbase = [&](int v) {  // element offset (within the thread's 64) of slot-order vector v
@@ -338,14 +341,14 @@ template <int BIN, int BOUT, bool STOCH, bool REMOTE, bool G64>
 cudaError_t k4_launch_v(const uint8_t* recv, size_t in_unit_bytes, int N, int M, size_t S, int G, const Dests& dst,
                         const SR& sr, int l_self, size_t sr_stride, size_t sr_off, int sms, cudaStream_t st,
                         const K4Pull& pull) {
-  constexpr int SMEM = K4Cfg<BIN, BOUT>::SMEM;
+  constexpr int SMEM = K4Cfg<BIN, BOUT, REMOTE>::SMEM;
   cudaError_t e = set_smem(k4_tlq_dq_reduce_q<BIN, BOUT, STOCH, REMOTE, G64>, SMEM);
   if (e != cudaSuccess) return e;
   uint32_t* sched = sched_counter();
   if (!sched) return cudaErrorMemoryAllocation;
   const uint32_t tpu = (uint32_t)((S + kK4Tile - 1) / kK4Tile);
   const uint32_t ntiles = tpu * (uint32_t)M;
-  const int grid = grid_for(ntiles, sms * kK4Ctas);
+  const int grid = grid_for(ntiles, sms * K4Cfg<BIN, BOUT, REMOTE>::CTAS);
   k4_tlq_dq_reduce_q<BIN, BOUT, STOCH, REMOTE, G64><<<grid, kK4Block, SMEM, st>>>(recv, in_unit_bytes, N, M, S, __builtin_ctz(G),
                                                                 dst, tpu, ntiles, -0.0f, sr, l_self, sr_stride, sr_off,
                                                                 pull, 16u, sched);
