@@ -11,11 +11,12 @@ constexpr uint32_t kK3NoTile = 0xffffffffu;
 
 template <int IN_R, int OUT_R>
 struct K3Cfg {
+  static constexpr int CTAS = IN_R == 128 ? 2 : 1;  // bf16 gradients: two CTAs per SM
   static constexpr int IN_TILE = kTileRows * IN_R;
   // one warp's output: 32 rows of codes + its scales (G >= 32: at most 64), 1024-aligned
   // (TMA swizzle atoms); double-buffered per warp
   static constexpr int OUT_W = (32 * OUT_R + 256 + 1023) / 1024 * 1024;
-  static constexpr int BUDGET = 200 * 1024;
+  static constexpr int BUDGET = CTAS == 2 ? 110 * 1024 : 200 * 1024;
   static constexpr int OB = 2 * kK3Warps * OUT_W + 2 * IN_TILE <= BUDGET ? 2 : 1;  // output tiles per warp
   static constexpr int OUT_BYTES = OB * kK3Warps * OUT_W;
   static constexpr int S0 = (BUDGET - OUT_BYTES) / IN_TILE;
@@ -62,7 +63,7 @@ __device__ __forceinline__ void store_warp_linear(const uint8_t* s_codes, uint32
 }
 
 template <int IN_R, int BITS, int B, bool STOCH>
-__global__ void __launch_bounds__(kK3Block, 1)
+__global__ void __launch_bounds__(kK3Block, K3Cfg<IN_R, kRowElems * BITS / 8>::CTAS)
     k3_tlq_had_quant(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ K3Out out, size_t S, int M,
                      int N, int lg, float cb, size_t unit_bytes, uint32_t tps, uint32_t ntiles, const SR sr,
                      size_t sr_stride, size_t sr_off, uint32_t* sched) {
@@ -239,7 +240,7 @@ cudaError_t launch_tlq_had_quant(const void* grad, size_t grad_stride, int grad_
   const uint64_t rows = S / kRowElems;
   const uint32_t tps = (uint32_t)((rows + kTileRows - 1) / kTileRows);
   const uint32_t ntiles = tps * (uint32_t)(M * N);
-  const int grid = grid_for(ntiles, sms);
+  const int grid = grid_for(ntiles, sms * (grad_dtype == kBF16 ? 2 : 1));  // K3Cfg::CTAS
   const int in_r = grad_dtype == kBF16 ? 128 : 256;
   const int out_r = kRowElems * bits / 8;
   CUtensorMap in_map;
