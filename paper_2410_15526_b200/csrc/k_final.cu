@@ -201,7 +201,7 @@ cudaError_t k5_launch(const CUtensorMap& in_map, float* out, const uint8_t* recv
   constexpr int SMEM = K5Cfg<IN_R>::SMEM;
   cudaError_t e = set_smem(k5_tlq_dq_reduce_had<IN_R, B>, SMEM);
   if (e != cudaSuccess) return e;
-  uint32_t* sched = sched_counter();
+  uint32_t* sched = sched_counter(st);
   if (!sched) return cudaErrorMemoryAllocation;
   k5_tlq_dq_reduce_had<IN_R, B><<<grid, kK5Block, SMEM, st>>>(in_map, recv, unit_bytes, M, S, __builtin_ctz(G), kappa,
                                                                 ntiles, -0.0f, out, sched);
@@ -228,7 +228,7 @@ cudaError_t launch_tlq_dq_reduce_had(const uint8_t* inter_recv, size_t in_unit_b
   return cudaErrorInvalidValue;
 }
 
-uint32_t* sched_counter() {
+uint32_t* sched_counter(cudaStream_t st) {
   constexpr int kSlots = 64;
   static uint32_t* pool = nullptr;
   static std::atomic<uint32_t> next{0};
@@ -237,7 +237,9 @@ uint32_t* sched_counter() {
     if (cudaMalloc(&pool, kSlots * 2 * sizeof(uint32_t)) == cudaSuccess) cudaMemset(pool, 0, kSlots * 2 * sizeof(uint32_t));
     else pool = nullptr;
   });
-  return pool ? pool + 2 * (next++ % kSlots) : nullptr;
+  if (!pool) return nullptr;
+  uint32_t* slot = pool + 2 * (next++ % kSlots);
+  return cudaMemsetAsync(slot, 0, 2 * sizeof(uint32_t), st) == cudaSuccess ? slot : nullptr;
 }
 
 cudaError_t launch_wait_flags(const FlagWait& w, cudaStream_t st) {

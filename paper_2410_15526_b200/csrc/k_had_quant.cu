@@ -208,7 +208,7 @@ cudaError_t k3_launch_t(const CUtensorMap& in_map, const K3Out& out, size_t S, i
   constexpr int SMEM = K3Cfg<IN_R, kRowElems * BITS / 8>::SMEM;
   cudaError_t e = set_smem(k3_tlq_had_quant<IN_R, BITS, B, STOCH>, SMEM);
   if (e != cudaSuccess) return e;
-  uint32_t* sched = sched_counter();
+  uint32_t* sched = sched_counter(st);
   if (!sched) return cudaErrorMemoryAllocation;
   k3_tlq_had_quant<IN_R, BITS, B, STOCH><<<grid, kK3Block, SMEM, st>>>(in_map, out, S, M, N, __builtin_ctz(G), cb,
                                                                         unit_bytes, tps, ntiles, sr, sr_stride, sr_off,

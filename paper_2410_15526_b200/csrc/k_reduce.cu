@@ -344,7 +344,7 @@ cudaError_t k4_launch_v(const uint8_t* recv, size_t in_unit_bytes, int N, int M,
   constexpr int SMEM = K4Cfg<BIN, BOUT, REMOTE>::SMEM;
   cudaError_t e = set_smem(k4_tlq_dq_reduce_q<BIN, BOUT, STOCH, REMOTE, G64>, SMEM);
   if (e != cudaSuccess) return e;
-  uint32_t* sched = sched_counter();
+  uint32_t* sched = sched_counter(st);
   if (!sched) return cudaErrorMemoryAllocation;
   const uint32_t tpu = (uint32_t)((S + kK4Tile - 1) / kK4Tile);
   const uint32_t ntiles = tpu * (uint32_t)M;

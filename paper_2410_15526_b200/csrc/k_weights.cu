@@ -462,7 +462,7 @@ cudaError_t launch_qwd_apply(const Dests& units, int P, size_t S, size_t stride,
   if (skip_rot) rot = (rot + 1) % P;
   if (U <= 0 || S == 0) return cudaSuccess;
   const int grid_r = grid_for((S + kK2rTile - 1) / kK2rTile * U, sms * 4);
-  uint32_t* sched = sched_counter();
+  uint32_t* sched = sched_counter(st);
   if (!sched) return cudaErrorMemoryAllocation;
 #define K2(TM, B, AD)                                                                          \
   do {                                                                                                 \

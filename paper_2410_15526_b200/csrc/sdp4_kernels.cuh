@@ -44,8 +44,11 @@ cudaError_t launch_wait_flags(const FlagWait& w, cudaStream_t st);
 // Dynamic tile scheduling: a persistent kernel's CTAs claim tiles from a global counter pair
 // {next, done} (so faster SMs take more tiles -- a static cyclic split measured 15-20% slower
 // on HBM-bound streams).  Counters come from a small per-process pool, one pair per launch
-// (round-robin), and are reset to zero by the kernel's last CTA.
-uint32_t* sched_counter();
+// (round-robin over 64, so concurrent launches on different streams never share one); the
+// pair is zeroed on the launch's stream right before the kernel (so it is correct whatever
+// the slot's history -- an aborted kernel, a replayed CUDA graph) and the kernel's last CTA
+// zeroes it again.  nullptr if the pool could not be allocated.
+uint32_t* sched_counter(cudaStream_t st);
 
 // K1: Alg. 2 l.2-3 -- d = w_main - w_model (this shard), k-bit group quantization
 // into the wire unit at every destination dst.p[0..n) (n = 1: local; n = P: all-gather push).
