@@ -40,6 +40,7 @@
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: host ranges for nsys / ncu (no link dependency)
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -52,6 +53,15 @@ constexpr int kDefaultNcclCtas = 16;
 constexpr double kDefaultTimeoutS = 300.0;  // P2P flag waits (SDP4_WAIT_TIMEOUT_S; 0 = unbounded memop waits)
 
 thread_local std::string g_err;
+
+// NVTX range around every data-path entry point (the call's name), so an nsys / ncu timeline
+// shows which collective each kernel, memop and NCCL call belongs to (SURVEY sec. 5 tracing).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 sdp4_status fail(sdp4_status st, const char* fmt, ...) {
   char buf[512];
@@ -734,6 +744,7 @@ sdp4_status sdp4_get_unique_id(unsigned char id[SDP4_UNIQUE_ID_BYTES]) {
 
 sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, int world, int groups_M,
                            int group_size_N, int nccl_ctas) {
+  NvtxRange nvtx_("sdp4_comm_init");
   sdp4_status s = check_topology(out, rank, world, groups_M, group_size_N);
   if (s != SDP4_OK) return s;
   if (world > 1 && !id) return fail(SDP4_EINVAL, "id is NULL with world > 1");
@@ -769,6 +780,7 @@ sdp4_status sdp4_comm_init(sdp4_comm_t* out, const unsigned char* id, int rank, 
 
 sdp4_status sdp4_comm_init_p2p(sdp4_comm_t* out, int rank, int world, int groups_M, int group_size_N,
                                sdp4_host_allgather_fn allgather, void* ctx) {
+  NvtxRange nvtx_("sdp4_comm_init_p2p");
   sdp4_status s = check_topology(out, rank, world, groups_M, group_size_N);
   if (s != SDP4_OK) return s;
   if (world > 1 && !allgather) return fail(SDP4_EINVAL, "allgather callback is NULL with world > 1");
@@ -791,6 +803,7 @@ sdp4_status sdp4_comm_init_p2p(sdp4_comm_t* out, int rank, int world, int groups
 }
 
 sdp4_status sdp4_comm_destroy(sdp4_comm_t c) {
+  NvtxRange nvtx_("sdp4_comm_destroy");
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (c->side) cudaStreamSynchronize(c->side);
   for (auto& p : c->pending) {
@@ -1045,12 +1058,14 @@ sdp4_status weight_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes,
 sdp4_status sdp4_qwd_quantize(sdp4_comm_t c, const float* w_main_shard, const void* w_model_full,
                               sdp4_dtype model_dtype, size_t numel, int bits, int group, sdp4_round rnd,
                               uint64_t seed, void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("sdp4_qwd_quantize");
   return weight_quantize(c, true, w_main_shard, w_model_full, model_dtype, numel, bits, group, rnd, seed, workspace,
                          workspace_bytes, stream, "K1_qwd_quantize");
 }
 
 sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes, size_t numel, int bits,
                                      int group, void* w_model_full, sdp4_dtype model_dtype, void* stream) {
+  NvtxRange nvtx_("sdp4_qwd_allgather_apply");
   return weight_apply(c, workspace, workspace_bytes, numel, bits, group, w_model_full, model_dtype, stream, true,
                       "K2_qwd_apply");
 }
@@ -1058,6 +1073,7 @@ sdp4_status sdp4_qwd_allgather_apply(sdp4_comm_t c, void* workspace, size_t work
 sdp4_status sdp4_qwd_step(sdp4_comm_t c, const float* w_main_shard, void* w_model_full, sdp4_dtype model_dtype,
                           size_t numel, int bits, int group, sdp4_round rnd, uint64_t seed, void* workspace,
                           size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("sdp4_qwd_step");
   sdp4_status s = weight_quantize(c, true, w_main_shard, w_model_full, model_dtype, numel, bits, group, rnd, seed,
                                   workspace, workspace_bytes, stream, "K1_qwd_quantize", true);
   if (s != SDP4_OK) return s;
@@ -1067,12 +1083,14 @@ sdp4_status sdp4_qwd_step(sdp4_comm_t c, const float* w_main_shard, void* w_mode
 
 sdp4_status sdp4_qw_quantize(sdp4_comm_t c, const float* w_main_shard, size_t numel, int bits, int group,
                              sdp4_round rnd, uint64_t seed, void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("sdp4_qw_quantize");
   return weight_quantize(c, false, w_main_shard, nullptr, SDP4_F32, numel, bits, group, rnd, seed, workspace,
                          workspace_bytes, stream, "K1_qw_quantize");
 }
 
 sdp4_status sdp4_qw_allgather_apply(sdp4_comm_t c, void* workspace, size_t workspace_bytes, size_t numel, int bits,
                                     int group, void* w_model_full, sdp4_dtype model_dtype, void* stream) {
+  NvtxRange nvtx_("sdp4_qw_allgather_apply");
   return weight_apply(c, workspace, workspace_bytes, numel, bits, group, w_model_full, model_dtype, stream, false,
                       "K2_qw_apply");
 }
@@ -1081,6 +1099,7 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
                                        int bits_intra, int bits_inter, int group, int hadamard_block, int average,
                                        sdp4_round rnd, uint64_t seed, float* out_shard, void* workspace,
                                        size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("sdp4_tlq_hs_reduce_scatter");
   g_err.clear();
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (!valid_round(rnd)) return fail(SDP4_EINVAL, "bad rounding mode %d", (int)rnd);
@@ -1272,6 +1291,7 @@ size_t sdp4_ring_workspace_bytes(int world, size_t numel, int bits, int group) {
 sdp4_status sdp4_ring_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dtype grad_dtype, size_t numel, int bits,
                                      int group, int average, float* out_shard, void* workspace,
                                      size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("sdp4_ring_reduce_scatter");
   g_err.clear();
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (!valid_bits(bits)) return fail(SDP4_EINVAL, "bits %d not in {4, 8, 32}", bits);
@@ -1336,6 +1356,7 @@ sdp4_status sdp4_ring_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dtype
 sdp4_status sdp4_tlq_stage_quantize(const void* grad, sdp4_dtype grad_dtype, size_t numel, int M, int N,
                                     int bits_intra, int group, int hadamard_block, sdp4_round rnd, uint64_t seed,
                                     int rank, void* intra_send, void* stream) {
+  NvtxRange nvtx_("sdp4_tlq_stage_quantize");
   g_err.clear();
   if (M < 1 || N < 1) return fail(SDP4_EINVAL, "bad topology %d x %d", M, N);
   if (!valid_round(rnd) || rank < 0 || rank >= M * N) return fail(SDP4_EINVAL, "bad rounding mode or rank");
@@ -1360,6 +1381,7 @@ sdp4_status sdp4_tlq_stage_quantize(const void* grad, sdp4_dtype grad_dtype, siz
 sdp4_status sdp4_tlq_stage_reduce(const void* intra_recv, size_t numel, int M, int N, int bits_intra,
                                   int bits_inter, int group, sdp4_round rnd, uint64_t seed, int rank,
                                   void* inter_send, void* stream) {
+  NvtxRange nvtx_("sdp4_tlq_stage_reduce");
   g_err.clear();
   if (M < 1 || N < 1) return fail(SDP4_EINVAL, "bad topology %d x %d", M, N);
   if (!valid_round(rnd) || rank < 0 || rank >= M * N) return fail(SDP4_EINVAL, "bad rounding mode or rank");
@@ -1383,6 +1405,7 @@ sdp4_status sdp4_tlq_stage_reduce(const void* intra_recv, size_t numel, int M, i
 
 sdp4_status sdp4_tlq_stage_final(const void* inter_recv, size_t numel, int M, int N, int bits_inter, int group,
                                  int hadamard_block, int average, float* out_shard, void* stream) {
+  NvtxRange nvtx_("sdp4_tlq_stage_final");
   g_err.clear();
   if (M < 1 || N < 1) return fail(SDP4_EINVAL, "bad topology %d x %d", M, N);
   sdp4_status s = check_tlq_args(M * N, numel, 8, bits_inter, group, hadamard_block);
@@ -1443,6 +1466,7 @@ sdp4_status sdp4_profile_read(sdp4_comm_t c, const char** names, double* ms, uin
 
 sdp4_status sdp4_nccl_reduce_scatter(sdp4_comm_t c, const void* send, void* recv, size_t numel, sdp4_dtype dtype,
                                      int average, void* stream) {
+  NvtxRange nvtx_("sdp4_nccl_reduce_scatter");
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (c->world > 1 && !c->world_c) return fail(SDP4_ESTATE, "this comm has no NCCL communicators");
   if (numel % (size_t)c->world) return fail(SDP4_EALIGN, "numel not divisible by world");
@@ -1458,6 +1482,7 @@ sdp4_status sdp4_nccl_reduce_scatter(sdp4_comm_t c, const void* send, void* recv
 
 sdp4_status sdp4_nccl_all_gather(sdp4_comm_t c, const void* send, void* recv, size_t numel, sdp4_dtype dtype,
                                  void* stream) {
+  NvtxRange nvtx_("sdp4_nccl_all_gather");
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (c->world > 1 && !c->world_c) return fail(SDP4_ESTATE, "this comm has no NCCL communicators");
   if (numel % (size_t)c->world) return fail(SDP4_EALIGN, "numel not divisible by world");
