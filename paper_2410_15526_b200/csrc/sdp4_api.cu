@@ -137,6 +137,7 @@ size_t qwd_total(int P, size_t S, int bits, int group, int C) {
 // [flags: kFlagBytes][region].  Flags are binary words flag[kind][stage][src] (see the sync
 // protocol below); one region, reused every call.
 constexpr int kFlagStages = 64, kFlagSrcs = 256;
+constexpr int kDrainStage = kFlagStages - 1;  // TLq-HS layout-change drain (stages 1..2C are per chunk)
 constexpr size_t kFlagBytes = 2 * (size_t)kFlagStages * kFlagSrcs * sizeof(uint32_t);
 enum FlagKind { kData = 0, kFree = 1 };
 inline size_t flag_off(int kind, int stage, int src) {
@@ -175,6 +176,8 @@ struct sdp4_comm {
     size_t numel = 0;
     int bits = 0, group = 0;
   } qwd_pending;
+  uint64_t tlq_layout[6] = {0, 0, 0, 0, 0, 0};  // layout of the last P2P TLq-HS call (drain on change)
+  bool tlq_layout_valid = false;
   unsigned long long timeout_ns = 0;  // > 0: flag waits are polling kernels with this deadline
   uint32_t* err_host = nullptr;       // host-mapped error word written by a timed-out wait
   uint32_t* err_dev = nullptr;
@@ -1147,6 +1150,39 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     for (int q = 0; q < N; ++q) group_ranks[q] = m * N + q;
     for (int q = 0; q < M; ++q) node_ranks[q] = q * N + l;
     const uint32_t remote = ((1u << N) - 1u) & ~(1u << l);
+    // Layout drain.  The receive regions are reused call after call, and a call's per-chunk
+    // flags only order it against the SAME chunk of the previous call.  When the layout
+    // changes (sizes, bit widths, G, chunk count or push/pull split), a region section of this
+    // call can overlap a different section of the previous one, still being read by a peer's
+    // K4 or K5.  So on a layout change every rank first waits until each exchange peer has
+    // finished the previous call: a data/free round on a dedicated stage, raised in stream
+    // order after the previous call's K5 (the same handshake as the data stages, so repeated
+    // drains are safe and a captured graph replays correctly).
+    {
+      const uint64_t sig[6] = {numel, (uint64_t)bits_intra, (uint64_t)bits_inter, (uint64_t)group,
+                               (uint64_t)C, (uint64_t)(pulling ? (pnum << 8 | pden) : 0)};
+      const bool changed = c->tlq_layout_valid && memcmp(sig, c->tlq_layout, sizeof(sig)) != 0;
+      memcpy(c->tlq_layout, sig, sizeof(sig));
+      c->tlq_layout_valid = true;
+      if (changed) {
+        std::vector<int> peers;
+        for (int q : group_ranks) peers.push_back(q);
+        for (int q : node_ranks)
+          if (std::find(peers.begin(), peers.end(), q) == peers.end()) peers.push_back(q);
+        std::vector<Wt> wf, wd;
+        std::vector<Sig> gd, gf;
+        for (int q : peers) {
+          wf.push_back({kFree, kDrainStage, q});
+          gd.push_back({q, kData, kDrainStage});
+          wd.push_back({kData, kDrainStage, q});
+          gf.push_back({q, kFree, kDrainStage});
+        }
+        if ((s = wait_flags(c, st, c->sym_tlq, wf, "wait_tlq_drain")) != SDP4_OK) return s;
+        if ((s = raise_flags(c, st, c->sym_tlq, gd)) != SDP4_OK) return s;
+        if ((s = wait_flags(c, st, c->sym_tlq, wd, "wait_tlq_drain")) != SDP4_OK) return s;
+        if ((s = raise_flags(c, st, c->sym_tlq, gf)) != SDP4_OK) return s;
+      }
+    }
     if (C > 1) c->link(st, c->side);
     for (int k = 0; k < C; ++k) {
       const Chunk& ch = chunks[k];
