@@ -557,40 +557,57 @@ def run_sdp4(a, rank, world, local_rank):
         del grad
         torch.cuda.empty_cache()
         comp = torch.cuda.current_stream()
-        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        # each direction's copies are split over 4 streams: with H2D and D2H in flight together,
+        # one copy per direction gets ~28 GB/s each way on this PCIe link, four ~41 GB/s
+        # (tools/pcie_probe.py)
+        NS = 4
+        s_ins = [torch.cuda.Stream() for _ in range(NS)]
+        s_outs = [torch.cuda.Stream() for _ in range(NS)]
         gd = [torch.empty_like(h_grad, device=dev) for _ in range(2)]
         wmn = [torch.empty_like(h_main, device=dev) for _ in range(2)]
         outs = [torch.empty(S, dtype=torch.float32, device=dev) for _ in range(2)]
-        ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in_ready", "in_free", "out_ready", "out_free")}
-        for k in ("in_free", "out_free"):
-            for e in ev[k]:
+        ev = {k: [[torch.cuda.Event() for _ in range(NS)] for _ in range(2)] for k in ("in_ready", "out_free")}
+        ev.update({k: [torch.cuda.Event() for _ in range(2)] for k in ("in_free", "out_ready")})
+        for e in ev["in_free"]:
+            e.record(comp)
+        for es in ev["out_free"]:
+            for e in es:
                 e.record(comp)
         it = [0]
+
+        def split_copy(dst, src, streams):
+            n, k = dst.numel(), len(streams)
+            for i, st_ in enumerate(streams):
+                with torch.cuda.stream(st_):
+                    dst[i * n // k:(i + 1) * n // k].copy_(src[i * n // k:(i + 1) * n // k], non_blocking=True)
 
         def e2e_step():
             sl = it[0] % 2
             it[0] += 1
-            with torch.cuda.stream(s_in):
-                s_in.wait_event(ev["in_free"][sl])
-                gd[sl].copy_(h_grad, non_blocking=True)
-                wmn[sl].copy_(h_main, non_blocking=True)
-                ev["in_ready"][sl].record(s_in)
-            comp.wait_event(ev["in_ready"][sl])
-            comp.wait_event(ev["out_free"][sl])
+            for st_ in s_ins:
+                st_.wait_event(ev["in_free"][sl])
+            split_copy(gd[sl], h_grad, s_ins)
+            split_copy(wmn[sl], h_main, s_ins)
+            for i, st_ in enumerate(s_ins):
+                ev["in_ready"][sl][i].record(st_)
+                comp.wait_event(ev["in_ready"][sl][i])
+            for e in ev["out_free"][sl]:
+                comp.wait_event(e)
             qwd(wmn[sl])
             comm.tlq_hs_reduce_scatter(gd[sl], outs[sl], ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
             ev["in_free"][sl].record(comp)
             ev["out_ready"][sl].record(comp)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(ev["out_ready"][sl])
-                h_out.copy_(outs[sl], non_blocking=True)
-                ev["out_free"][sl].record(s_out)
+            for st_ in s_outs:
+                st_.wait_event(ev["out_ready"][sl])
+            split_copy(h_out, outs[sl], s_outs)
+            for i, st_ in enumerate(s_outs):
+                ev["out_free"][sl][i].record(st_)
 
         def e2e_run(n):
             for _ in range(n):
                 e2e_step()
-            comp.wait_stream(s_out)    # the region ends when the last readback has landed
-            comp.wait_stream(s_in)
+            for st_ in s_outs + s_ins:   # the region ends when the last readback has landed
+                comp.wait_stream(st_)
 
         e2e_run(2)
         steps_e2e = max(3, min(a.steps, 6))
@@ -599,7 +616,8 @@ def run_sdp4(a, rank, world, local_rank):
                "h2d_bytes_per_step": int(h_grad.numel() * h_grad.element_size() + h_main.numel() * 4),
                "d2h_bytes_per_step": int(h_out.numel() * 4), "ms_per_step": round(ms_e2e, 3),
                "steps": steps_e2e,
-               "schedule": "double-buffered: H2D of step i+1 and D2H of step i overlap step i's kernels"}
+               "schedule": "double-buffered: H2D of step i+1 and D2H of step i overlap step i's kernels; "
+                           "each direction split over 4 copy streams"}
         del h_grad, h_main, h_out, gd, wmn, outs
 
     cpu = None
