@@ -13,5 +13,5 @@ CUDA_VISIBLE_DEVICES=0,1 R 2 bench.py --gpus 2 --steps 20 --warmup 5 --groups 1 
 R 4 bench.py --gpus 4 --steps 20 --warmup 5 > gpurun_out/multi/bench_n4_2x2.json 2> gpurun_out/multi/bench_n4_2x2.err; summ gpurun_out/multi/bench_n4_2x2.json
 R 4 bench.py --gpus 4 --steps 20 --warmup 5 --groups 1 --no-e2e > gpurun_out/multi/bench_n4_1x4.json 2> gpurun_out/multi/bench_n4_1x4.err; summ gpurun_out/multi/bench_n4_1x4.json
 R 4 bench.py --gpus 4 --steps 20 --warmup 5 --groups 4 --no-e2e > gpurun_out/multi/bench_n4_4x1.json 2> gpurun_out/multi/bench_n4_4x1.err; summ gpurun_out/multi/bench_n4_4x1.json
-R 4 tools/size_sweep.py --out gpurun_out/multi/size_sweep_n4_2x2.json > gpurun_out/multi/size_2x2.log 2>&1; tail -2 gpurun_out/multi/size_2x2.log
-R 4 tools/size_sweep.py --groups 1 --out gpurun_out/multi/size_sweep_n4_1x4.json > gpurun_out/multi/size_1x4.log 2>&1; tail -2 gpurun_out/multi/size_1x4.log
+R 4 tools/size_sweep.py --graphs --out gpurun_out/multi/size_sweep_n4_2x2.json > gpurun_out/multi/size_2x2.log 2>&1; tail -2 gpurun_out/multi/size_2x2.log
+R 4 tools/size_sweep.py --graphs --groups 1 --out gpurun_out/multi/size_sweep_n4_1x4.json > gpurun_out/multi/size_1x4.log 2>&1; tail -2 gpurun_out/multi/size_1x4.log

@@ -25,7 +25,8 @@ from paper_2410_15526_b200 import Comm, default_split, pad_numel  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--groups", type=int, default=None)
-    ap.add_argument("--sizes-mb", type=str, default="1,4,16,64,256,1024,4096")
+    ap.add_argument("--sizes-mb", type=str, default="1,2,4,8,16,32,64,128,256,512,1024,2048,4096")
+    ap.add_argument("--graphs", action="store_true", help="also time CUDA-graph replays of every call")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--out", type=str, default=None)
     a = ap.parse_args()
@@ -63,15 +64,34 @@ def main():
         out = torch.empty(S, dtype=torch.float32, device=dev)
         ws_q = torch.empty(comm.qwd_workspace_bytes(D, 4, G), dtype=torch.uint8, device=dev)
         ws_t = torch.empty(comm.tlq_workspace_bytes(D, 8, 4, G), dtype=torch.uint8, device=dev)
-        t_q = timed(lambda: (comm.qwd_quantize(w_main, w_model, ws_q, 4, G), comm.qwd_allgather_apply(ws_q, w_model, 4, G)))
-        t_t = timed(lambda: comm.tlq_hs_reduce_scatter(grad, out, ws_t, 8, 4, G, b, True))
+        fq = lambda: comm.qwd_step(w_main, w_model, ws_q, 4, G)  # noqa: E731
+        ft = lambda: comm.tlq_hs_reduce_scatter(grad, out, ws_t, 8, 4, G, b, True)  # noqa: E731
+        t_q = timed(fq)
+        t_t = timed(ft)
         big = torch.empty(D, dtype=torch.float32, device=dev)
         shard = torch.empty(S, dtype=torch.float32, device=dev)
-        t_ag = timed(lambda: dist.all_gather_into_tensor(big, shard))
-        t_rs = timed(lambda: dist.reduce_scatter_tensor(out, grad, op=dist.ReduceOp.AVG))
-        rows.append({"mbytes": mb, "D": D, "qwd_ms": round(t_q, 4), "nccl_all_gather_ms": round(t_ag, 4),
-                     "ag_speedup": round(t_ag / t_q, 3), "tlq_ms": round(t_t, 4), "nccl_reduce_scatter_ms": round(t_rs, 4),
-                     "rs_speedup": round(t_rs / t_t, 3)})
+        fag = lambda: dist.all_gather_into_tensor(big, shard)  # noqa: E731
+        frs = lambda: dist.reduce_scatter_tensor(out, grad, op=dist.ReduceOp.AVG)  # noqa: E731
+        t_ag = timed(fag)
+        t_rs = timed(frs)
+        row = {"mbytes": mb, "D": D, "qwd_ms": round(t_q, 4), "nccl_all_gather_ms": round(t_ag, 4),
+               "ag_speedup": round(t_ag / t_q, 3), "tlq_ms": round(t_t, 4), "nccl_reduce_scatter_ms": round(t_rs, 4),
+               "rs_speedup": round(t_rs / t_t, 3)}
+        if a.graphs:   # every call captured in a CUDA graph and replayed (the P2P flags carry no epoch)
+            gs = {}
+            side = torch.cuda.Stream()
+            for name, fn in (("qwd", fq), ("tlq", ft), ("ag", fag), ("rs", frs)):
+                g = torch.cuda.CUDAGraph()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.graph(g, stream=side):
+                    fn()
+                torch.cuda.synchronize()
+                gs[name] = timed(g.replay)
+            row.update({"graph_qwd_ms": round(gs["qwd"], 4), "graph_nccl_all_gather_ms": round(gs["ag"], 4),
+                        "graph_ag_speedup": round(gs["ag"] / gs["qwd"], 3), "graph_tlq_ms": round(gs["tlq"], 4),
+                        "graph_nccl_reduce_scatter_ms": round(gs["rs"], 4),
+                        "graph_rs_speedup": round(gs["rs"] / gs["tlq"], 3)})
+        rows.append(row)
         if rank == 0:
             print(json.dumps(rows[-1]), flush=True)
         del w_model, w_main, grad, out, ws_q, ws_t, big, shard
