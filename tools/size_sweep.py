@@ -77,30 +77,35 @@ def main():
         row = {"mbytes": mb, "D": D, "qwd_ms": round(t_q, 4), "nccl_all_gather_ms": round(t_ag, 4),
                "ag_speedup": round(t_ag / t_q, 3), "tlq_ms": round(t_t, 4), "nccl_reduce_scatter_ms": round(t_rs, 4),
                "rs_speedup": round(t_rs / t_t, 3)}
-        if a.graphs:   # every call captured in a CUDA graph and replayed (the P2P flags carry no epoch)
+        if a.graphs:   # libsdp4's calls captured in CUDA graphs and replayed (the P2P flags carry no
+            # epoch); NCCL stays eager (torch's process group hangs at teardown once its
+            # collectives have been captured)
             gs = {}
             side = torch.cuda.Stream()
-            for name, fn in (("qwd", fq), ("tlq", ft), ("ag", fag), ("rs", frs)):
+            for name, fn in (("qwd", fq), ("tlq", ft)):
                 g = torch.cuda.CUDAGraph()
                 side.wait_stream(torch.cuda.current_stream())
                 with torch.cuda.graph(g, stream=side):
                     fn()
                 torch.cuda.synchronize()
                 gs[name] = timed(g.replay)
-            row.update({"graph_qwd_ms": round(gs["qwd"], 4), "graph_nccl_all_gather_ms": round(gs["ag"], 4),
-                        "graph_ag_speedup": round(gs["ag"] / gs["qwd"], 3), "graph_tlq_ms": round(gs["tlq"], 4),
-                        "graph_nccl_reduce_scatter_ms": round(gs["rs"], 4),
-                        "graph_rs_speedup": round(gs["rs"] / gs["tlq"], 3)})
+                del g
+            row.update({"graph_qwd_ms": round(gs["qwd"], 4), "graph_ag_speedup": round(t_ag / gs["qwd"], 3),
+                        "graph_tlq_ms": round(gs["tlq"], 4), "graph_rs_speedup": round(t_rs / gs["tlq"], 3)})
         rows.append(row)
         if rank == 0:
             print(json.dumps(rows[-1]), flush=True)
         del w_model, w_main, grad, out, ws_q, ws_t, big, shard
         torch.cuda.empty_cache()
+    if os.environ.get("SDP4_SWEEP_TRACE"):
+        print(f"rank {rank}: sweep done, closing", flush=True)
     if rank == 0 and a.out:
         with open(a.out, "w") as f:
             json.dump({"n_gpus": P, "split": f"{M}x{N}", "transport": comm.transport, "G": G, "b": b,
                        "bits": "4/8/4", "rows": rows}, f, indent=1)
     comm.close()
+    if os.environ.get("SDP4_SWEEP_TRACE"):
+        print(f"rank {rank}: comm closed", flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
