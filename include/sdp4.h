@@ -142,6 +142,17 @@ sdp4_status sdp4_comm_check(sdp4_comm_t comm);
  * (R16).  EINVAL unless 0 <= num <= den, 1 <= den <= 64. */
 sdp4_status sdp4_comm_set_intra_pull(sdp4_comm_t comm, int num, int den);
 
+/* Host.  Small-message path of the P2P transport: sdp4_qwd_step and
+ * sdp4_tlq_hs_reduce_scatter calls on buffers of numel <= limit elements run as ONE kernel per
+ * rank -- the producing phase writes peer memory over NVLink, the consuming phase polls its
+ * flags in-kernel (same flags, same deadline and SDP4_ETIMEOUT behaviour as the multi-launch
+ * path), so a call costs one launch instead of two or three stream-ordered hand-offs (Alg. 2
+ * l.2-5; Alg. 3, P:368-379 -- the arithmetic and results are identical, R16).
+ * Applies when the ranks are on distinct GPUs, with one chunk, and for TLq-HS when
+ * bits_intra and bits_inter are in {4, 8}; other calls take the multi-launch path.  Default
+ * 0 (off; SDP4_FUSED_MAX_NUMEL overrides); 0 disables it. */
+sdp4_status sdp4_comm_set_fused_limit(sdp4_comm_t comm, size_t numel);
+
 /* Host, collective (every rank calls it).  Waits for this rank's work, then -- if symmetric
  * buffers were allocated -- barriers with the peers (they may still be pulling from this
  * rank's buffers) before unmapping and freeing them; destroys the NCCL communicators and
@@ -306,6 +317,32 @@ sdp4_status sdp4_tlq_stage_reduce(const void* intra_recv, size_t numel, int grou
 sdp4_status sdp4_tlq_stage_final(const void* inter_recv, size_t numel, int groups_M, int group_size_N,
                                  int bits_inter, int group, int hadamard_block, int average, float* out_shard,
                                  void* stream);
+
+/* ---------------------------------------------------------------------------
+ * One-launch kernels on an EMULATED job (tests): all P = world (or M * N <= 8) ranks of a job
+ * run in ONE launch of the small-message kernels on the current device, each rank's symmetric
+ * buffer (flags + region) a slice of `workspace` (device, caller-owned, >= the *_workspace_bytes
+ * value; 0 = invalid arguments).  Array arguments are HOST arrays of P device pointers, rank q
+ * at index q: w_main_shards[q] (fp32, numel / P), w_model_full[q] (its replica, numel, updated
+ * in place as sdp4_qwd_step would on rank q), grads[q] (numel), out_shards[q] (fp32, numel / P,
+ * written as sdp4_tlq_hs_reduce_scatter would on rank q).  fresh != 0 resets the emulated flags
+ * to their initial state (a first call); fresh == 0 continues from the previous call on the
+ * same workspace and sizes (exercises the flag resets between calls).  Stream-ordered on
+ * `stream`; a kernel whose waits do not complete within 20 s gives up (wrong results, no hang).
+ * Errors: EINVAL (arguments, or bits outside the one-launch set), EALIGN, ESTATE (workspace
+ * too small), ECUDA (launch).
+ * ------------------------------------------------------------------------- */
+size_t sdp4_emu_qwd_workspace_bytes(int world, size_t numel, int bits, int group);
+sdp4_status sdp4_emu_qwd_step(int world, const float* const* w_main_shards, void* const* w_model_full,
+                              sdp4_dtype model_dtype, size_t numel, int bits, int group, sdp4_round rnd,
+                              uint64_t seed, int fresh, void* workspace, size_t workspace_bytes, void* stream);
+size_t sdp4_emu_tlq_workspace_bytes(int groups_M, int group_size_N, size_t numel, int bits_intra, int bits_inter,
+                                    int group);
+sdp4_status sdp4_emu_tlq_hs_reduce_scatter(int groups_M, int group_size_N, const void* const* grads,
+                                           sdp4_dtype grad_dtype, size_t numel, int bits_intra, int bits_inter,
+                                           int group, int hadamard_block, int average, sdp4_round rnd, uint64_t seed,
+                                           float* const* out_shards, int fresh, void* workspace,
+                                           size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Instrumentation (measurement only; no effect on results).

@@ -12,8 +12,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsdp4.so")
-SOURCES = ["sdp4_api.cu", "k_weights.cu", "k_had_quant.cu", "k_reduce.cu", "k_final.cu"]
-HEADERS = ["sdp4_kernels.cuh", "sdp4_device.cuh"]
+SOURCES = ["sdp4_api.cu", "k_weights.cu", "k_had_quant.cu", "k_reduce.cu", "k_final.cu", "k_fused.cu",
+           "k_fused_tlq8.cu", "k_fused_tlq4.cu"]
+HEADERS = ["sdp4_kernels.cuh", "sdp4_device.cuh", "k_fused.cuh", "k_fused_tlq.cuh"]
 
 
 def nccl_dirs():

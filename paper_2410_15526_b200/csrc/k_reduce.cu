@@ -43,56 +43,6 @@ struct K4Cfg {
   static constexpr int EPC = 64 / CPT;            // elements per chunk
 };
 
-// K4 helper: decode + dequantize the thread's 64 codes of one source (slot order; chunk c holds
-// elements of half ((c ^ f) * EPC) >> 5) and fold them into acc.  FIRST: acc = x (for quantized
-// inputs 0 + x_0 == x_0 since a dequantized code is never -0; the identity codec keeps the add
-// so that -0 becomes +0 as in R8's acc = 0; acc += x); else acc += x.
-template <int BIN, int CPT, int EPC, bool FIRST>
-__device__ __forceinline__ void k4_item(const uint8_t* codes, float ds0, float ds1, int f, float z, float2* acc) {
-  constexpr float kDec = BIN == 8 ? kDec8 : kDec4;
-#pragma unroll
-  for (int c = 0; c < CPT; ++c) {
-    const uint4 u = *reinterpret_cast<const uint4*>(codes + 16 * (c ^ f));
-    float2* ac = acc + c * (EPC / 2);
-    if constexpr (BIN == 32) {
-      const float2 x0 = make_float2(__uint_as_float(u.x), __uint_as_float(u.y));
-      const float2 x1 = make_float2(__uint_as_float(u.z), __uint_as_float(u.w));
-      ac[0] = f2add(FIRST ? make_float2(0.f, 0.f) : ac[0], x0);
-      ac[1] = f2add(FIRST ? make_float2(0.f, 0.f) : ac[1], x1);
-    } else {
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-      const float2 dec = make_float2(-kDec, -kDec);
-      const float d = (((c ^ f) * EPC) >> 5) ? ds1 : ds0;
-      const float2 dd = make_float2(d, d);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float2 v[BIN == 8 ? 2 : 4];
-        if constexpr (BIN == 8) {  // 4 codes
-          const uint32_t xw = w[q] ^ 0x80808080u;
-          v[0] = f2add(make_float2(__uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7540)),
-                                   __uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7541))), dec);
-          v[1] = f2add(make_float2(__uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7542)),
-                                   __uint_as_float(__byte_perm(xw, 0x4B000000u, 0x7543))), dec);
-        } else {  // 8 codes
-          const uint32_t xw = w[q] ^ 0x88888888u;
-          const uint32_t lo = xw & 0x0F0F0F0Fu, hi = (xw >> 4) & 0x0F0F0F0Fu;
-#pragma unroll
-          for (int b = 0; b < 4; ++b)
-            v[b] = f2add(make_float2(__uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7540 + b)),
-                                     __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7540 + b))), dec);
-        }
-        constexpr int NV = BIN == 8 ? 2 : 4;
-#pragma unroll
-        for (int b = 0; b < NV; ++b) {
-          const float2 x = f2mulz(v[b], dd, z);  // rn(code * ds) (R5); added next: fusion barrier
-          if constexpr (FIRST) ac[NV * q + b] = x;
-          else ac[NV * q + b] = f2add(ac[NV * q + b], x);
-        }
-      }
-    }
-  }
-}
-
 struct K4Pull {  // IntraPull, K4 side: tiles of source l with ts % den < num come from src[l]
   const uint8_t* src[kMaxN];
   uint32_t mask, num, den;

@@ -51,6 +51,9 @@ namespace {
 constexpr int kMaxChunks = 16;
 constexpr int kDefaultNcclCtas = 16;
 constexpr double kDefaultTimeoutS = 300.0;  // P2P flag waits (SDP4_WAIT_TIMEOUT_S; 0 = unbounded memop waits)
+// P2P calls on buffers of at most this many elements run as one kernel per rank (k_fused.cu);
+// SDP4_FUSED_MAX_NUMEL / sdp4_comm_set_fused_limit override (measured crossover)
+constexpr size_t kDefaultFusedLimit = 0;  // off until it beats the multi-launch path
 
 thread_local std::string g_err;
 
@@ -136,13 +139,12 @@ size_t qwd_total(int P, size_t S, int bits, int group, int C) {
 // Library-owned receive buffer, mapped on every rank (CUDA IPC).  Layout:
 // [flags: kFlagBytes][region].  Flags are binary words flag[kind][stage][src] (see the sync
 // protocol below); one region, reused every call.
-constexpr int kFlagStages = 64, kFlagSrcs = 256;
+using sdp4::kFlagStages;
+using sdp4::kFlagSrcs;
 constexpr int kDrainStage = kFlagStages - 1;  // TLq-HS layout-change drain (stages 1..2C are per chunk)
 constexpr size_t kFlagBytes = 2 * (size_t)kFlagStages * kFlagSrcs * sizeof(uint32_t);
-enum FlagKind { kData = 0, kFree = 1 };
-inline size_t flag_off(int kind, int stage, int src) {
-  return (((size_t)kind * kFlagStages + stage) * kFlagSrcs + src) * sizeof(uint32_t);
-}
+enum FlagKind { kData = sdp4::kFlagData, kFree = sdp4::kFlagFree };
+inline size_t flag_off(int kind, int stage, int src) { return sdp4::flag_word(kind, stage, src) * sizeof(uint32_t); }
 struct SymBuf {
   uint8_t* local = nullptr;
   size_t bytes = 0, region = 0;
@@ -178,6 +180,8 @@ struct sdp4_comm {
   } qwd_pending;
   uint64_t tlq_layout[6] = {0, 0, 0, 0, 0, 0};  // layout of the last P2P TLq-HS call (drain on change)
   bool tlq_layout_valid = false;
+  size_t fused_limit = 0;             // P2P calls with numel <= this run as one kernel (k_fused.cu)
+  uint32_t* fused_ctr = nullptr;      // counter blocks of the one-launch kernels (qWD, TLq-HS)
   unsigned long long timeout_ns = 0;  // > 0: flag waits are polling kernels with this deadline
   uint32_t* err_host = nullptr;       // host-mapped error word written by a timed-out wait
   uint32_t* err_dev = nullptr;
@@ -714,8 +718,68 @@ sdp4_comm* comm_new(int rank, int world, int groups_M, int group_size_N, int ncc
     double sec = kDefaultTimeoutS;
     if (const char* e = getenv("SDP4_WAIT_TIMEOUT_S")) sec = atof(e);
     c->timeout_ns = (sec > 0 && c->err_dev) ? (unsigned long long)(sec * 1e9) : 0ull;
+    // one-launch small-message path; counters zeroed once, then by the kernels
+    if (cudaMalloc(&c->fused_ctr, 2 * sdp4::kFusedCtrWords * sizeof(uint32_t)) == cudaSuccess &&
+        cudaMemset(c->fused_ctr, 0, 2 * sdp4::kFusedCtrWords * sizeof(uint32_t)) == cudaSuccess) {
+      c->fused_limit = kDefaultFusedLimit;
+      if (const char* e = getenv("SDP4_FUSED_MAX_NUMEL")) c->fused_limit = (size_t)strtoull(e, nullptr, 10);
+    } else {
+      cudaGetLastError();
+      if (c->fused_ctr) cudaFree(c->fused_ctr);
+      c->fused_ctr = nullptr;
+    }
   }
   return c;
+}
+
+// SDP4_FUSED_TRACE=1 (debugging only): every one-launch call records %globaltimer stamps of its
+// phases, synchronizes, and prints them to stderr as one JSON line per (virtual) rank, in us
+// from the kernel's entry: [exit, A start, A end, B start, B end, C start, C end].
+struct FusedTrace {
+  unsigned long long* host = nullptr;
+  unsigned long long* dev = nullptr;
+};
+FusedTrace* fused_trace() {
+  static FusedTrace t;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    const size_t bytes = sdp4::kMaxVr * sdp4::kTraceSlots * sizeof(unsigned long long);
+    if (getenv("SDP4_FUSED_TRACE") && cudaHostAlloc(&t.host, bytes, cudaHostAllocMapped) == cudaSuccess)
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&t.dev), t.host, 0);
+    else
+      cudaGetLastError();
+  }
+  return t.dev ? &t : nullptr;
+}
+void trace_begin(sdp4::FusedSync& fs) {
+  FusedTrace* t = fused_trace();
+  if (!t) return;
+  for (int i = 0; i < sdp4::kMaxVr * sdp4::kTraceSlots; ++i) t->host[i] = (i & 1) ? 0ull : ~0ull;
+  fs.trace = t->dev;
+}
+void trace_end(const char* what, const sdp4::FusedSync& fs, cudaStream_t st) {
+  FusedTrace* t = fused_trace();
+  if (!t) return;
+  cudaStreamSynchronize(st);
+  const unsigned long long t0 = t->host[0];
+  for (int v = 0; v < fs.nv; ++v) {
+    const unsigned long long* x = t->host + v * sdp4::kTraceSlots;
+    std::string line = std::string("{\"fused_trace\": \"") + what + "\", \"rank\": " + std::to_string(fs.rank[v]) + ", \"us\": [";
+    for (int k = 1; k < sdp4::kTraceSlots; ++k) {
+      const unsigned long long y = (v == 0 || k > 1) ? x[k] : t->host[1];
+      char b[32];
+      snprintf(b, sizeof(b), "%s%.2f", k > 1 ? ", " : "", (y == 0 || y == ~0ull) ? -1.0 : (double)(long long)(y - t0) * 1e-3);
+      line += b;
+    }
+    fprintf(stderr, "%s]}\n", line.c_str());
+  }
+}
+
+// The one-launch path needs distinct GPUs (its kernels poll for other ranks' kernels, which
+// processes sharing one GPU cannot guarantee to run concurrently).
+bool use_fused(const sdp4_comm* c, size_t numel) {
+  return c->transport == kTransportP2P && c->world > 1 && !c->shared_gpu && c->fused_ctr && numel <= c->fused_limit;
 }
 
 void comm_free(sdp4_comm* c) {
@@ -724,6 +788,7 @@ void comm_free(sdp4_comm* c) {
   if (c->world_c) ncclCommDestroy(c->world_c);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->err_host) cudaFreeHost(c->err_host);
+  if (c->fused_ctr) cudaFree(c->fused_ctr);
   delete c;
 }
 }  // namespace
@@ -856,6 +921,12 @@ sdp4_status sdp4_comm_set_intra_pull(sdp4_comm_t c, int num, int den) {
   if (den < 1 || den > 64 || num < 0 || num > den) return fail(SDP4_EINVAL, "intra pull %d/%d not in [0, 1]", num, den);
   c->pull_num = num;
   c->pull_den = den;
+  return SDP4_OK;
+}
+
+sdp4_status sdp4_comm_set_fused_limit(sdp4_comm_t c, size_t numel) {
+  if (!c) return fail(SDP4_EINVAL, "comm is NULL");
+  c->fused_limit = numel;
   return SDP4_OK;
 }
 
@@ -1077,6 +1148,45 @@ sdp4_status sdp4_qwd_step(sdp4_comm_t c, const float* w_main_shard, void* w_mode
                           size_t numel, int bits, int group, sdp4_round rnd, uint64_t seed, void* workspace,
                           size_t workspace_bytes, void* stream) {
   NvtxRange nvtx_("sdp4_qwd_step");
+  if (c && use_fused(c, numel)) {  // small message: the whole step as one kernel per rank
+    g_err.clear();
+    if (!valid_round(rnd)) return fail(SDP4_EINVAL, "bad rounding mode %d", (int)rnd);
+    if (!valid_wbits(bits)) return fail(SDP4_EINVAL, "bits %d not in {2, 4, 8, 32}", bits);
+    if (model_dtype != SDP4_F32 && model_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad model dtype");
+    sdp4_status s = check_sizes(c->world, numel, group);
+    if (s != SDP4_OK) return s;
+    if ((s = check_ptr(w_main_shard, "w_main_shard")) != SDP4_OK) return s;
+    if ((s = check_ptr(w_model_full, "w_model_full")) != SDP4_OK) return s;
+    if ((s = async_check(c)) != SDP4_OK) return s;
+    if (c->qwd_pending.valid)
+      return fail(SDP4_ESTATE, "P2P: the unit of the previous quantize has not been applied yet (one outstanding "
+                               "quantize per comm: call the matching allgather_apply first)");
+    const size_t S = numel / c->world;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if ((s = sym_ensure(c, c->sym_qwd, unit_bytes(S, bits, group), st)) != SDP4_OK) return s;
+    sdp4::FusedSync fs;
+    memset(&fs, 0, sizeof(fs));
+    for (int q = 0; q < c->world; ++q) {
+      fs.region[q] = sym_region(c->sym_qwd, q);
+      fs.flags[q] = reinterpret_cast<uint32_t*>(c->sym_qwd.peer[q]);
+    }
+    fs.rank[0] = c->rank;
+    fs.nv = 1;
+    fs.P = c->world;
+    fs.ctr = c->fused_ctr;
+    fs.err = c->err_dev;
+    fs.timeout_ns = c->timeout_ns;
+    const uint32_t key = sr_key(seed, kStageQwd, c->rank);
+    const float* wm = w_main_shard;
+    void* wmod = w_model_full;
+    trace_begin(fs);
+    s = launch(c, "KF_qwd_step", st, [&] {
+      return sdp4::launch_fused_qwd(fs, &wm, &wmod, model_dtype, S, bits, group, rnd == SDP4_STOCHASTIC, &key,
+                                    c->sm_count, st);
+    });
+    trace_end("qwd", fs, st);
+    return s;
+  }
   sdp4_status s = weight_quantize(c, true, w_main_shard, w_model_full, model_dtype, numel, bits, group, rnd, seed,
                                   workspace, workspace_bytes, stream, "K1_qwd_quantize", true);
   if (s != SDP4_OK) return s;
@@ -1135,7 +1245,9 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     // between the caller's stream and the side stream, so K4/K5 of chunk k overlap the
     // NVLink-bound K3 of chunk k+1 (the overlap of P:344).  Symmetric region, per chunk:
     // [intra receive: N blocks][inter receive: M units][outbox: N blocks].
-    const int pnum = c->pull_num >= 0 ? c->pull_num : (N <= 2 ? 0 : 1);  // auto split
+    // small messages: the whole reduce-scatter as one kernel per rank (push-only layout)
+    const bool fused = C == 1 && use_fused(c, numel) && sdp4::fused_tlq_supported(bits_intra, bits_inter, b);
+    const int pnum = fused ? 0 : c->pull_num >= 0 ? c->pull_num : (N <= 2 ? 0 : 1);  // auto split
     const int pden = c->pull_num >= 0 ? c->pull_den : 2;
     const bool pulling = N > 1 && pnum > 0;
     if (C > kMaxChunks) return fail(SDP4_EINVAL, "too many chunks");
@@ -1182,6 +1294,30 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
         if ((s = wait_flags(c, st, c->sym_tlq, wd, "wait_tlq_drain")) != SDP4_OK) return s;
         if ((s = raise_flags(c, st, c->sym_tlq, gf)) != SDP4_OK) return s;
       }
+    }
+    if (fused) {
+      sdp4::FusedSync fs;
+      memset(&fs, 0, sizeof(fs));
+      for (int q = 0; q < P; ++q) {
+        fs.region[q] = sym_region(c->sym_tlq, q);
+        fs.flags[q] = reinterpret_cast<uint32_t*>(c->sym_tlq.peer[q]);
+      }
+      fs.rank[0] = c->rank;
+      fs.nv = 1;
+      fs.P = P;
+      fs.ctr = c->fused_ctr + sdp4::kFusedCtrWords;
+      fs.err = c->err_dev;
+      fs.timeout_ns = c->timeout_ns;
+      const void* g = grad;
+      float* o = out_shard;
+      trace_begin(fs);
+      s = launch(c, "KF_tlq_hs", st, [&] {
+        return sdp4::launch_fused_tlq(fs, &g, grad_dtype, &o, M, N, S, group, b, cb, kappa, bits_intra, bits_inter,
+                                      unit_bytes(S, bits_intra, group), unit_bytes(S, bits_inter, group), sr, &key8,
+                                      &key4, c->sm_count, st);
+      });
+      trace_end("tlq", fs, st);
+      return s;
     }
     if (C > 1) c->link(st, c->side);
     for (int k = 0; k < C; ++k) {
@@ -1455,6 +1591,129 @@ sdp4_status sdp4_tlq_stage_final(const void* inter_recv, size_t numel, int M, in
                                                  hadamard_block, final_kappa(hadamard_block, M * N, average),
                                                  out_shard, sm_count_current(), st);
   return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "K5 launch failed: %s", cudaGetErrorString(e));
+}
+
+// ---- One-launch kernels on an emulated P-rank job (every rank's symmetric buffer a slice of
+// one device workspace, all ranks in ONE launch): the parity tests' route to the kernels of
+// the small-message path on a single GPU.  Workspace: [counters: 256 B][rank 0: flags, region]...
+namespace {
+constexpr size_t kEmuHead = 256;
+size_t emu_rank_bytes(size_t region) { return kFlagBytes + round_up(region, 256); }
+
+sdp4_status emu_prepare(uint8_t* ws, int P, size_t region, int fresh, cudaStream_t st, sdp4::FusedSync* fs) {
+  memset(fs, 0, sizeof(*fs));
+  const size_t rb = emu_rank_bytes(region);
+  for (int q = 0; q < P; ++q) {
+    uint8_t* base = ws + kEmuHead + (size_t)q * rb;
+    fs->flags[q] = reinterpret_cast<uint32_t*>(base);
+    fs->region[q] = base + kFlagBytes;
+    fs->rank[q] = q;
+    if (fresh) {  // a first call: data flags 0, free flags 1 (sym_ensure's initial state)
+      const size_t half = flag_off(kFree, 0, 0) / 4;
+      cudaError_t e = sdp4::launch_fill32(fs->flags[q], half, 0u, st);
+      if (e == cudaSuccess) e = sdp4::launch_fill32(fs->flags[q] + half, kFlagBytes / 4 - half, 1u, st);
+      if (e != cudaSuccess) return fail(SDP4_ECUDA, "flag init: %s", cudaGetErrorString(e));
+    }
+  }
+  fs->nv = P;
+  fs->P = P;
+  fs->ctr = reinterpret_cast<uint32_t*>(ws);
+  fs->err = nullptr;
+  fs->timeout_ns = 20ull * 1000000000ull;  // a broken kernel gives up (wrong results, no hang)
+  if (fresh && cudaMemsetAsync(ws, 0, kEmuHead, st) != cudaSuccess) return fail(SDP4_ECUDA, "counter init failed");
+  return SDP4_OK;
+}
+}  // namespace
+
+size_t sdp4_emu_qwd_workspace_bytes(int world, size_t numel, int bits, int group) {
+  if (world < 2 || world > sdp4::kMaxVr || !valid_wbits(bits) || !is_pow2(group) || numel % (size_t)world) return 0;
+  return kEmuHead + (size_t)world * emu_rank_bytes(unit_bytes(numel / world, bits, group));
+}
+
+sdp4_status sdp4_emu_qwd_step(int world, const float* const* w_main_shards, void* const* w_model_full,
+                              sdp4_dtype model_dtype, size_t numel, int bits, int group, sdp4_round rnd,
+                              uint64_t seed, int fresh, void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("sdp4_emu_qwd_step");
+  g_err.clear();
+  if (world < 2 || world > sdp4::kMaxVr) return fail(SDP4_EINVAL, "world %d not in [2, %d]", world, sdp4::kMaxVr);
+  if (!w_main_shards || !w_model_full) return fail(SDP4_EINVAL, "pointer arrays are NULL");
+  if (!valid_round(rnd)) return fail(SDP4_EINVAL, "bad rounding mode %d", (int)rnd);
+  if (!valid_wbits(bits)) return fail(SDP4_EINVAL, "bits %d not in {2, 4, 8, 32}", bits);
+  if (model_dtype != SDP4_F32 && model_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad model dtype");
+  sdp4_status s = check_sizes(world, numel, group);
+  if (s != SDP4_OK) return s;
+  for (int q = 0; q < world; ++q) {
+    if ((s = check_ptr(w_main_shards[q], "w_main_shards[q]")) != SDP4_OK) return s;
+    if ((s = check_ptr(w_model_full[q], "w_model_full[q]")) != SDP4_OK) return s;
+  }
+  if ((s = check_ptr(workspace, "workspace")) != SDP4_OK) return s;
+  const size_t need = sdp4_emu_qwd_workspace_bytes(world, numel, bits, group);
+  if (workspace_bytes < need) return fail(SDP4_ESTATE, "workspace %zu < %zu bytes", workspace_bytes, need);
+  const size_t S = numel / world;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  sdp4::FusedSync fs;
+  if ((s = emu_prepare(static_cast<uint8_t*>(workspace), world, unit_bytes(S, bits, group), fresh, st, &fs)) != SDP4_OK)
+    return s;
+  uint32_t keys[sdp4::kMaxVr];
+  for (int q = 0; q < world; ++q) keys[q] = sr_key(seed, kStageQwd, q);
+  trace_begin(fs);
+  cudaError_t e = sdp4::launch_fused_qwd(fs, w_main_shards, w_model_full, model_dtype, S, bits, group,
+                                         rnd == SDP4_STOCHASTIC, keys, sm_count_current(), st);
+  trace_end("emu_qwd", fs, st);
+  return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "one-launch qWD failed: %s", cudaGetErrorString(e));
+}
+
+size_t sdp4_emu_tlq_workspace_bytes(int M, int N, size_t numel, int bits_intra, int bits_inter, int group) {
+  const int P = M * N;
+  if (M < 1 || N < 1 || P < 2 || P > sdp4::kMaxVr || !valid_bits(bits_intra) || !valid_bits(bits_inter) ||
+      !is_pow2(group) || numel % (size_t)P)
+    return 0;
+  const size_t S = numel / P;
+  return kEmuHead + (size_t)P * emu_rank_bytes((size_t)N * M * unit_bytes(S, bits_intra, group) +
+                                               (size_t)M * unit_bytes(S, bits_inter, group));
+}
+
+sdp4_status sdp4_emu_tlq_hs_reduce_scatter(int M, int N, const void* const* grads, sdp4_dtype grad_dtype,
+                                           size_t numel, int bits_intra, int bits_inter, int group,
+                                           int hadamard_block, int average, sdp4_round rnd, uint64_t seed,
+                                           float* const* out_shards, int fresh, void* workspace,
+                                           size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("sdp4_emu_tlq_hs_reduce_scatter");
+  g_err.clear();
+  const int P = M * N, b = hadamard_block;
+  if (M < 1 || N < 1 || P < 2 || P > sdp4::kMaxVr) return fail(SDP4_EINVAL, "bad topology %d x %d", M, N);
+  if (!grads || !out_shards) return fail(SDP4_EINVAL, "pointer arrays are NULL");
+  if (!valid_round(rnd)) return fail(SDP4_EINVAL, "bad rounding mode %d", (int)rnd);
+  if (grad_dtype != SDP4_F32 && grad_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad grad dtype");
+  sdp4_status s = check_tlq_args(P, numel, bits_intra, bits_inter, group, b);
+  if (s != SDP4_OK) return s;
+  if (!sdp4::fused_tlq_supported(bits_intra, bits_inter, b))
+    return fail(SDP4_EINVAL, "the one-launch path takes bits_intra, bits_inter in {4, 8}");
+  for (int q = 0; q < P; ++q) {
+    if ((s = check_ptr(grads[q], "grads[q]")) != SDP4_OK) return s;
+    if ((s = check_ptr(out_shards[q], "out_shards[q]")) != SDP4_OK) return s;
+  }
+  if ((s = check_ptr(workspace, "workspace")) != SDP4_OK) return s;
+  const size_t need = sdp4_emu_tlq_workspace_bytes(M, N, numel, bits_intra, bits_inter, group);
+  if (workspace_bytes < need) return fail(SDP4_ESTATE, "workspace %zu < %zu bytes", workspace_bytes, need);
+  const size_t S = numel / P;
+  const size_t w8 = unit_bytes(S, bits_intra, group), w4 = unit_bytes(S, bits_inter, group);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  sdp4::FusedSync fs;
+  if ((s = emu_prepare(static_cast<uint8_t*>(workspace), P, (size_t)N * M * w8 + (size_t)M * w4, fresh, st, &fs)) !=
+      SDP4_OK)
+    return s;
+  uint32_t k8[sdp4::kMaxVr], k4[sdp4::kMaxVr];
+  for (int q = 0; q < P; ++q) {
+    k8[q] = sr_key(seed, kStageIntra, q);
+    k4[q] = sr_key(seed, kStageInter, q);
+  }
+  trace_begin(fs);
+  cudaError_t e = sdp4::launch_fused_tlq(fs, grads, grad_dtype, out_shards, M, N, S, group, b, hadamard_cb(b),
+                                         final_kappa(b, P, average), bits_intra, bits_inter, w8, w4,
+                                         rnd == SDP4_STOCHASTIC, k8, k4, sm_count_current(), st);
+  trace_end("emu_tlq", fs, st);
+  return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "one-launch TLq-HS failed: %s", cudaGetErrorString(e));
 }
 
 uint64_t sdp4_launch_count(sdp4_comm_t c, int reset) {

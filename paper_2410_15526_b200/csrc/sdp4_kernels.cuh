@@ -114,4 +114,53 @@ cudaError_t launch_tlq_dq_reduce_had(const uint8_t* inter_recv, size_t in_unit_b
                                      int M, size_t S, int G, int b, float kappa, float* out,
                                      int sms, cudaStream_t st);
 
+// ---- P2P flag layout (the sync protocol of sdp4_api.cu): word flag[kind][stage][src] of a
+// rank's symmetric buffer; kind 0 = data (src published into my region), 1 = free (src is done
+// with the region I wrote / it reads).
+constexpr int kFlagStages = 64, kFlagSrcs = 256;
+constexpr int kFlagData = 0, kFlagFree = 1;
+__host__ __device__ inline size_t flag_word(int kind, int stage, int src) {
+  return ((size_t)kind * kFlagStages + stage) * kFlagSrcs + src;
+}
+
+// ---- One-launch P2P paths ("small messages").  The whole exchange runs as
+// ONE kernel per rank: the producing phase writes its units (peer memory over NVLink), the last
+// warp / CTA to finish a phase raises the peers' data flags with system-scope release stores,
+// the consuming phase polls its own flags with acquire loads (deadline: timeout_ns, then
+// *err = code and carry on), and the last consumer raises the free flags -- the same flags, in
+// the same order, as the multi-launch path, so the two paths interoperate call by call.
+// Phases are claimed in order from one counter, so a task that waits for another phase finds
+// every task of that phase already claimed by a running CTA: no co-residency assumption.
+// nv > 1 virtual ranks in one launch emulate a P-rank job on one device (region / flags of
+// every virtual rank are then plain device buffers): the parity tests' route on one GPU.
+constexpr int kMaxVr = 8;  // virtual ranks per launch
+constexpr int kFusedCtrWords = 32;  // per-op counter block: claim, exit, done[phase][vr]
+struct FusedSync {
+  uint8_t* region[kMaxDests];   // symmetric region of every rank (this process's mapping)
+  uint32_t* flags[kMaxDests];   // flag words of every rank
+  int rank[kMaxVr];             // ranks this launch acts for
+  int nv, P;
+  uint32_t* ctr;                // kFusedCtrWords counters, zero between launches
+  uint32_t* err;                // host-mapped error word (timeouts), may be null
+  unsigned long long timeout_ns;  // 0: wait forever
+  unsigned long long* trace;    // debugging (SDP4_FUSED_TRACE): kTraceSlots %globaltimer stamps per rank
+};
+constexpr int kTraceSlots = 8;  // entry, exit, A start, A end, B start, B end, C start, C end (even: min, odd: max)
+// qWD step (Alg. 2 l.2-5): phase A quantizes the own shard into region[rank] and applies it to
+// the own replica shard (K1 with apply_own); phase B applies every peer's unit (K2's pull).
+// bits in {2, 4, 8, 32}, G <= 2048.  Flag stage 0.
+cudaError_t launch_fused_qwd(const FusedSync& fs, const float* const* w_main, void* const* w_model, int model_dtype,
+                             size_t S, int bits, int G, int sr_on, const uint32_t* sr_key, int sms, cudaStream_t st);
+// TLq-HS (Alg. 3): phase A = K3 (push into the group peers' intra receive blocks), B = K4 (push
+// into the node peers' inter slots), C = K5; the push-only single-chunk layout of the P2P path
+// ([intra receive: N blocks of M units of w8][inter receive: M units of w4]).  bits_intra and
+// bits_inter in {4, 8}; b in {0, 2, ..., 256}.  Flag stages 1 (intra) and 2 (inter).
+cudaError_t launch_fused_tlq(const FusedSync& fs, const void* const* grad, int grad_dtype, float* const* out,
+                             int M, int N, size_t S, int G, int b, float cb, float kappa, int bits_intra,
+                             int bits_inter, size_t w8, size_t w4, int sr_on, const uint32_t* key8,
+                             const uint32_t* key4, int sms, cudaStream_t st);
+bool fused_tlq_supported(int bits_intra, int bits_inter, int b);
+// Fill n words with v (flag initialization of emulated symmetric buffers).
+cudaError_t launch_fill32(uint32_t* p, size_t n, uint32_t v, cudaStream_t st);
+
 }  // namespace sdp4

@@ -46,6 +46,7 @@ SIGNATURES = {
     "sdp4_comm_set_transport": (_ci, [_vp, _ci]),
     "sdp4_comm_transport": (_ci, [_vp]),
     "sdp4_comm_set_intra_pull": (_ci, [_vp, _ci, _ci]),
+    "sdp4_comm_set_fused_limit": (_ci, [_vp, _c_size]),
     "sdp4_wire_unit_bytes": (_c_size, [_c_size, _ci, _ci]),
     "sdp4_qwd_workspace_bytes": (_c_size, [_ci, _c_size, _ci, _ci]),
     "sdp4_tlq_workspace_bytes": (_c_size, [_ci, _ci, _c_size, _ci, _ci, _ci]),
@@ -62,6 +63,12 @@ SIGNATURES = {
     "sdp4_tlq_stage_quantize": (_ci, [_vp, _ci, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _u64, _ci, _vp, _vp]),
     "sdp4_tlq_stage_reduce": (_ci, [_vp, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _u64, _ci, _vp, _vp]),
     "sdp4_tlq_stage_final": (_ci, [_vp, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _vp, _vp]),
+    "sdp4_emu_qwd_workspace_bytes": (_c_size, [_ci, _c_size, _ci, _ci]),
+    "sdp4_emu_qwd_step": (_ci, [_ci, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _ci, _c_size, _ci, _ci, _ci, _u64,
+                                _ci, _vp, _c_size, _vp]),
+    "sdp4_emu_tlq_workspace_bytes": (_c_size, [_ci, _ci, _c_size, _ci, _ci, _ci]),
+    "sdp4_emu_tlq_hs_reduce_scatter": (_ci, [_ci, _ci, ctypes.POINTER(_vp), _ci, _c_size, _ci, _ci, _ci, _ci, _ci,
+                                             _ci, _u64, ctypes.POINTER(_vp), _ci, _vp, _c_size, _vp]),
     "sdp4_launch_count": (_u64, [_vp, _ci]),
     "sdp4_profile_enable": (_ci, [_vp, _ci]),
     "sdp4_profile_read": (_ci, [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
@@ -163,6 +170,41 @@ def tlq_stage_final(inter_recv: torch.Tensor, out_shard: torch.Tensor, numel: in
                                       int(bool(average)), _ptr(out_shard), _stream(stream)))
 
 
+def _ptr_array(ts):
+    return (_vp * len(ts))(*[_ptr(t) for t in ts])
+
+
+def emu_qwd_workspace_bytes(world: int, numel: int, bits: int = 4, group: int = 128) -> int:
+    return lib().sdp4_emu_qwd_workspace_bytes(world, numel, bits, group)
+
+
+def emu_qwd_step(w_main_shards, w_models, workspace: torch.Tensor, bits: int = 4, group: int = 128, seed=None,
+                 fresh: bool = True, stream=None):
+    """The one-launch qWD step of every rank of an emulated job in one launch on this device
+    (sdp4_emu_qwd_step): w_models[q] is updated as rank q's replica."""
+    P = len(w_main_shards)
+    _check(lib().sdp4_emu_qwd_step(P, _ptr_array(w_main_shards), _ptr_array(w_models), _DT[w_models[0].dtype],
+                                   w_models[0].numel(), bits, group, RNE if seed is None else STOCHASTIC, seed or 0,
+                                   int(bool(fresh)), _ptr(workspace), _nbytes(workspace), _stream(stream)))
+
+
+def emu_tlq_workspace_bytes(M: int, N: int, numel: int, bits_intra: int = 8, bits_inter: int = 4,
+                            group: int = 128) -> int:
+    return lib().sdp4_emu_tlq_workspace_bytes(M, N, numel, bits_intra, bits_inter, group)
+
+
+def emu_tlq_hs_reduce_scatter(M: int, N: int, grads, out_shards, workspace: torch.Tensor, bits_intra: int = 8,
+                              bits_inter: int = 4, group: int = 128, hadamard_block: int = 64,
+                              average: bool = True, seed=None, fresh: bool = True, stream=None):
+    """The one-launch TLq-HS of every rank of an emulated M x N job in one launch on this device
+    (sdp4_emu_tlq_hs_reduce_scatter): out_shards[q] receives rank q's shard."""
+    _check(lib().sdp4_emu_tlq_hs_reduce_scatter(M, N, _ptr_array(grads), _DT[grads[0].dtype], grads[0].numel(),
+                                                bits_intra, bits_inter, group, hadamard_block, int(bool(average)),
+                                                RNE if seed is None else STOCHASTIC, seed or 0,
+                                                _ptr_array(out_shards), int(bool(fresh)), _ptr(workspace),
+                                                _nbytes(workspace), _stream(stream)))
+
+
 def get_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(UNIQUE_ID_BYTES)
     _check(lib().sdp4_get_unique_id(buf))
@@ -245,6 +287,11 @@ class Comm:
         """P2P: share num/den of the peer tiles of the intra all-to-all pulled by K4 (the rest
         pushed by K3); see sdp4_comm_set_intra_pull."""
         _check(lib().sdp4_comm_set_intra_pull(self._h, num, den))
+
+    def set_fused_limit(self, numel: int):
+        """P2P calls on at most `numel` elements run as one kernel per rank (0: never); see
+        sdp4_comm_set_fused_limit."""
+        _check(lib().sdp4_comm_set_fused_limit(self._h, numel))
 
     @property
     def transport(self) -> str:

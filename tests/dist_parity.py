@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--timeout-test", action="store_true", help="rank 1 skips a call; rank 0 must time out")
     ap.add_argument("--graph", action="store_true", help="also replay CUDA-graph-captured P2P calls")
     ap.add_argument("--wait", type=str, default="kernel", help="P2P waits: kernel (timeout) or memop (unbounded)")
+    ap.add_argument("--fused-limit", type=int, default=None, help="timeout test: sdp4_comm_set_fused_limit value")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = 0 if a.virtual else int(os.environ.get("LOCAL_RANK", rank))
@@ -54,7 +55,7 @@ def main():
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if a.timeout_test:
-        ok, msg = run_timeout_test(rank, world)
+        ok, msg = run_timeout_test(rank, world, fused_limit=a.fused_limit)
         print(f"rank {rank}/{world} {'PASS' if ok else 'FAIL'} timeout test: {msg}", flush=True)
         dist.barrier()
         dist.destroy_process_group()
@@ -136,15 +137,23 @@ def run_matrix(comm, rank, P, M, N, G, b, runs, graph=False):
                 comm.set_intra_pull(*{-1: (0, 1), -3: (2, 3)}[chunks])
             else:
                 comm.set_intra_pull(1, 2) if N > 2 else comm.set_intra_pull(0, 1)
-        for S in (16384 * 2 + 64 * 5 * max(1, G // 64), 16384 * 12 + 640):
-            S -= S % max(G, 64)
-            ok_c, m_c = run_checks(comm, rank, P, M, N, G, b, S, seed)
-            ok &= ok_c
-            msgs += [f"{tr} chunks={chunks} seed={seed} S={S} ({comm.chunks(P * S, G)} used): {m}" for m in m_c]
+        # P2P single-chunk calls run as one kernel per rank below the fused limit (k_fused.cu) and
+        # multi-launch above it: both, on the same comm, interleaved call by call
+        limits = (0, 1 << 40) if tr == "p2p" and chunks in (0, -1, -3) else (0,)
+        for lim in limits:
+            comm.set_fused_limit(lim)
+            for S in (16384 * 2 + 64 * 5 * max(1, G // 64), 16384 * 12 + 640):
+                S -= S % max(G, 64)
+                ok_c, m_c = run_checks(comm, rank, P, M, N, G, b, S, seed)
+                ok &= ok_c
+                msgs += [f"{tr} chunks={chunks} seed={seed} fused={lim > 0} S={S} ({comm.chunks(P * S, G)} used): {m}"
+                         for m in m_c]
     if graph and comm.transport == "p2p":
-        ok_g, m_g = run_graph(comm, rank, P, M, N, G, b)
-        ok &= ok_g
-        msgs += m_g
+        for lim in (0, 1 << 40):
+            comm.set_fused_limit(lim)
+            ok_g, m_g = run_graph(comm, rank, P, M, N, G, b)
+            ok &= ok_g
+            msgs += [f"fused={lim > 0}: {m}" for m in m_g]
     msgs.append(f"{len(runs)} runs x 2 sizes{' + graph replays' if graph else ''}")
     return ok, msgs
 
@@ -199,13 +208,15 @@ def run_graph(comm, rank, P, M, N, G, b, S=16384 * 2 + 640, replays=3):
     return ok, msgs
 
 
-def run_timeout_test(rank, world, timeout_s=1.0):
+def run_timeout_test(rank, world, timeout_s=1.0, fused_limit=None):
     """Bounded waits: after one good call on both ranks, rank 1 skips the next collective call.
     Rank 0's flag waits must give up at the deadline (the stream drains, no hang) and the
     following call must return SDP4_ETIMEOUT; rank 1 is unaffected."""
     import time
     from paper_2410_15526_b200 import sdp4
     comm = Comm.from_process_group(1 if world == 2 else None)
+    if fused_limit is not None:   # 0: the multi-launch path's wait kernels; else the one-launch kernel's waits
+        comm.set_fused_limit(fused_limit)
     P = world
     S = 16384 * 2
     D = P * S

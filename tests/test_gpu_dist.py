@@ -50,14 +50,17 @@ def test_dist_parity_memop_waits(nproc, groups):
     assert r.stdout.count("PASS") == nproc, r.stdout
 
 
-def test_dist_wait_timeout():
+@pytest.mark.parametrize("fused_limit", [0, 1 << 40])
+def test_dist_wait_timeout(fused_limit):
     """Bounded waits on two GPUs: rank 1 skips a collective call; rank 0's polling waits give
-    up at the deadline (its stream drains, no hang) and its next call returns SDP4_ETIMEOUT."""
+    up at the deadline (its stream drains, no hang) and its next call returns SDP4_ETIMEOUT --
+    for the multi-launch path's wait kernels (limit 0) and the one-launch kernel's in-kernel
+    waits."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29590", os.path.join(ROOT, "tests", "dist_parity.py"),
-           "--timeout-test"]
+           "--master-addr=127.0.0.1", f"--master-port={29590 + (fused_limit > 0)}",
+           os.path.join(ROOT, "tests", "dist_parity.py"), "--timeout-test", "--fused-limit", str(fused_limit)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("PASS") == 2, r.stdout

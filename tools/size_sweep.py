@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--graphs", action="store_true", help="also time CUDA-graph replays of every call")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--out", type=str, default=None)
+    ap.add_argument("--fused-limit", type=int, default=None,
+                    help="sdp4_comm_set_fused_limit (elements; 0 = always multi-launch)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -37,6 +39,8 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     M, N = default_split(world, a.groups)
     comm = Comm.from_process_group(a.groups, dev)
+    if a.fused_limit is not None:
+        comm.set_fused_limit(a.fused_limit)
     P, G, b = world, 128, 64
 
     def timed(fn):
