@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kFThreads) kf_qwd_step(const FusedSync fs, con
     s_free_ok = 0;
     for (int v = 0; v < kMaxVr; ++v) s_seen[v] = 0;
   }
-  if (t == 0) tstamp(fs, 0, 0);
+  if (t == 0) tstamp(fs, blockIdx.x, 0);
   for (;;) {
     if (t == 0) s_task = atomicAdd(fs.ctr, 1u);
     __syncthreads();
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kFThreads) kf_qwd_step(const FusedSync fs, con
       const int v = (int)(task % nv);
       const uint32_t ts = task / nv;
       const int r = fs.rank[v];
-      if (t == 0) tstamp(fs, v, 2);
+      if (t == 0) tstamp(fs, blockIdx.x, 2);
       if (t == 0 && !((s_free_ok >> v) & 1u)) {
         for (int q2 = 0; q2 < P; ++q2)
           if (q2 != r) wait_flag(fs, flag(fs, r, kFlagFree, 0, q2), wait_code(kFlagFree, 0, q2));
@@ -151,15 +151,14 @@ __global__ void __launch_bounds__(kFThreads) kf_qwd_step(const FusedSync fs, con
           store_replica8<TM>(wm + e0, m, f);
         }
       }
-      __threadfence_system();
       __syncthreads();
-      if (t == 0) tstamp(fs, v, 3);
+      if (t == 0) tstamp(fs, blockIdx.x, 3);
       if (t == 0 && finish_task(fs, 0, v, tpu)) {
         for (int q2 = 0; q2 < P; ++q2)
           if (q2 != r) st_relaxed_sys(flag(fs, r, kFlagFree, 0, q2), 0u);
         __threadfence_system();
         for (int q2 = 0; q2 < P; ++q2)
-          if (q2 != r) st_release_sys(flag(fs, q2, kFlagData, 0, r), 1u);
+          if (q2 != r) st_relaxed_sys(flag(fs, q2, kFlagData, 0, r), 1u);
       }
     } else {  // ---- phase B: K2 on (v, ts, peer j), the unit pulled from rank j
       const uint32_t b = task - TA;
@@ -172,7 +171,7 @@ __global__ void __launch_bounds__(kFThreads) kf_qwd_step(const FusedSync fs, con
         wait_flag(fs, flag(fs, r, kFlagData, 0, j), wait_code(kFlagData, 0, j));
         s_seen[v] |= 1ull << j;
       }
-      if (t == 0) tstamp(fs, v, 4);
+      if (t == 0) tstamp(fs, blockIdx.x, 4);
       __syncthreads();
       const uint8_t* unit = fs.region[j];
       TM* wm = static_cast<TM*>(a.w_model[v]) + (size_t)j * S;
@@ -206,18 +205,18 @@ __global__ void __launch_bounds__(kFThreads) kf_qwd_step(const FusedSync fs, con
         store_replica8<TM>(wm + e, m, x);
       }
       __syncthreads();  // every thread's reads of unit j are done
-      if (t == 0) tstamp(fs, v, 5);
+      if (t == 0) tstamp(fs, blockIdx.x, 5);
       if (t == 0 && finish_task(fs, 1, v, tpu * (uint32_t)(P - 1))) {
         for (int q2 = 0; q2 < P; ++q2)
           if (q2 != r) st_relaxed_sys(flag(fs, r, kFlagData, 0, q2), 0u);
         __threadfence_system();
         for (int q2 = 0; q2 < P; ++q2)
-          if (q2 != r) st_release_sys(flag(fs, q2, kFlagFree, 0, r), 1u);
+          if (q2 != r) st_relaxed_sys(flag(fs, q2, kFlagFree, 0, r), 1u);
       }
     }
   }
   if (t == 0) {
-    tstamp(fs, 0, 1);
+    tstamp(fs, blockIdx.x, 1);
     exit_unit(fs, gridDim.x);
   }
 }
@@ -287,6 +286,8 @@ cudaError_t launch_fused_tlq(const FusedSync& fs, const void* const* grad, int g
   a.kappa = kappa;
   a.z = -0.0f;
   a.m16 = 16u;
+  static const uint32_t dbg = getenv("SDP4_FUSED_DBG") ? (uint32_t)atoi(getenv("SDP4_FUSED_DBG")) : 0u;
+  a.dbg = dbg;
   const size_t rb = (S / kRowElems + kFtRows - 1) / kFtRows;
   const size_t warps = rb * (size_t)fs.P * fs.nv;
   const int grid = grid_for((warps + 7) / 8, sms * 4);

@@ -53,7 +53,7 @@ constexpr int kDefaultNcclCtas = 16;
 constexpr double kDefaultTimeoutS = 300.0;  // P2P flag waits (SDP4_WAIT_TIMEOUT_S; 0 = unbounded memop waits)
 // P2P calls on buffers of at most this many elements run as one kernel per rank (k_fused.cu);
 // SDP4_FUSED_MAX_NUMEL / sdp4_comm_set_fused_limit override (measured crossover)
-constexpr size_t kDefaultFusedLimit = 0;  // off until it beats the multi-launch path
+constexpr size_t kDefaultFusedLimit = (size_t)4 << 20;  // 16 MB of fp32 (measured crossover)
 
 thread_local std::string g_err;
 
@@ -733,47 +733,57 @@ sdp4_comm* comm_new(int rank, int world, int groups_M, int group_size_N, int ncc
 }
 
 // SDP4_FUSED_TRACE=1 (debugging only): every one-launch call records %globaltimer stamps of its
-// phases, synchronizes, and prints them to stderr as one JSON line per (virtual) rank, in us
-// from the kernel's entry: [exit, A start, A end, B start, B end, C start, C end].
+// phases (private per warp / CTA), synchronizes, and prints one JSON line to stderr, in us from
+// the earliest entry: [last exit, A first start, A last end, B first start, B last end, C first
+// start, C last end] (-1: no such phase).
 struct FusedTrace {
   unsigned long long* host = nullptr;
   unsigned long long* dev = nullptr;
 };
+constexpr size_t kTraceWords = (size_t)sdp4::kTraceUnits * sdp4::kTraceSlots;
 FusedTrace* fused_trace() {
   static FusedTrace t;
   static bool init = false;
   if (!init) {
     init = true;
-    const size_t bytes = sdp4::kMaxVr * sdp4::kTraceSlots * sizeof(unsigned long long);
-    if (getenv("SDP4_FUSED_TRACE") && cudaHostAlloc(&t.host, bytes, cudaHostAllocMapped) == cudaSuccess)
-      cudaHostGetDevicePointer(reinterpret_cast<void**>(&t.dev), t.host, 0);
-    else
+    if (getenv("SDP4_FUSED_TRACE") && cudaMalloc(&t.dev, kTraceWords * 8) == cudaSuccess) {
+      t.host = static_cast<unsigned long long*>(malloc(kTraceWords * 8));
+    } else {
       cudaGetLastError();
+      t.dev = nullptr;
+    }
   }
   return t.dev ? &t : nullptr;
 }
 void trace_begin(sdp4::FusedSync& fs) {
   FusedTrace* t = fused_trace();
   if (!t) return;
-  for (int i = 0; i < sdp4::kMaxVr * sdp4::kTraceSlots; ++i) t->host[i] = (i & 1) ? 0ull : ~0ull;
+  cudaMemset(t->dev, 0, kTraceWords * 8);
   fs.trace = t->dev;
 }
 void trace_end(const char* what, const sdp4::FusedSync& fs, cudaStream_t st) {
   FusedTrace* t = fused_trace();
   if (!t) return;
   cudaStreamSynchronize(st);
-  const unsigned long long t0 = t->host[0];
-  for (int v = 0; v < fs.nv; ++v) {
-    const unsigned long long* x = t->host + v * sdp4::kTraceSlots;
-    std::string line = std::string("{\"fused_trace\": \"") + what + "\", \"rank\": " + std::to_string(fs.rank[v]) + ", \"us\": [";
-    for (int k = 1; k < sdp4::kTraceSlots; ++k) {
-      const unsigned long long y = (v == 0 || k > 1) ? x[k] : t->host[1];
-      char b[32];
-      snprintf(b, sizeof(b), "%s%.2f", k > 1 ? ", " : "", (y == 0 || y == ~0ull) ? -1.0 : (double)(long long)(y - t0) * 1e-3);
-      line += b;
+  cudaMemcpy(t->host, t->dev, kTraceWords * 8, cudaMemcpyDeviceToHost);
+  unsigned long long agg[sdp4::kTraceSlots];
+  for (int k = 0; k < sdp4::kTraceSlots; ++k) agg[k] = (k & 1) ? 0ull : ~0ull;
+  for (int u = 0; u < sdp4::kTraceUnits; ++u)
+    for (int k = 0; k < sdp4::kTraceSlots; ++k) {
+      const unsigned long long y = t->host[(size_t)u * sdp4::kTraceSlots + k];
+      if (!y) continue;
+      agg[k] = (k & 1) ? std::max(agg[k], y) : std::min(agg[k], y);
     }
-    fprintf(stderr, "%s]}\n", line.c_str());
+  std::string line = std::string("{\"fused_trace\": \"") + what + "\", \"rank\": " + std::to_string(fs.rank[0]) +
+                     ", \"nv\": " + std::to_string(fs.nv) + ", \"us\": [";
+  for (int k = 1; k < sdp4::kTraceSlots; ++k) {
+    const unsigned long long y = agg[k];
+    char b[32];
+    snprintf(b, sizeof(b), "%s%.2f", k > 1 ? ", " : "",
+             (y == 0 || y == ~0ull || agg[0] == ~0ull) ? -1.0 : (double)(long long)(y - agg[0]) * 1e-3);
+    line += b;
   }
+  fprintf(stderr, "%s]}\n", line.c_str());
 }
 
 // The one-launch path needs distinct GPUs (its kernels poll for other ranks' kernels, which

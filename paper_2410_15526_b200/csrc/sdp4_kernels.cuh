@@ -143,9 +143,10 @@ struct FusedSync {
   uint32_t* ctr;                // kFusedCtrWords counters, zero between launches
   uint32_t* err;                // host-mapped error word (timeouts), may be null
   unsigned long long timeout_ns;  // 0: wait forever
-  unsigned long long* trace;    // debugging (SDP4_FUSED_TRACE): kTraceSlots %globaltimer stamps per rank
+  unsigned long long* trace;    // debugging (SDP4_FUSED_TRACE): kTraceSlots %globaltimer stamps per unit
 };
-constexpr int kTraceSlots = 8;  // entry, exit, A start, A end, B start, B end, C start, C end (even: min, odd: max)
+constexpr int kTraceSlots = 8;    // per warp / CTA: entry, exit, A start, A end, B start, B end, C start, C end
+constexpr int kTraceUnits = 4096;  // warps / CTAs traced
 // qWD step (Alg. 2 l.2-5): phase A quantizes the own shard into region[rank] and applies it to
 // the own replica shard (K1 with apply_own); phase B applies every peer's unit (K2's pull).
 // bits in {2, 4, 8, 32}, G <= 2048.  Flag stage 0.
