@@ -149,9 +149,9 @@ sdp4_status sdp4_comm_set_intra_pull(sdp4_comm_t comm, int num, int den);
  * path), so a call costs one launch instead of two or three stream-ordered hand-offs (Alg. 2
  * l.2-5; Alg. 3, P:368-379 -- the arithmetic and results are identical, R16).
  * Applies when the ranks are on distinct GPUs, with one chunk, and for TLq-HS when
- * bits_intra and bits_inter are in {4, 8}; other calls take the multi-launch path.  Default
- * 4 Mi elements (16 MB of fp32, the measured crossover; SDP4_FUSED_MAX_NUMEL overrides); 0
- * disables it. */
+ * bits_intra and bits_inter are in {4, 8}; other calls take the multi-launch path.  Defaults
+ * (the measured crossovers): 8 Mi elements for the qWD step, 16 Mi for TLq-HS; a value set
+ * here (or SDP4_FUSED_MAX_NUMEL) applies to both; 0 disables the path. */
 sdp4_status sdp4_comm_set_fused_limit(sdp4_comm_t comm, size_t numel);
 
 /* Host, collective (every rank calls it).  Waits for this rank's work, then -- if symmetric

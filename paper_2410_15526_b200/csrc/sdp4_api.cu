@@ -53,7 +53,8 @@ constexpr int kDefaultNcclCtas = 16;
 constexpr double kDefaultTimeoutS = 300.0;  // P2P flag waits (SDP4_WAIT_TIMEOUT_S; 0 = unbounded memop waits)
 // P2P calls on buffers of at most this many elements run as one kernel per rank (k_fused.cu);
 // SDP4_FUSED_MAX_NUMEL / sdp4_comm_set_fused_limit override (measured crossover)
-constexpr size_t kDefaultFusedLimit = (size_t)4 << 20;  // 16 MB of fp32 (measured crossover)
+constexpr size_t kDefaultFusedLimit = (size_t)8 << 20;      // qWD: 32 MB of fp32 (measured crossover,
+constexpr size_t kDefaultFusedLimitTlq = (size_t)16 << 20;  // TLq-HS: 64 MB           DESIGN.md sec. 9)
 
 thread_local std::string g_err;
 
@@ -180,7 +181,8 @@ struct sdp4_comm {
   } qwd_pending;
   uint64_t tlq_layout[6] = {0, 0, 0, 0, 0, 0};  // layout of the last P2P TLq-HS call (drain on change)
   bool tlq_layout_valid = false;
-  size_t fused_limit = 0;             // P2P calls with numel <= this run as one kernel (k_fused.cu)
+  size_t fused_limit = 0;             // P2P qWD steps with numel <= this run as one kernel (k_fused.cu)
+  size_t fused_limit_tlq = 0;         // P2P TLq-HS calls likewise
   uint32_t* fused_ctr = nullptr;      // counter blocks of the one-launch kernels (qWD, TLq-HS)
   unsigned long long timeout_ns = 0;  // > 0: flag waits are polling kernels with this deadline
   uint32_t* err_host = nullptr;       // host-mapped error word written by a timed-out wait
@@ -722,7 +724,8 @@ sdp4_comm* comm_new(int rank, int world, int groups_M, int group_size_N, int ncc
     if (cudaMalloc(&c->fused_ctr, 2 * sdp4::kFusedCtrWords * sizeof(uint32_t)) == cudaSuccess &&
         cudaMemset(c->fused_ctr, 0, 2 * sdp4::kFusedCtrWords * sizeof(uint32_t)) == cudaSuccess) {
       c->fused_limit = kDefaultFusedLimit;
-      if (const char* e = getenv("SDP4_FUSED_MAX_NUMEL")) c->fused_limit = (size_t)strtoull(e, nullptr, 10);
+      c->fused_limit_tlq = kDefaultFusedLimitTlq;
+      if (const char* e = getenv("SDP4_FUSED_MAX_NUMEL")) c->fused_limit = c->fused_limit_tlq = strtoull(e, nullptr, 10);
     } else {
       cudaGetLastError();
       if (c->fused_ctr) cudaFree(c->fused_ctr);
@@ -788,8 +791,9 @@ void trace_end(const char* what, const sdp4::FusedSync& fs, cudaStream_t st) {
 
 // The one-launch path needs distinct GPUs (its kernels poll for other ranks' kernels, which
 // processes sharing one GPU cannot guarantee to run concurrently).
-bool use_fused(const sdp4_comm* c, size_t numel) {
-  return c->transport == kTransportP2P && c->world > 1 && !c->shared_gpu && c->fused_ctr && numel <= c->fused_limit;
+bool use_fused(const sdp4_comm* c, size_t numel, bool tlq) {
+  return c->transport == kTransportP2P && c->world > 1 && !c->shared_gpu && c->fused_ctr &&
+         numel <= (tlq ? c->fused_limit_tlq : c->fused_limit);
 }
 
 void comm_free(sdp4_comm* c) {
@@ -936,7 +940,7 @@ sdp4_status sdp4_comm_set_intra_pull(sdp4_comm_t c, int num, int den) {
 
 sdp4_status sdp4_comm_set_fused_limit(sdp4_comm_t c, size_t numel) {
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
-  c->fused_limit = numel;
+  c->fused_limit = c->fused_limit_tlq = numel;
   return SDP4_OK;
 }
 
@@ -1158,7 +1162,7 @@ sdp4_status sdp4_qwd_step(sdp4_comm_t c, const float* w_main_shard, void* w_mode
                           size_t numel, int bits, int group, sdp4_round rnd, uint64_t seed, void* workspace,
                           size_t workspace_bytes, void* stream) {
   NvtxRange nvtx_("sdp4_qwd_step");
-  if (c && use_fused(c, numel)) {  // small message: the whole step as one kernel per rank
+  if (c && use_fused(c, numel, false)) {  // small message: the whole step as one kernel per rank
     g_err.clear();
     if (!valid_round(rnd)) return fail(SDP4_EINVAL, "bad rounding mode %d", (int)rnd);
     if (!valid_wbits(bits)) return fail(SDP4_EINVAL, "bits %d not in {2, 4, 8, 32}", bits);
@@ -1256,7 +1260,7 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     // NVLink-bound K3 of chunk k+1 (the overlap of P:344).  Symmetric region, per chunk:
     // [intra receive: N blocks][inter receive: M units][outbox: N blocks].
     // small messages: the whole reduce-scatter as one kernel per rank (push-only layout)
-    const bool fused = C == 1 && use_fused(c, numel) && sdp4::fused_tlq_supported(bits_intra, bits_inter, b);
+    const bool fused = C == 1 && use_fused(c, numel, true) && sdp4::fused_tlq_supported(bits_intra, bits_inter, b);
     const int pnum = fused ? 0 : c->pull_num >= 0 ? c->pull_num : (N <= 2 ? 0 : 1);  // auto split
     const int pden = c->pull_num >= 0 ? c->pull_den : 2;
     const bool pulling = N > 1 && pnum > 0;

@@ -43,20 +43,26 @@ def main():
         comm.set_fused_limit(a.fused_limit)
     P, G, b = world, 128, 64
 
-    def timed(fn):
+    def timed(fn, iters=None):
+        # median of three timed runs (each: max over ranks of the per-call device time), the
+        # same method for libsdp4 and NCCL; small messages run more calls per run
+        iters = iters or a.iters
         for _ in range(3):
             fn()
-        dist.barrier(device_ids=[local])
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(a.iters):
-            fn()
-        e1.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / a.iters], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        runs = []
+        for _ in range(3):
+            dist.barrier(device_ids=[local])
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(iters):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / iters], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            runs.append(float(t.item()))
+        return sorted(runs)[1]
 
     rows = []
     for mb in [int(x) for x in a.sizes_mb.split(",")]:
@@ -70,14 +76,15 @@ def main():
         ws_t = torch.empty(comm.tlq_workspace_bytes(D, 8, 4, G), dtype=torch.uint8, device=dev)
         fq = lambda: comm.qwd_step(w_main, w_model, ws_q, 4, G)  # noqa: E731
         ft = lambda: comm.tlq_hs_reduce_scatter(grad, out, ws_t, 8, 4, G, b, True)  # noqa: E731
-        t_q = timed(fq)
-        t_t = timed(ft)
+        it = max(a.iters, 50) if mb <= 64 else a.iters
+        t_q = timed(fq, it)
+        t_t = timed(ft, it)
         big = torch.empty(D, dtype=torch.float32, device=dev)
         shard = torch.empty(S, dtype=torch.float32, device=dev)
         fag = lambda: dist.all_gather_into_tensor(big, shard)  # noqa: E731
         frs = lambda: dist.reduce_scatter_tensor(out, grad, op=dist.ReduceOp.AVG)  # noqa: E731
-        t_ag = timed(fag)
-        t_rs = timed(frs)
+        t_ag = timed(fag, it)
+        t_rs = timed(frs, it)
         row = {"mbytes": mb, "D": D, "qwd_ms": round(t_q, 4), "nccl_all_gather_ms": round(t_ag, 4),
                "ag_speedup": round(t_ag / t_q, 3), "tlq_ms": round(t_t, 4), "nccl_reduce_scatter_ms": round(t_rs, 4),
                "rs_speedup": round(t_rs / t_t, 3)}
@@ -92,7 +99,7 @@ def main():
                 with torch.cuda.graph(g, stream=side):
                     fn()
                 torch.cuda.synchronize()
-                gs[name] = timed(g.replay)
+                gs[name] = timed(g.replay, it)
                 del g
             row.update({"graph_qwd_ms": round(gs["qwd"], 4), "graph_ag_speedup": round(t_ag / gs["qwd"], 3),
                         "graph_tlq_ms": round(gs["tlq"], 4), "graph_rs_speedup": round(t_rs / gs["tlq"], 3)})
