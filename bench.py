@@ -133,6 +133,8 @@ def kernel_bytes(name, D, S, P, M, N, a):
         return S * (4 + m) + wire(S, a.bits_w, a.qwd_group) + own * S * m
     if name.startswith("K2"):
         return wire(D - own * S, a.bits_w, a.qwd_group) + 2 * m * (D - own * S)
+    if name.startswith("K345"):                 # world 1: K3 -> K4 -> K5 in one kernel (k_local.cu)
+        return D * g + 4 * S
     if name.startswith("K3"):
         return D * g + wire(D, a.bits_intra, a.group)
     if name.startswith("K4"):
@@ -460,16 +462,48 @@ def run_sdp4(a, rank, world, local_rank):
         t_tlq32 = timed(lambda: comm.tlq_hs_reduce_scatter(g32, out, ws_t, a.bits_intra, a.bits_inter, a.group,
                                                            a.hadamard, True), a.steps)
         a32 = argparse.Namespace(**dict(vars(a), grad_dtype="fp32"))
-        k3 = {n: v for n, v in prof32.items() if n.startswith("K3")}
-        k3_ms = sum(v[0] for v in k3.values()) / max(1, sum(v[1] for v in k3.values()))
-        k3_bytes = kernel_bytes("K3", D, S, P, M, N, a32)
+        # the kernel that reads the gradient: K3, or at world 1 the fused K345
+        tk = "K345_tlq_local" if "K345_tlq_local" in prof32 else "K3_tlq_had_quant"
+        k_t, k_c = prof32.get(tk, (0.0, 0))
+        k_ms = k_t / max(1, k_c)
+        k_bytes = kernel_bytes(tk, D, S, P, M, N, a32)
         variants = {"fp32_grad": {"ms_per_step": round(ms32, 4),
                                   "value": round(P * D * (4 + 4) / (ms32 * 1e-3) / 1e9, 2), "unit": "GB/s",
                                   "tlq_hs_reduce_scatter_ms": round(t_tlq32, 4),
-                                  "K3_avg_ms": round(k3_ms, 4),
-                                  "K3_gbs": round(k3_bytes / (k3_ms * 1e-3) / 1e9, 1) if k3_ms else None,
-                                  "K3_frac_of_peak": round(k3_bytes / (k3_ms * 1e-3) / 1e9 / peak, 4) if k3_ms else None}}
+                                  "grad_kernel": tk, "grad_kernel_avg_ms": round(k_ms, 4),
+                                  "grad_kernel_gbs": round(k_bytes / (k_ms * 1e-3) / 1e9, 1) if k_ms else None,
+                                  "grad_kernel_frac_of_peak":
+                                      round(k_bytes / (k_ms * 1e-3) / 1e9 / peak, 4) if k_ms else None}}
         del g32
+    if not a.no_variants and P == 1 and "K345_tlq_local" in prof:
+        # the same step through the three kernels K3 -> K4 -> K5 (what every rank of a P > 1 job
+        # runs), with each kernel's roofline
+        comm.set_local_fusion(False)
+        for _ in range(2):
+            qwd(w_main)
+            comm.tlq_hs_reduce_scatter(grad, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
+
+        def step3():
+            qwd(w_main)
+            comm.tlq_hs_reduce_scatter(grad, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
+        ms3 = timed(step3, a.steps)
+        comm.profile_enable(True)
+        comm.profile_read()
+        timed(step3, a.steps)
+        prof3 = comm.profile_read()
+        comm.profile_enable(False)
+        comm.set_local_fusion(True)
+        k3k = {}
+        for n, (tt, cc) in prof3.items():
+            if n.startswith("K3") or n.startswith("K4") or n.startswith("K5"):
+                avg = tt / max(1, cc)
+                kb = kernel_bytes(n, D, S, P, M, N, a)
+                k3k[n] = {"avg_ms": round(avg, 4), "gbs": round(kb / (avg * 1e-3) / 1e9, 1),
+                          "frac_of_peak": round(kb / (avg * 1e-3) / 1e9 / peak, 4)}
+        variants = dict(variants or {})
+        variants["three_kernel_tlq"] = {"ms_per_step": round(ms3, 4),
+                                        "value": round(P * pre_bytes_rank / (ms3 * 1e-3) / 1e9, 2),
+                                        "unit": "GB/s", "kernels": k3k}
 
     # ablation (NEXT-3): TLq-HS with the Hadamard transforms as separate passes ("SDP4Bit (HS
     # w/o fused)") -- K3 identity codec forward pass, the b = 0 reduce-scatter, K5

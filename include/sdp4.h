@@ -154,6 +154,13 @@ sdp4_status sdp4_comm_set_intra_pull(sdp4_comm_t comm, int num, int den);
  * here (or SDP4_FUSED_MAX_NUMEL) applies to both; 0 disables the path. */
 sdp4_status sdp4_comm_set_fused_limit(sdp4_comm_t comm, size_t numel);
 
+/* Host.  World size 1: sdp4_tlq_hs_reduce_scatter with bits 8 / 4 runs K3 -> K4 -> K5 as ONE
+ * kernel (both all-to-alls of Alg. 3 are the identity with one rank, so the 8- and 4-bit
+ * codes never leave the registers: 6 instead of ~9 bytes of HBM traffic per element, same
+ * operations, bit-identical results).  enable = 0 selects the three-kernel path (measurement;
+ * default 1). */
+sdp4_status sdp4_comm_set_local_fusion(sdp4_comm_t comm, int enable);
+
 /* Host, collective (every rank calls it).  Waits for this rank's work, then -- if symmetric
  * buffers were allocated -- barriers with the peers (they may still be pulling from this
  * rank's buffers) before unmapping and freeing them; destroys the NCCL communicators and

@@ -183,6 +183,7 @@ struct sdp4_comm {
   bool tlq_layout_valid = false;
   size_t fused_limit = 0;             // P2P qWD steps with numel <= this run as one kernel (k_fused.cu)
   size_t fused_limit_tlq = 0;         // P2P TLq-HS calls likewise
+  bool local_fusion = true;           // world 1: TLq-HS as one kernel (k_local.cu)
   uint32_t* fused_ctr = nullptr;      // counter blocks of the one-launch kernels (qWD, TLq-HS)
   unsigned long long timeout_ns = 0;  // > 0: flag waits are polling kernels with this deadline
   uint32_t* err_host = nullptr;       // host-mapped error word written by a timed-out wait
@@ -944,6 +945,12 @@ sdp4_status sdp4_comm_set_fused_limit(sdp4_comm_t c, size_t numel) {
   return SDP4_OK;
 }
 
+sdp4_status sdp4_comm_set_local_fusion(sdp4_comm_t c, int enable) {
+  if (!c) return fail(SDP4_EINVAL, "comm is NULL");
+  c->local_fusion = enable != 0;
+  return SDP4_OK;
+}
+
 sdp4_status sdp4_comm_set_transport(sdp4_comm_t c, int transport) {
   if (!c) return fail(SDP4_EINVAL, "comm is NULL");
   if (transport != kTransportNccl && transport != kTransportP2P) return fail(SDP4_EINVAL, "bad transport %d", transport);
@@ -1400,6 +1407,12 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     }
     if (C > 1) c->link(c->side, st);
     return SDP4_OK;
+  }
+  if (P == 1 && c->local_fusion && C == 1 && bits_intra == 8 && bits_inter == 4) {
+    // one rank: both all-to-alls are the identity -- K3, K4 and K5 as one kernel (k_local.cu)
+    return launch(c, "K345_tlq_local", st, [&] {
+      return sdp4::launch_tlq_local(grad, grad_dtype, S, group, b, cb, kappa, sr, key8, key4, out_shard, sms, st);
+    });
   }
   std::vector<TlqRegions> reg;
   size_t base = 0;

@@ -161,6 +161,11 @@ cudaError_t launch_fused_tlq(const FusedSync& fs, const void* const* grad, int g
                              int bits_inter, size_t w8, size_t w4, int sr_on, const uint32_t* key8,
                              const uint32_t* key4, int sms, cudaStream_t st);
 bool fused_tlq_supported(int bits_intra, int bits_inter, int b);
+
+// TLq-HS at world size 1 (M = N = 1) as one kernel, K3 -> K4 -> K5 fused in registers
+// (k_local.cu): out[S] from grad[S], bits 8 (intra) / 4 (inter), any b.
+cudaError_t launch_tlq_local(const void* grad, int grad_dtype, size_t S, int G, int b, float cb, float kappa,
+                             int sr_on, uint32_t key8, uint32_t key4, float* out, int sms, cudaStream_t st);
 // Fill n words with v (flag initialization of emulated symmetric buffers).
 cudaError_t launch_fill32(uint32_t* p, size_t n, uint32_t v, cudaStream_t st);
 

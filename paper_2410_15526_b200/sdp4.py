@@ -47,6 +47,7 @@ SIGNATURES = {
     "sdp4_comm_transport": (_ci, [_vp]),
     "sdp4_comm_set_intra_pull": (_ci, [_vp, _ci, _ci]),
     "sdp4_comm_set_fused_limit": (_ci, [_vp, _c_size]),
+    "sdp4_comm_set_local_fusion": (_ci, [_vp, _ci]),
     "sdp4_wire_unit_bytes": (_c_size, [_c_size, _ci, _ci]),
     "sdp4_qwd_workspace_bytes": (_c_size, [_ci, _c_size, _ci, _ci]),
     "sdp4_tlq_workspace_bytes": (_c_size, [_ci, _ci, _c_size, _ci, _ci, _ci]),
@@ -292,6 +293,11 @@ class Comm:
         """P2P calls on at most `numel` elements run as one kernel per rank (0: never); see
         sdp4_comm_set_fused_limit."""
         _check(lib().sdp4_comm_set_fused_limit(self._h, numel))
+
+    def set_local_fusion(self, enable: bool):
+        """World size 1: TLq-HS (8/4 bits) as one kernel (default) or K3 + K4 + K5; see
+        sdp4_comm_set_local_fusion."""
+        _check(lib().sdp4_comm_set_local_fusion(self._h, int(bool(enable))))
 
     @property
     def transport(self) -> str:

@@ -46,10 +46,17 @@ def run():
     ws_q = torch.empty(comm.qwd_workspace_bytes(D, BITS_W, GW), dtype=torch.uint8, device=dev)
     ws_t = torch.empty(comm.tlq_workspace_bytes(D, BI, BE, G), dtype=torch.uint8, device=dev)
     out = torch.empty(D, dtype=torch.float32, device=dev)
-    comm.qwd_step(w_main, w_model, ws_q, BITS_W, GW)   # the call bench.py times
-    comm.tlq_hs_reduce_scatter(grad, out, ws_t, BI, BE, G, B, True)
+    comm.qwd_step(w_main, w_model, ws_q, BITS_W, GW)   # the calls bench.py times: at world 1
+    comm.tlq_hs_reduce_scatter(grad, out, ws_t, BI, BE, G, B, True)   # TLq-HS is one kernel (K345)
+    # the three-kernel path (K3 -> K4 -> K5, what each rank of a P > 1 job runs): its wire
+    # units land in the workspace and are checked too
+    out3 = torch.empty(D, dtype=torch.float32, device=dev)
+    comm.set_local_fusion(False)
+    comm.tlq_hs_reduce_scatter(grad, out3, ws_t, BI, BE, G, B, True)
+    comm.set_local_fusion(True)
     torch.cuda.synchronize()
-    yield dict(D=D, w_model0=wm0, w_model=w_model, w_main=w_main, grad=grad, out=out, ws_q=ws_q, ws_t=ws_t)
+    yield dict(D=D, w_model0=wm0, w_model=w_model, w_main=w_main, grad=grad, out=out, out3=out3, ws_q=ws_q,
+               ws_t=ws_t)
     comm.close()
 
 
@@ -87,8 +94,9 @@ def test_fullsize_tlq_hs_windows(run):
         cb, gsc = unit_window(run["ws_t"], o_inter, D, BE, G, s, WIN)
         assert np.array_equal(cb, oracle.pack_codes(c4, BE)), f"K4 codes differ in window {s}"
         assert np.array_equal(gsc.view(np.uint32), s4.view(np.uint32)), f"K4 scales differ in window {s}"
-        got = run["out"][s:s + WIN].cpu().numpy()
-        assert np.array_equal(got.view(np.uint32), tr.out[0].view(np.uint32)), f"output differs in window {s}"
+        for key in ("out", "out3"):   # the fused kernel (bench) and the three kernels
+            got = run[key][s:s + WIN].cpu().numpy()
+            assert np.array_equal(got.view(np.uint32), tr.out[0].view(np.uint32)), f"{key} differs in window {s}"
 
 
 def test_fullsize_output_sanity(run):

@@ -21,6 +21,7 @@ def comm():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     c = Comm()
+    c.set_local_fusion(False)   # the three kernels, whose wire units these tests inspect
     yield c
     c.close()
 
@@ -281,3 +282,37 @@ def test_qwd_step_launches(comm):
     comm.qwd_step(w_main, w_model, ws)
     torch.cuda.synchronize()
     assert comm.launch_count() - n0 == 1
+
+
+# ------------------------------------------------------------------ world-1 fused TLq-HS
+LOCAL_CASES = [(G, b, dt, seed) for G in (32, 128, 2048) for b in (0, 2, 64, 256) if b <= G
+               for dt in (torch.bfloat16, torch.float32) for seed in (None, 77)]
+
+
+@pytest.mark.parametrize("G,b,dt,seed", LOCAL_CASES)
+def test_tlq_local_fused(G, b, dt, seed):
+    """At world 1 TLq-HS 8/4 is one kernel (K3 -> K4 -> K5 in registers, k_local.cu): its
+    output equals the oracle's and the three-kernel path's bit for bit -- several tiles, a
+    ragged tail, edge-case groups, nearest and stochastic rounding."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    D = 16384 * 3 + max(G, 64) * 7
+    D -= D % max(G, 64)
+    g = synth.gradient(D, seed=91, dtype=dt)
+    e = synth.edge_case_groups(G)[:D].to(dt)
+    g[D - e.numel():] = e
+    c = Comm()
+    out1 = torch.empty(D, dtype=torch.float32, device="cuda")
+    out3 = torch.empty(D, dtype=torch.float32, device="cuda")
+    ws = torch.zeros(c.tlq_workspace_bytes(D, 8, 4, G), dtype=torch.uint8, device="cuda")
+    c.launch_count(reset=True)
+    c.tlq_hs_reduce_scatter(g.cuda(), out1, ws, 8, 4, G, b, True, seed=seed)
+    torch.cuda.synchronize()
+    assert c.launch_count() == 1, "world-1 TLq-HS 8/4 should be one kernel"
+    c.set_local_fusion(False)
+    c.tlq_hs_reduce_scatter(g.cuda(), out3, ws, 8, 4, G, b, True, seed=seed)
+    torch.cuda.synchronize()
+    c.close()
+    want = oracle_tlq(g, 8, 4, G, b, True, seed).out[0]
+    assert f32_equal(out1.cpu().numpy(), want), "fused world-1 TLq-HS differs from the oracle"
+    assert f32_equal(out3.cpu().numpy(), want), "three-kernel TLq-HS differs from the oracle"
