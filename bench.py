@@ -135,6 +135,8 @@ def kernel_bytes(name, D, S, P, M, N, a):
         return wire(D - own * S, a.bits_w, a.qwd_group) + 2 * m * (D - own * S)
     if name.startswith("K345"):                 # world 1: K3 -> K4 -> K5 in one kernel (k_local.cu)
         return D * g + 4 * S
+    if name.startswith("K34"):                  # N = 1: K3 + K4 in one kernel (k_local34.cu)
+        return D * g + wire(D, a.bits_inter, a.group)
     if name.startswith("K3"):
         return D * g + wire(D, a.bits_intra, a.group)
     if name.startswith("K4"):
@@ -161,6 +163,8 @@ def kernel_nvlink_bytes(name, D, S, P, M, N, a, transport):
     num, den = [int(x) for x in (a.intra_pull or ("0/1" if N <= 2 else "1/2")).split("/")]   # library default
     f = num / den if N > 1 else 0.0                      # share of intra tiles K4 pulls
     intra = (N - 1) * M * wire(S, a.bits_intra, a.group)
+    if name.startswith("K34"):                           # N = 1: the inter units it pushes
+        return (M - 1) * wire(S, a.bits_inter, a.group)
     if name.startswith("K3"):                            # pushed intra tiles (egress)
         return (1 - f) * intra
     if name.startswith("K4"):                            # max(pulled intra ingress, inter egress)

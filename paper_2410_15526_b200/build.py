@@ -13,7 +13,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsdp4.so")
 SOURCES = ["sdp4_api.cu", "k_weights.cu", "k_had_quant.cu", "k_reduce.cu", "k_final.cu", "k_fused.cu",
-           "k_fused_tlq8.cu", "k_fused_tlq4.cu", "k_local.cu"]
+           "k_fused_tlq8.cu", "k_fused_tlq4.cu", "k_local.cu",
+           "k_local34.cu"]
 HEADERS = ["sdp4_kernels.cuh", "sdp4_device.cuh", "k_fused.cuh", "k_fused_tlq.cuh"]
 
 

@@ -1340,6 +1340,38 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
       trace_end("tlq", fs, st);
       return s;
     }
+    if (N == 1 && M > 1 && C == 1 && c->local_fusion && bits_intra == 8 && bits_inter == 4) {
+      // one GPU per group: the intra all-to-all is the identity, so K3 and K4 are one kernel
+      // (k_local34.cu) that pushes each 4-bit unit straight to its node's inter slot; then K5
+      const size_t w8 = unit_bytes(S, bits_intra, group), w4 = unit_bytes(S, bits_inter, group);
+      const size_t intra_bytes = (size_t)N * M * w8;
+      std::vector<Wt> wf, wd;
+      std::vector<Sig> gd, gf;
+      for (int q : node_ranks) {
+        wf.push_back({kFree, 2, q});  // q's K5 of the previous call is done with my push
+        gd.push_back({q, kData, 2});
+        wd.push_back({kData, 2, q});
+        gf.push_back({q, kFree, 2});
+      }
+      uint8_t* units[sdp4::kMaxDests];
+      for (int mp = 0; mp < M; ++mp) units[mp] = sym_region(c->sym_tlq, mp) + intra_bytes + (size_t)m * w4;
+      const uint64_t remote = (~0ull >> (64 - M)) & ~(1ull << m);
+      if ((s = wait_flags(c, st, c->sym_tlq, wf, "wait_tlq_free")) != SDP4_OK) return s;
+      s = launch(c, "K34_tlq_q84", st, [&] {
+        return sdp4::launch_tlq_q84(grad, S, grad_dtype, S, M, group, b, cb, units, remote, sr, key8, key4,
+                                    c->sm_count, st);
+      });
+      if (s != SDP4_OK) return s;
+      if ((s = raise_flags(c, st, c->sym_tlq, gd)) != SDP4_OK) return s;
+      if ((s = wait_flags(c, st, c->sym_tlq, wd, "wait_tlq_inter")) != SDP4_OK) return s;
+      uint8_t* my = sym_region(c->sym_tlq, c->rank);
+      s = launch(c, "K5_tlq_dq_reduce_had", st, [&] {
+        return sdp4::launch_tlq_dq_reduce_had(my + intra_bytes, w4, bits_inter, M, S, group, b, kappa, out_shard,
+                                              c->sm_count, st);
+      });
+      if (s != SDP4_OK) return s;
+      return raise_flags(c, st, c->sym_tlq, gf);
+    }
     if (C > 1) c->link(st, c->side);
     for (int k = 0; k < C; ++k) {
       const Chunk& ch = chunks[k];

@@ -162,6 +162,13 @@ cudaError_t launch_fused_tlq(const FusedSync& fs, const void* const* grad, int g
                              const uint32_t* key4, int sms, cudaStream_t st);
 bool fused_tlq_supported(int bits_intra, int bits_inter, int b);
 
+// TLq-HS with N = 1 (M > 1): K3 + K4 fused (k_local34.cu).  Shard j = m' of the gradient
+// (at grad + j * grad_stride elements) -> its 4-bit unit at units[m'] (slot m of node m''s
+// inter receive region; remote_mask bit m' = peer memory).  bits 8 / 4, any b.
+cudaError_t launch_tlq_q84(const void* grad, size_t grad_stride, int grad_dtype, size_t S, int M, int G, int b,
+                           float cb, uint8_t* const* units, uint64_t remote_mask, int sr_on, uint32_t key8,
+                           uint32_t key4, int sms, cudaStream_t st);
+
 // TLq-HS at world size 1 (M = N = 1) as one kernel, K3 -> K4 -> K5 fused in registers
 // (k_local.cu): out[S] from grad[S], bits 8 (intra) / 4 (inter), any b.
 cudaError_t launch_tlq_local(const void* grad, int grad_dtype, size_t S, int G, int b, float cb, float kappa,
