@@ -692,6 +692,7 @@ sdp4_comm* comm_new(int rank, int world, int groups_M, int group_size_N, int ncc
   c->m = rank / group_size_N;
   c->l = rank % group_size_N;
   c->nccl_ctas = nccl_ctas ? nccl_ctas : kDefaultNcclCtas;
+  if (getenv("SDP4_NO_LOCAL_FUSION")) c->local_fusion = false;  // measurement: K3 -> K4 -> K5 unfused
   cudaGetDevice(&c->device);
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device);
   if (c->nccl_ctas >= c->sm_count) c->nccl_ctas = c->sm_count / 2;

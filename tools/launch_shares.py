@@ -9,7 +9,7 @@ import json
 import sys
 
 KERNELS = ("k1_qwd_quantize", "k2_qwd_apply", "k3_tlq_had_quant", "k4_tlq_dq_reduce_q", "k5_tlq_dq_reduce_had",
-           "k6_ring_hop", "k_wait_flags")
+           "k6_ring_hop", "k_wait_flags", "k_tlq_local", "k_tlq_q84", "kf_qwd_step", "kf_tlq")
 
 
 def main():
@@ -29,8 +29,11 @@ def main():
                "share": round(sum(v[warm:]) / tot, 4)} for n, v in sorted(times.items())}
     if len(sys.argv) > 3:
         d = json.load(open(sys.argv[3]))
+        bench_names = {"K345": "k_tlq_local", "K34": "k_tlq_q84", "KF": None}
         for n, v in d.get("kernels", {}).items():
-            k = next((x for x in KERNELS if x.split("_")[0].upper() == n.split("_")[0]), None)
+            tag = n.split("_")[0]
+            k = bench_names[tag] if tag in bench_names else next(
+                (x for x in KERNELS if x.split("_")[0].upper() == tag), None)
             if k in out:
                 out[k]["bench_share"] = v["share_of_kernel_time"]
                 out[k]["bench_avg_ms"] = v["avg_ms"]
