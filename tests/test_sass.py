@@ -72,3 +72,20 @@ def test_blackwell_async_copy_present(sass):
         assert "STG.E.128" in "\n".join(fns[n]), n
     for n in k3 + k4:   # 1-D bulk copies (K4 ring loads; K3/K4 staged tile stores, local or peer)
         assert "UBLKCP" in "\n".join(fns[n]), n
+
+
+def test_fused_kernels_use_tma(sass):
+    # the world-1 (K345) and N = 1 (K34) fused kernels keep K3's TMA + mbarrier input ring;
+    # K34 bulk-copies its 4-bit tiles (to a peer or locally), K345 writes the fp32 shard with
+    # coalesced 16-byte stores
+    fns = functions(sass)
+    loc = [n for n in fns if "k_tlq_local" in n]
+    q84 = [n for n in fns if "k_tlq_q84" in n]
+    assert loc and q84
+    for n in loc + q84:
+        body = "\n".join(fns[n])
+        assert "UTMALDG" in body and "SYNCS" in body, n
+    for n in q84:
+        assert "UBLKCP" in "\n".join(fns[n]), n
+    for n in loc:
+        assert "STG.E.128" in "\n".join(fns[n]), n
