@@ -176,8 +176,8 @@ __global__ void __launch_bounds__(kFThreads) kf_qwd_step(const FusedSync fs, con
       const uint8_t* unit = fs.region[j];
       TM* wm = static_cast<TM*>(a.w_model[v]) + (size_t)j * S;
       const size_t e = (size_t)ts * kFqTile + t * 8;
+      float x[8];
       if (e < S) {
-        float x[8];
         if constexpr (BITS == 32) {
           const float4 u0 = __ldcg(reinterpret_cast<const float4*>(unit + e * 4));
           const float4 u1 = __ldcg(reinterpret_cast<const float4*>(unit + e * 4 + 16));
@@ -200,12 +200,11 @@ __global__ void __launch_bounds__(kFThreads) kf_qwd_step(const FusedSync fs, con
 #pragma unroll
           for (int i = 0; i < 8; ++i) x[i] = mulz(fv[i], ds, a.z);
         }
-        float m[8];
-        load_replica8<TM>(wm + e, m);
-        store_replica8<TM>(wm + e, m, x);
       }
-      __syncthreads();  // every thread's reads of unit j are done
-      if (t == 0) tstamp(fs, blockIdx.x, 5);
+      // every thread's reads of unit j are done (their values are in x): the last task to get
+      // here frees every peer's unit -- before the replica update, so the fence and raises
+      // overlap it
+      __syncthreads();
       if (t == 0 && finish_task(fs, 1, v, tpu * (uint32_t)(P - 1))) {
         for (int q2 = 0; q2 < P; ++q2)
           if (q2 != r) st_relaxed_sys(flag(fs, r, kFlagData, 0, q2), 0u);
@@ -213,6 +212,13 @@ __global__ void __launch_bounds__(kFThreads) kf_qwd_step(const FusedSync fs, con
         for (int q2 = 0; q2 < P; ++q2)
           if (q2 != r) st_relaxed_sys(flag(fs, q2, kFlagFree, 0, r), 1u);
       }
+      if (e < S) {
+        float m[8];
+        load_replica8<TM>(wm + e, m);
+        store_replica8<TM>(wm + e, m, x);
+      }
+      __syncthreads();  // (the next task's s_task write waits for every thread)
+      if (t == 0) tstamp(fs, blockIdx.x, 5);
     }
   }
   if (t == 0) {

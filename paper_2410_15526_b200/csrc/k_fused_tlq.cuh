@@ -388,10 +388,10 @@ __global__ void __launch_bounds__(kFThreads) kf_tlq(const FusedSync fs, const Ft
           else c_source<BE, false>(unit, sc, (int)row, lg, a.z, acc);
         }
       }
-      c_finish<B>(acc, a.kappa, ot, a.out[v] + (size_t)rb * kFtTask, min((uint32_t)kFtRows, rows - rb * kFtRows),
-                  lane);
-      __syncwarp();  // every lane's reads of the inter slots are done
-      if (lane == 0) tstamp(fs, tunit, 7);
+      // every lane's reads of the inter slots are done (their values are in acc): the last
+      // task to get here frees the slots for the peers' next call -- before the butterfly and
+      // the stores, so the fence and raises overlap the tail of the kernel
+      __syncwarp();
       if (lane == 0 && finish_task(fs, 2, v, TC1)) {
         for (int q2 = 0; q2 < M; ++q2)
           if (q2 * N + l != r) st_relaxed_sys(flag(fs, r, kFlagData, 2, q2 * N + l), 0u);
@@ -399,6 +399,10 @@ __global__ void __launch_bounds__(kFThreads) kf_tlq(const FusedSync fs, const Ft
         for (int q2 = 0; q2 < M; ++q2)
           if (q2 * N + l != r) st_relaxed_sys(flag(fs, q2 * N + l, kFlagFree, 2, r), 1u);
       }
+      c_finish<B>(acc, a.kappa, ot, a.out[v] + (size_t)rb * kFtTask, min((uint32_t)kFtRows, rows - rb * kFtRows),
+                  lane);
+      __syncwarp();
+      if (lane == 0) tstamp(fs, tunit, 7);
     }
   }
   if (lane == 0) {
