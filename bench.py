@@ -303,12 +303,13 @@ def run_sdp4(a, rank, world, local_rank):
     w_main = synth.main_weights(w_model[rank * S:(rank + 1) * S], seed=synth.seed_for(rank, 2), lr=lr)
     grad = synth.gradient(D, seed=synth.seed_for(rank, 3), device=dev, dtype=gdt)
     out = torch.empty(S, dtype=torch.float32, device=dev)
+    local_fused = P == 1 and a.bits_intra == 8 and a.bits_inter == 4   # world 1: K345, no TLq workspace
     if comm.transport == "p2p":   # exchanges through libsdp4's own symmetric buffers
         ws_q = ws_t = None
     else:
         ws_q = torch.empty(comm.qwd_workspace_bytes(D, a.bits_w, a.qwd_group), dtype=torch.uint8, device=dev)
-        ws_t = torch.empty(comm.tlq_workspace_bytes(D, a.bits_intra, a.bits_inter, a.group), dtype=torch.uint8,
-                           device=dev)
+        ws_t = None if local_fused else torch.empty(comm.tlq_workspace_bytes(D, a.bits_intra, a.bits_inter, a.group),
+                                                    dtype=torch.uint8, device=dev)
 
     def qwd(wmain):
         if a.qwd_two_call:
@@ -479,17 +480,20 @@ def run_sdp4(a, rank, world, local_rank):
                                   "grad_kernel_frac_of_peak":
                                       round(k_bytes / (k_ms * 1e-3) / 1e9 / peak, 4) if k_ms else None}}
         del g32
-    if not a.no_variants and P == 1 and "K345_tlq_local" in prof:
+    ws3_bytes = comm.tlq_workspace_bytes(D, a.bits_intra, a.bits_inter, a.group)
+    if not a.no_variants and P == 1 and "K345_tlq_local" in prof and \
+            torch.cuda.mem_get_info(dev)[0] > ws3_bytes + (2 << 30):
         # the same step through the three kernels K3 -> K4 -> K5 (what every rank of a P > 1 job
-        # runs), with each kernel's roofline
+        # runs), with each kernel's roofline; they need the TLq-HS workspace K345 does without
+        ws3 = torch.empty(ws3_bytes, dtype=torch.uint8, device=dev)
         comm.set_local_fusion(False)
         for _ in range(2):
             qwd(w_main)
-            comm.tlq_hs_reduce_scatter(grad, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
+            comm.tlq_hs_reduce_scatter(grad, out, ws3, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
 
         def step3():
             qwd(w_main)
-            comm.tlq_hs_reduce_scatter(grad, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
+            comm.tlq_hs_reduce_scatter(grad, out, ws3, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
         ms3 = timed(step3, a.steps)
         comm.profile_enable(True)
         comm.profile_read()
@@ -504,6 +508,8 @@ def run_sdp4(a, rank, world, local_rank):
                 kb = kernel_bytes(n, D, S, P, M, N, a)
                 k3k[n] = {"avg_ms": round(avg, 4), "gbs": round(kb / (avg * 1e-3) / 1e9, 1),
                           "frac_of_peak": round(kb / (avg * 1e-3) / 1e9 / peak, 4)}
+        del ws3
+        torch.cuda.empty_cache()
         variants = dict(variants or {})
         variants["three_kernel_tlq"] = {"ms_per_step": round(ms3, 4),
                                         "value": round(P * pre_bytes_rank / (ms3 * 1e-3) / 1e9, 2),

@@ -300,7 +300,10 @@ sdp4_status sdp4_ring_reduce_scatter(sdp4_comm_t comm, const void* grad, sdp4_dt
  * grad: D elements of grad_dtype (fp32 or bf16).  out_shard: fp32[S], shard r.
  * hadamard_block b in {0, 2, 4, ..., 256} with G % b == 0; b = 0 gives
  * TLq; (bits_intra, bits_inter, b) = (4, 4, 0) gives ULq.
- * bits_intra, bits_inter in {4, 8, 32}.  workspace_bytes >= sdp4_tlq_workspace_bytes. */
+ * bits_intra, bits_inter in {4, 8, 32}.  workspace_bytes >= sdp4_tlq_workspace_bytes, except
+ * with the P2P transport (library-owned buffers) and at world size 1 with bits 8 / 4 and the
+ * local fusion on (K3 -> K4 -> K5 as one kernel, sdp4_comm_set_local_fusion), where the
+ * workspace is not used and may be NULL. */
 sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t comm, const void* grad, sdp4_dtype grad_dtype,
                                        size_t numel, int bits_intra, int bits_inter, int group,
                                        int hadamard_block, int average, sdp4_round rnd, uint64_t seed,

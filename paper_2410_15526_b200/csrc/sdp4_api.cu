@@ -1245,14 +1245,16 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
   if ((s = check_ptr(grad, "grad")) != SDP4_OK) return s;
   if ((s = check_ptr(out_shard, "out_shard")) != SDP4_OK) return s;
   const int M = c->M, N = c->N, P = c->world;
-  const size_t need = sdp4_tlq_workspace_bytes(M, N, numel, bits_intra, bits_inter, group);
-  if ((s = check_workspace(c, workspace, workspace_bytes, need)) != SDP4_OK) return s;
-  if ((s = async_check(c)) != SDP4_OK) return s;
-
   const size_t S = numel / P;
-  const size_t es = esize(grad_dtype);
   const auto chunks = plan_chunks(S, c->chunks(S), group);
   const int C = (int)chunks.size();
+  // world 1, bits 8 / 4: one kernel (k_local.cu) that needs no workspace
+  const bool local_fused = P == 1 && c->local_fusion && C == 1 && bits_intra == 8 && bits_inter == 4;
+  const size_t need = sdp4_tlq_workspace_bytes(M, N, numel, bits_intra, bits_inter, group);
+  if (!local_fused && (s = check_workspace(c, workspace, workspace_bytes, need)) != SDP4_OK) return s;
+  if ((s = async_check(c)) != SDP4_OK) return s;
+
+  const size_t es = esize(grad_dtype);
   const bool overlap = C > 1;
   const int sms = c->sms(overlap);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1441,7 +1443,7 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t c, const void* grad, sdp4_dty
     if (C > 1) c->link(c->side, st);
     return SDP4_OK;
   }
-  if (P == 1 && c->local_fusion && C == 1 && bits_intra == 8 && bits_inter == 4) {
+  if (local_fused) {
     // one rank: both all-to-alls are the identity -- K3, K4 and K5 as one kernel (k_local.cu)
     return launch(c, "K345_tlq_local", st, [&] {
       return sdp4::launch_tlq_local(grad, grad_dtype, S, group, b, cb, kappa, sr, key8, key4, out_shard, sms, st);

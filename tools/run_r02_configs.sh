@@ -1,7 +1,8 @@
 # Round-2 BASELINE configs 3-4 and the qWD G=2048 row with the current
 # kernels: GPT-6.7B at 1 GPU and 2x2 / 4x1 / 1x4; GPT-13B at 2 GPUs (2x1, 1x2) and 4 GPUs (2x2)
 # with G in {64, 128, 256}; GPT-1.3B with G in {64, 256} and qWD at G_w = 2048 at 1 and 4 GPUs.
-# (13B at 1 GPU needs ~181 GB of the 179 GB: recorded in DESIGN.md, not run.)
+# GPT-13B at 1 GPU: with the world-1 fused TLq-HS kernel (no 20 GB of 8- / 4-bit workspace)
+# the step needs ~161 GB of the 179 GB.
 mkdir -p gpurun_out/cfg
 R() { n=$1; shift; python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port $((29600 + RANDOM % 300)) "$@"; }
 summ() { python -c "
@@ -15,6 +16,7 @@ one n1_1.3B_G64 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --group 64 --qw
 one n1_1.3B_G256 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --group 256 --qwd-group 256
 one n1_1.3B_Gw2048 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --qwd-group 2048
 one n1_6.7B --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --model 6.7B
+one n1_13B --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-comparators --no-variants --model 13B
 many 4 n4_1.3B_G64 --steps 10 --warmup 3 --no-e2e --group 64 --qwd-group 64
 many 4 n4_1.3B_G256 --steps 10 --warmup 3 --no-e2e --group 256 --qwd-group 256
 many 4 n4_1.3B_Gw2048 --steps 10 --warmup 3 --no-e2e --qwd-group 2048
