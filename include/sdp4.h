@@ -318,10 +318,16 @@ sdp4_status sdp4_tlq_hs_reduce_scatter(sdp4_comm_t comm, const void* grad, sdp4_
  * W(S, bits_intra, G); inter_send / inter_recv = M units W(S, bits_inter, G).
  *   stage_quantize  K3: Alg. 3 l.2-3: grad (D) -> intra_send
  *   stage_reduce    K4: Alg. 3 l.5,7,9 for local rank l: intra_recv -> inter_send
- *   stage_final     K5: Alg. 3 l.11-13: inter_recv -> out_shard (S) */
+ *   stage_final     K5: Alg. 3 l.11-13: inter_recv -> out_shard (S)
+ *   stage_quantize_reduce  K34, one GPU per group (N = 1, bits 8 / 4): Alg. 3 l.2-9 for rank
+ *                   `rank` = node m: grad (D) -> inter_send, unit m' = shard m' (the 8-bit
+ *                   intra units never materialize; sdp4_tlq_hs_reduce_scatter's N = 1 path) */
 sdp4_status sdp4_tlq_stage_quantize(const void* grad, sdp4_dtype grad_dtype, size_t numel, int groups_M,
                                     int group_size_N, int bits_intra, int group, int hadamard_block,
                                     sdp4_round rnd, uint64_t seed, int rank, void* intra_send, void* stream);
+sdp4_status sdp4_tlq_stage_quantize_reduce(const void* grad, sdp4_dtype grad_dtype, size_t numel, int groups_M,
+                                           int group, int hadamard_block, sdp4_round rnd, uint64_t seed, int rank,
+                                           void* inter_send, void* stream);
 sdp4_status sdp4_tlq_stage_reduce(const void* intra_recv, size_t numel, int groups_M, int group_size_N,
                                   int bits_intra, int bits_inter, int group, sdp4_round rnd, uint64_t seed,
                                   int rank, void* inter_send, void* stream);

@@ -66,7 +66,14 @@ __device__ __forceinline__ void quant_dequant_row(float2* p, int t, int lg, floa
     // the code value (exact: magic bits minus the magic constant), zero for a group that is
     // not ok; then rn(code * ds) as K4 / K5 decode it
     const float2 cv = f2add(y, make_float2(-kMagic, -kMagic));
-    p[i] = f2mulz(make_float2(p0.ok ? cv.x : 0.f, p1.ok ? cv.y : 0.f), make_float2(d0, d1), z);
+    if constexpr (STOCH) {
+      p[i] = f2mulz(make_float2(p0.ok ? cv.x : 0.f, p1.ok ? cv.y : 0.f), make_float2(d0, d1), z);
+    } else {
+      // no select needed: a group that is not ok has inv = 0, so cv is +0 for finite
+      // elements and NaN for non-finite ones -- and such a group's d is 0 (tiny) or
+      // non-finite (NaN / Inf max), where code 0 * d gives the same +0 / NaN
+      p[i] = f2mulz(cv, make_float2(d0, d1), z);
+    }
   }
 }
 

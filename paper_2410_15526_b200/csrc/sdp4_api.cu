@@ -1612,6 +1612,28 @@ sdp4_status sdp4_tlq_stage_quantize(const void* grad, sdp4_dtype grad_dtype, siz
   return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "K3 launch failed: %s", cudaGetErrorString(e));
 }
 
+sdp4_status sdp4_tlq_stage_quantize_reduce(const void* grad, sdp4_dtype grad_dtype, size_t numel, int M, int group,
+                                           int hadamard_block, sdp4_round rnd, uint64_t seed, int rank,
+                                           void* inter_send, void* stream) {
+  NvtxRange nvtx_("sdp4_tlq_stage_quantize_reduce");
+  g_err.clear();
+  if (M < 1 || M > sdp4::kMaxDests) return fail(SDP4_EINVAL, "bad groups_M %d", M);
+  if (!valid_round(rnd) || rank < 0 || rank >= M) return fail(SDP4_EINVAL, "bad rounding mode or rank");
+  if (grad_dtype != SDP4_F32 && grad_dtype != SDP4_BF16) return fail(SDP4_EINVAL, "bad grad dtype");
+  sdp4_status s = check_tlq_args(M, numel, 8, 4, group, hadamard_block);
+  if (s != SDP4_OK) return s;
+  if ((s = check_ptr(grad, "grad")) != SDP4_OK) return s;
+  if ((s = check_ptr(inter_send, "inter_send")) != SDP4_OK) return s;
+  const size_t S = numel / M;
+  const size_t w4 = unit_bytes(S, 4, group);
+  uint8_t* units[sdp4::kMaxDests];
+  for (int mp = 0; mp < M; ++mp) units[mp] = static_cast<uint8_t*>(inter_send) + (size_t)mp * w4;
+  cudaError_t e = sdp4::launch_tlq_q84(grad, S, grad_dtype, S, M, group, hadamard_block, hadamard_cb(hadamard_block),
+                                       units, 0ull, rnd == SDP4_STOCHASTIC, sr_key(seed, kStageIntra, rank),
+                                       sr_key(seed, kStageInter, rank), sm_count_current(), static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SDP4_OK : fail(SDP4_ECUDA, "K34 launch failed: %s", cudaGetErrorString(e));
+}
+
 sdp4_status sdp4_tlq_stage_reduce(const void* intra_recv, size_t numel, int M, int N, int bits_intra,
                                   int bits_inter, int group, sdp4_round rnd, uint64_t seed, int rank,
                                   void* inter_send, void* stream) {

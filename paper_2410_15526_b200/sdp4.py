@@ -62,6 +62,7 @@ SIGNATURES = {
     "sdp4_tlq_hs_reduce_scatter": (_ci, [_vp, _vp, _ci, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _u64, _vp, _vp,
                                          _c_size, _vp]),
     "sdp4_tlq_stage_quantize": (_ci, [_vp, _ci, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _u64, _ci, _vp, _vp]),
+    "sdp4_tlq_stage_quantize_reduce": (_ci, [_vp, _ci, _c_size, _ci, _ci, _ci, _ci, _u64, _ci, _vp, _vp]),
     "sdp4_tlq_stage_reduce": (_ci, [_vp, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _u64, _ci, _vp, _vp]),
     "sdp4_tlq_stage_final": (_ci, [_vp, _c_size, _ci, _ci, _ci, _ci, _ci, _ci, _vp, _vp]),
     "sdp4_emu_qwd_workspace_bytes": (_c_size, [_ci, _c_size, _ci, _ci]),
@@ -161,6 +162,15 @@ def tlq_stage_reduce(intra_recv: torch.Tensor, inter_send: torch.Tensor, numel: 
     _check(lib().sdp4_tlq_stage_reduce(_ptr(intra_recv), numel, M, N, bits_intra, bits_inter, group,
                                        RNE if seed is None else STOCHASTIC, seed or 0, rank, _ptr(inter_send),
                                        _stream(stream)))
+
+
+def tlq_stage_quantize_reduce(grad: torch.Tensor, inter_send: torch.Tensor, M: int, group: int = 128,
+                              hadamard_block: int = 64, seed=None, rank: int = 0, stream=None):
+    """K34 alone (one GPU per group, N = 1, bits 8 / 4): Alg. 3 l.2-9 for node `rank`,
+    no communication -- every 4-bit unit into inter_send (M units)."""
+    _check(lib().sdp4_tlq_stage_quantize_reduce(_ptr(grad), _DT[grad.dtype], grad.numel(), M, group, hadamard_block,
+                                                RNE if seed is None else STOCHASTIC, seed or 0, rank,
+                                                _ptr(inter_send), _stream(stream)))
 
 
 def tlq_stage_final(inter_recv: torch.Tensor, out_shard: torch.Tensor, numel: int, M: int, N: int,

@@ -96,3 +96,41 @@ def test_multirank_matches_exact_mean_within_quantization_error():
     exact = oracle.exact_reduce_scatter_f64([g.numpy() for g in grads], P)
     rel = np.linalg.norm(np.concatenate(outs) - np.concatenate(exact)) / np.linalg.norm(np.concatenate(exact))
     assert rel < 0.2
+
+
+K34_CASES = [  # (M, G, b, dtype, seed): one GPU per group (N = 1), K3 + K4 fused
+    (2, 128, 64, torch.bfloat16, None),
+    (3, 64, 16, torch.float32, None),
+    (4, 32, 32, torch.bfloat16, None),
+    (8, 2048, 256, torch.bfloat16, None),
+    (2, 256, 0, torch.float32, None),
+    (4, 128, 64, torch.bfloat16, 2410),
+]
+
+
+@pytest.mark.parametrize("M,G,b,dtype,seed", K34_CASES)
+def test_k34_units_emulated(M, G, b, dtype, seed):
+    """K34 (sdp4_tlq_stage_quantize_reduce) on every node of an emulated M x 1 job: its 4-bit
+    inter units equal the oracle's messages of Alg. 3 l.10 bit for bit (the 8-bit intra units
+    it dequantizes in registers are the oracle's intra messages by construction)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2410_15526_b200 import tlq_stage_quantize_reduce
+    P = M
+    align = P * max(G, 64)
+    D = ((16384 * P * 2 + 64 * 37 * P) // align + 1) * align
+    grads = [synth.gradient(D, seed=synth.seed_for(r, 5), dtype=dtype) for r in range(P)]
+    e = synth.edge_case_groups(G)[:D // P].to(dtype)
+    grads[0][:e.numel()] = e
+    S = D // P
+    w4 = wire_unit_bytes(S, 4, G)
+    tr = oracle.tlq_hs_reduce_scatter([g.float().numpy() for g in grads], oracle.Topology(M, 1), G, b, 8, 4, True,
+                                      seed=seed)
+    for r in range(P):
+        buf = torch.zeros(M * w4, dtype=torch.uint8, device="cuda")
+        tlq_stage_quantize_reduce(grads[r].cuda(), buf, M, G, b, seed=seed, rank=r)
+        torch.cuda.synchronize()
+        got = buf.cpu().numpy()
+        for mp in range(M):
+            c, s = tr.inter_send[r][mp]
+            assert_unit_equal(got[mp * w4:(mp + 1) * w4], c, s, 4, G, S, f"K34 rank {r} inter unit {mp}")
