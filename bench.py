@@ -310,6 +310,12 @@ def run_sdp4(a, rank, world, local_rank):
         ws_q = torch.empty(comm.qwd_workspace_bytes(D, a.bits_w, a.qwd_group), dtype=torch.uint8, device=dev)
         ws_t = None if local_fused else torch.empty(comm.tlq_workspace_bytes(D, a.bits_intra, a.bits_inter, a.group),
                                                     dtype=torch.uint8, device=dev)
+    # the three-kernel variant's TLq-HS workspace (world 1), allocated with the inputs -- not
+    # after the other measurements have fragmented the allocator -- when it fits
+    ws3_bytes = comm.tlq_workspace_bytes(D, a.bits_intra, a.bits_inter, a.group)
+    ws3 = None
+    if local_fused and not a.no_variants and torch.cuda.mem_get_info(dev)[0] > ws3_bytes + (8 << 30):
+        ws3 = torch.empty(ws3_bytes, dtype=torch.uint8, device=dev)
 
     def qwd(wmain):
         if a.qwd_two_call:
@@ -448,44 +454,10 @@ def run_sdp4(a, rank, world, local_rank):
                              "nvlink_GBps": round(nv / (t * 1e-3) / 1e9, 1) if nv else None,
                              "nvlink_frac_of_900": round(nv / (t * 1e-3) / 900e9, 4) if nv else None}
 
-    # the paper's FP32-gradient setting (P:502, P:680): the same step with fp32 gradients
-    variants, t_tlq32 = None, None
-    if not a.no_variants and gdt == torch.bfloat16:
-        g32 = grad.float()
-
-        def step32():
-            qwd(w_main)
-            comm.tlq_hs_reduce_scatter(g32, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
-        for _ in range(2):
-            step32()
-        ms32 = timed(step32, a.steps)
-        comm.profile_enable(True)
-        comm.profile_read()
-        timed(step32, a.steps)
-        prof32 = comm.profile_read()
-        comm.profile_enable(False)
-        t_tlq32 = timed(lambda: comm.tlq_hs_reduce_scatter(g32, out, ws_t, a.bits_intra, a.bits_inter, a.group,
-                                                           a.hadamard, True), a.steps)
-        a32 = argparse.Namespace(**dict(vars(a), grad_dtype="fp32"))
-        # the kernel that reads the gradient: K3, or at world 1 the fused K345
-        tk = "K345_tlq_local" if "K345_tlq_local" in prof32 else "K3_tlq_had_quant"
-        k_t, k_c = prof32.get(tk, (0.0, 0))
-        k_ms = k_t / max(1, k_c)
-        k_bytes = kernel_bytes(tk, D, S, P, M, N, a32)
-        variants = {"fp32_grad": {"ms_per_step": round(ms32, 4),
-                                  "value": round(P * D * (4 + 4) / (ms32 * 1e-3) / 1e9, 2), "unit": "GB/s",
-                                  "tlq_hs_reduce_scatter_ms": round(t_tlq32, 4),
-                                  "grad_kernel": tk, "grad_kernel_avg_ms": round(k_ms, 4),
-                                  "grad_kernel_gbs": round(k_bytes / (k_ms * 1e-3) / 1e9, 1) if k_ms else None,
-                                  "grad_kernel_frac_of_peak":
-                                      round(k_bytes / (k_ms * 1e-3) / 1e9 / peak, 4) if k_ms else None}}
-        del g32
-    ws3_bytes = comm.tlq_workspace_bytes(D, a.bits_intra, a.bits_inter, a.group)
-    if not a.no_variants and P == 1 and "K345_tlq_local" in prof and \
-            torch.cuda.mem_get_info(dev)[0] > ws3_bytes + (2 << 30):
+    variants = None
+    if ws3 is not None and "K345_tlq_local" in prof:
         # the same step through the three kernels K3 -> K4 -> K5 (what every rank of a P > 1 job
         # runs), with each kernel's roofline; they need the TLq-HS workspace K345 does without
-        ws3 = torch.empty(ws3_bytes, dtype=torch.uint8, device=dev)
         comm.set_local_fusion(False)
         for _ in range(2):
             qwd(w_main)
@@ -508,13 +480,46 @@ def run_sdp4(a, rank, world, local_rank):
                 kb = kernel_bytes(n, D, S, P, M, N, a)
                 k3k[n] = {"avg_ms": round(avg, 4), "gbs": round(kb / (avg * 1e-3) / 1e9, 1),
                           "frac_of_peak": round(kb / (avg * 1e-3) / 1e9 / peak, 4)}
-        del ws3
-        torch.cuda.empty_cache()
         variants = dict(variants or {})
         variants["three_kernel_tlq"] = {"ms_per_step": round(ms3, 4),
                                         "value": round(P * pre_bytes_rank / (ms3 * 1e-3) / 1e9, 2),
                                         "unit": "GB/s", "kernels": k3k}
+    ws3 = None
+    torch.cuda.empty_cache()
 
+    # the paper's FP32-gradient setting (P:502, P:680): the same step with fp32 gradients
+    t_tlq32 = None
+    if not a.no_variants and gdt == torch.bfloat16:
+        g32 = grad.float()
+
+        def step32():
+            qwd(w_main)
+            comm.tlq_hs_reduce_scatter(g32, out, ws_t, a.bits_intra, a.bits_inter, a.group, a.hadamard, True)
+        for _ in range(2):
+            step32()
+        ms32 = timed(step32, a.steps)
+        comm.profile_enable(True)
+        comm.profile_read()
+        timed(step32, a.steps)
+        prof32 = comm.profile_read()
+        comm.profile_enable(False)
+        t_tlq32 = timed(lambda: comm.tlq_hs_reduce_scatter(g32, out, ws_t, a.bits_intra, a.bits_inter, a.group,
+                                                           a.hadamard, True), a.steps)
+        a32 = argparse.Namespace(**dict(vars(a), grad_dtype="fp32"))
+        # the kernel that reads the gradient: K3, or at world 1 the fused K345
+        tk = "K345_tlq_local" if "K345_tlq_local" in prof32 else "K3_tlq_had_quant"
+        k_t, k_c = prof32.get(tk, (0.0, 0))
+        k_ms = k_t / max(1, k_c)
+        k_bytes = kernel_bytes(tk, D, S, P, M, N, a32)
+        variants = dict(variants or {})
+        variants["fp32_grad"] = {"ms_per_step": round(ms32, 4),
+                                  "value": round(P * D * (4 + 4) / (ms32 * 1e-3) / 1e9, 2), "unit": "GB/s",
+                                  "tlq_hs_reduce_scatter_ms": round(t_tlq32, 4),
+                                  "grad_kernel": tk, "grad_kernel_avg_ms": round(k_ms, 4),
+                                  "grad_kernel_gbs": round(k_bytes / (k_ms * 1e-3) / 1e9, 1) if k_ms else None,
+                                  "grad_kernel_frac_of_peak":
+                                      round(k_bytes / (k_ms * 1e-3) / 1e9 / peak, 4) if k_ms else None}
+        del g32
     # ablation (NEXT-3): TLq-HS with the Hadamard transforms as separate passes ("SDP4Bit (HS
     # w/o fused)") -- K3 identity codec forward pass, the b = 0 reduce-scatter, K5
     # identity codec inverse pass -- against the fused path
