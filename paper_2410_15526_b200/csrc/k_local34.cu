@@ -34,9 +34,15 @@ struct Q4Out {
   uint64_t remote;           // bit m': peer memory
 };
 
+// The 8-bit step's dequantization steps d and whether both of the row's groups are ok.
+struct DQ8 {
+  float d0, d1;
+  bool ok;
+};
+
 // quant_dequant_row (k_local.cu): the row quantized at BITS and replaced by its dequantization
 template <int BITS, bool STOCH>
-__device__ __forceinline__ void quant_dequant_row34(float2* p, int lg, float c, const SR& sr, uint64_t i0, float z) {
+__device__ __forceinline__ DQ8 quant_dequant_row34(float2* p, int lg, float c, const SR& sr, uint64_t i0, float z) {
   constexpr float q = float((1 << (BITS - 1)) - 1);
   const float rq_ = __fdiv_rn(1.f, q);
   float a0 = 0.f, a1 = 0.f;
@@ -78,26 +84,41 @@ __device__ __forceinline__ void quant_dequant_row34(float2* p, int lg, float c, 
       p[i] = f2mulz(cv, make_float2(d0, d1), z);
     }
   }
+  return DQ8{d0, d1, p0.ok && p1.ok};
 }
 
 // K4's 4-bit requantization of a row held as pairs (quant_row<4>'s arithmetic: group max,
 // qparam, RNE / stochastic codes, stored scale rn(s * 1)) with K4's packing: biased magic
 // bits (kMagicB4) and pack4x8_b (4 ALU instructions per 8 codes instead of pack4x8's 11).
 // Codes of the row at out_tile + t * 32 (linear), scales as quant_row places them.
+//
+// The 4-bit group is the 8-bit group (one G), so when that group was ok its max |x| is known
+// without a pass over the row: the element of max |u| got code +-127 (|u| * rn(127/|u|) =
+// 127 (1 + d), |d| <= 2^-24, rounds to 127), every |x| = rn(|code| * d8) is monotone in |code|,
+// so max |x| = rn(127 * d8) -- bit for bit the max the pass would find.  Nearest rounding
+// only (a stochastic code of the max element can be 126); a warp with any group not ok (zero,
+// tiny, Inf, NaN: the ragged tail or edge groups) takes the pass.
 template <bool STOCH>
 __device__ __forceinline__ void quant_row4_b(const float2* p, int t, int lg, bool act, uint8_t* out_tile,
-                                             float* scales_tile, const SR& sr, uint64_t i0, uint32_t m16) {
+                                             float* scales_tile, const SR& sr, uint64_t i0, uint32_t m16,
+                                             const DQ8& r8) {
   constexpr float q = 7.f;
   float a0 = 0.f, a1 = 0.f;
+  const bool known = !STOCH && __all_sync(0xffffffffu, r8.ok);
+  if (known) {
+    a0 = __fmul_rn(127.f, r8.d0);
+    a1 = __fmul_rn(127.f, r8.d1);
+  } else {
 #pragma unroll
-  for (int i = 0; i < 32; i += 2) {
-    a0 = max3_abs_nan(a0, p[i].x, p[i + 1].x);
-    a1 = max3_abs_nan(a1, p[i].y, p[i + 1].y);
+    for (int i = 0; i < 32; i += 2) {
+      a0 = max3_abs_nan(a0, p[i].x, p[i + 1].x);
+      a1 = max3_abs_nan(a1, p[i].y, p[i + 1].y);
+    }
   }
   QP p0, p1;
   if (lg >= 6) {
-    a0 = max_nan(a0, a1);
-    const int rpg = 1 << (lg - 6);
+    const int rpg = known ? 1 : 1 << (lg - 6);
+    if (!known) a0 = max_nan(a0, a1);
     for (int off = 1; off < rpg; off <<= 1) a0 = max_nan(a0, __shfl_xor_sync(0xffffffffu, a0, off));
     p0 = qparam(a0, q);
     p1 = p0;
@@ -221,14 +242,14 @@ __global__ void __launch_bounds__(kQBlock, QCfg<IN_R>::CTAS)
     }
     const uint64_t i0 = (uint64_t)j * S + (uint64_t)row * kRowElems;  // global index (shard j, R14)
     fwht_pairs<B>(p);                                      // K3: H (unnormalized)
-    quant_dequant_row34<8, STOCH>(p, lg, cb, sr8, i0, z);  // K3: Q8; K4: DQ8 of the one source
+    const DQ8 r8 = quant_dequant_row34<8, STOCH>(p, lg, cb, sr8, i0, z);  // K3: Q8; K4: DQ8 of the one source
     // K4: requantize at 4 bits into the warp's linear output tile (K3's quantizer with c = 1:
     // the same codes and scales as K4's requantization), then to the destination unit
     uint8_t* ot = ob0 + (i % C::OB) * C::OUT_W;
     float* osc = reinterpret_cast<float*>(ot + 32 * kQOutR);
     if (lane == 0) bulk_wait_read<C::OB - 1>();  // this warp's store of tile i - OB has left ot
     __syncwarp();
-    quant_row4_b<STOCH>(p, lane, lg, act, ot, osc, sr4, i0, m16);
+    quant_row4_b<STOCH>(p, lane, lg, act, ot, osc, sr4, i0, m16, r8);
     fence_proxy_async();
     __syncwarp();
     const uint32_t wrow0 = ts * kTileRows + 32 * warp;
