@@ -117,9 +117,11 @@ __device__ __forceinline__ void quant_row4_b(const float2* p, int t, int lg, boo
   }
   QP p0, p1;
   if (lg >= 6) {
-    const int rpg = known ? 1 : 1 << (lg - 6);
-    if (!known) a0 = max_nan(a0, a1);
-    for (int off = 1; off < rpg; off <<= 1) a0 = max_nan(a0, __shfl_xor_sync(0xffffffffu, a0, off));
+    const int rpg = 1 << (lg - 6);
+    if (!known) {
+      a0 = max_nan(a0, a1);
+      for (int off = 1; off < rpg; off <<= 1) a0 = max_nan(a0, __shfl_xor_sync(0xffffffffu, a0, off));
+    }
     p0 = qparam(a0, q);
     p1 = p0;
     if (act && (t & (rpg - 1)) == 0) scales_tile[t >> (lg - 6)] = stored_scale(a0, 1.f);

@@ -134,3 +134,40 @@ def test_k34_units_emulated(M, G, b, dtype, seed):
         for mp in range(M):
             c, s = tr.inter_send[r][mp]
             assert_unit_equal(got[mp * w4:(mp + 1) * w4], c, s, 4, G, S, f"K34 rank {r} inter unit {mp}")
+
+
+@pytest.mark.parametrize("M,G,b,dtype", [(2, 128, 64, torch.bfloat16), (3, 32, 0, torch.float32),
+                                          (2, 256, 16, torch.float32), (4, 64, 64, torch.bfloat16)])
+def test_k34_code_map_tiny_inter_groups(M, G, b, dtype):
+    """K34's shortcut for ok 8-bit groups (the 4-bit group max taken as rn(127 * d8) instead
+    of a pass over the row, k_local34.cu) on groups whose 8-bit scale is ok but whose 4-bit max
+    lands at or below 2^-120 (a zero group at 4 bits, R2): every third group of every rank is scaled
+    to a max in [2^-120, 2^-116] (incl. 2^-120 and one ulp above), all other groups are plain gaussian, so whole warps take the
+    shortcut.  Inter units bit-exact against the oracle (R2, R3, R5)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2410_15526_b200 import tlq_stage_quantize_reduce
+    P = M
+    align = P * max(G, 64)
+    D = ((16384 * P * 2 + 64 * 37 * P) // align + 1) * align
+    grads = []
+    for r in range(P):
+        g = synth.gradient(D, seed=synth.seed_for(r, 6), dtype=torch.float32).view(-1, G).clone()
+        gen = torch.Generator().manual_seed(100 + r)
+        sel = torch.arange(0, g.shape[0], 3)
+        tgt = torch.exp2(torch.empty(sel.numel()).uniform_(-120.0, -116.0, generator=gen))
+        tgt[::7] = 2.0 ** -120                      # the R2 boundary itself, and one ulp above
+        tgt[1::7] = 2.0 ** -120 * (1 + 2.0 ** -23)
+        g[sel] = g[sel] / g[sel].abs().amax(dim=1, keepdim=True) * tgt[:, None]
+        grads.append(g.reshape(-1).to(dtype))
+    S = D // P
+    w4 = wire_unit_bytes(S, 4, G)
+    tr = oracle.tlq_hs_reduce_scatter([g.float().numpy() for g in grads], oracle.Topology(M, 1), G, b, 8, 4, True)
+    for r in range(P):
+        buf = torch.zeros(M * w4, dtype=torch.uint8, device="cuda")
+        tlq_stage_quantize_reduce(grads[r].cuda(), buf, M, G, b, rank=r)
+        torch.cuda.synchronize()
+        got = buf.cpu().numpy()
+        for mp in range(M):
+            c, s = tr.inter_send[r][mp]
+            assert_unit_equal(got[mp * w4:(mp + 1) * w4], c, s, 4, G, S, f"K34 rank {r} inter unit {mp}")
