@@ -29,22 +29,39 @@ struct LCfg {
 // max, qparam, RNE or stochastic codes, stored scale rn(s * c)) and replace it by what the
 // consumer of the wire unit decodes: code * div_by_q(stored scale, q) (K4's / K5's
 // dequantization; zero codes for groups that are not ok).  i0: stochastic index of element 0.
+//
+// `known` (the 4-bit step after the 8-bit one, nearest rounding, every group of the warp ok at
+// 8 bits): the group max is rn(127 * d8) without a pass over the row -- the 8-bit code of the
+// max element is +-127 and |rn(c8 * d8)| is monotone in |c8| (K34's argument, k_local34.cu,
+// DESIGN.md sec. 7).
+struct DQR {
+  float d0, d1;
+  bool ok;
+};
 template <int BITS, bool STOCH>
-__device__ __forceinline__ void quant_dequant_row(float2* p, int t, int lg, float c, const SR& sr, uint64_t i0,
-                                                  float z) {
+__device__ __forceinline__ DQR quant_dequant_row(float2* p, int t, int lg, float c, const SR& sr, uint64_t i0,
+                                                 float z, const DQR* known = nullptr) {
   constexpr float q = float((1 << (BITS - 1)) - 1);
   const float rq_ = __fdiv_rn(1.f, q);
   float a0 = 0.f, a1 = 0.f;
+  const bool kn = !STOCH && known && __all_sync(0xffffffffu, known->ok);
+  if (kn) {
+    a0 = __fmul_rn(127.f, known->d0);
+    a1 = __fmul_rn(127.f, known->d1);
+  } else {
 #pragma unroll
-  for (int i = 0; i < 32; i += 2) {
-    a0 = max3_abs_nan(a0, p[i].x, p[i + 1].x);
-    a1 = max3_abs_nan(a1, p[i].y, p[i + 1].y);
+    for (int i = 0; i < 32; i += 2) {
+      a0 = max3_abs_nan(a0, p[i].x, p[i + 1].x);
+      a1 = max3_abs_nan(a1, p[i].y, p[i + 1].y);
+    }
   }
   QP p0, p1;
   if (lg >= 6) {  // a group spans G/64 rows (lanes)
-    a0 = max_nan(a0, a1);
-    const int rpg = 1 << (lg - 6);
-    for (int off = 1; off < rpg; off <<= 1) a0 = max_nan(a0, __shfl_xor_sync(0xffffffffu, a0, off));
+    if (!kn) {
+      a0 = max_nan(a0, a1);
+      const int rpg = 1 << (lg - 6);
+      for (int off = 1; off < rpg; off <<= 1) a0 = max_nan(a0, __shfl_xor_sync(0xffffffffu, a0, off));
+    }
     a1 = a0;
     p0 = qparam(a0, q);
     p1 = p0;
@@ -75,6 +92,7 @@ __device__ __forceinline__ void quant_dequant_row(float2* p, int t, int lg, floa
       p[i] = f2mulz(cv, make_float2(d0, d1), z);
     }
   }
+  return DQR{d0, d1, p0.ok && p1.ok};
 }
 
 template <int IN_R, int B, bool STOCH>
@@ -166,8 +184,8 @@ __global__ void __launch_bounds__(kLBlock, 1)
     }
     const uint64_t i0 = (uint64_t)row * kRowElems;  // stochastic index of the row (shard 0 = the buffer)
     fwht_pairs<B>(p);                                           // K3: H (unnormalized)
-    quant_dequant_row<8, STOCH>(p, t, lg, cb, sr8, i0, z);      // K3: Q8 (scale * c_b); K4: DQ8 (N = 1)
-    quant_dequant_row<4, STOCH>(p, t, lg, 1.f, sr4, i0, z);     // K4: Q4; K5: DQ4 (M = 1)
+    const DQR r8 = quant_dequant_row<8, STOCH>(p, t, lg, cb, sr8, i0, z);  // K3: Q8 (scale * c_b); K4: DQ8 (N = 1)
+    quant_dequant_row<4, STOCH>(p, t, lg, 1.f, sr4, i0, z, &r8);            // K4: Q4; K5: DQ4 (M = 1)
     fwht_pairs<B>(p);                                           // K5: H after the reduction
     const float2 kk = make_float2(kappa, kappa);
 #pragma unroll

@@ -173,6 +173,22 @@ def test_tlq_bf16_extremes(comm):
     check_tlq(comm, g.to(torch.bfloat16), 8, 4, 128, 0)
 
 
+@pytest.mark.parametrize("G,b,dtype", [(128, 64, torch.bfloat16), (32, 0, torch.float32), (256, 16, torch.float32)])
+def test_tlq_tiny_inter_groups(comm, G, b, dtype):
+    """The world-1 kernel's known 4-bit max (rn(127 * d8), k_local.cu) on groups that are ok at
+    8 bits but zero groups at 4 bits (max at or below 2^-120, R2): every third group scaled to a
+    max in [2^-120, 2^-116] (incl. 2^-120 and one ulp above), the rest plain gaussian."""
+    D = 16384 * 2 + max(G, 64) * 9
+    g = synth.gradient(D, seed=77 + G, dtype=torch.float32).view(-1, G).clone()
+    gen = torch.Generator().manual_seed(200 + G)
+    sel = torch.arange(0, g.shape[0], 3)
+    tgt = torch.exp2(torch.empty(sel.numel()).uniform_(-120.0, -116.0, generator=gen))
+    tgt[::7] = 2.0 ** -120
+    tgt[1::7] = 2.0 ** -120 * (1 + 2.0 ** -23)
+    g[sel] = g[sel] / g[sel].abs().amax(dim=1, keepdim=True) * tgt[:, None]
+    check_tlq(comm, g.reshape(-1).to(dtype), 8, 4, G, b)
+
+
 def test_repeatability(comm):
     # R16: bit-identical across repeated runs
     grad = synth.gradient(16384 * 4, seed=1234, dtype=torch.bfloat16)
